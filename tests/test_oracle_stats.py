@@ -1,0 +1,89 @@
+"""Pins for oracle step O10 (statistics) and statistical pins of the full run.
+
+  * SPEC.md:377 worked example of the paper's error formula;
+  * unbiasedness: every construction / conditioning mode of QMC-CPW and the
+    LR+MC baseline estimate the same Greeks (within 4.5 combined SE);
+  * VRF magnitudes printed by the paper (Tables 1-3) for QMC-CPW
+    and QMC+BB-CPW at the paper's P = 2^15, d = 64, K = 100.  The paper's
+    randomisation and L = 500 runs are unknown (reading 10), so the pin is an
+    order-of-magnitude band (x/20).  It catches the printed lookback-vega
+    1/d (reading 3), which moves that VRF by ~10^3.
+"""
+import math
+
+import numpy as np
+import pytest
+
+
+def test_spec_error_formula_example(O):
+    # runs (1,2,3,4) -> C = 2.5, sigma = sqrt(1.25) (divisor L)
+    m, se, sg = O.summarize([1.0, 2.0, 3.0, 4.0])
+    assert m == 2.5 and abs(sg - math.sqrt(1.25)) < 1e-15
+    assert abs(se - math.sqrt(5.0 / 12.0)) < 1e-15   # sqrt(sum dev^2 / (L (L-1)))
+    m, se, sg = O.summarize([3.0])
+    assert m == 3.0 and math.isnan(se) and math.isnan(sg)
+
+
+def test_run_statistics_consistent_with_replicate_means(O):
+    mk = O.market(d=4)
+    res, rm = O.price_greeks([(0, 100.0), (1, 100.0)], mk, 1024, 8, O.config(construction=1),
+                             want_rep_means=True)
+    for o in range(2):
+        for q in range(4):
+            m, se, sg = O.summarize(rm[:, o, q])
+            assert res[o]["mean"][q] == m and res[o]["se"][q] == se and res[o]["sigma_run"][q] == sg
+
+
+def test_thread_count_does_not_change_bits(O):
+    mk = O.market(d=8)
+    a, _ = O.price_greeks([(2, 95.0)], mk, 512, 6, O.config(construction=2), n_threads=1)
+    b, _ = O.price_greeks([(2, 95.0)], mk, 512, 6, O.config(construction=2), n_threads=5)
+    assert all(np.array_equal(a[0][k], b[0][k]) for k in ("mean", "se", "sigma_run", "within_var"))
+
+
+def _agree(r1, r2, n_se=4.5):
+    for q in range(4):
+        diff = abs(r1["mean"][q] - r2["mean"][q])
+        comb = math.hypot(r1["se"][q], r2["se"][q])
+        assert diff <= n_se * comb + 1e-12 * abs(r1["mean"][q]), (q, r1["mean"][q], r2["mean"][q], comb)
+
+
+@pytest.mark.slow
+def test_all_modes_estimate_the_same_greeks(O):
+    d, N, L = 16, 1 << 12, 16
+    mk = O.market(d=d)
+    opts = [(0, 100.0), (1, 100.0), (2, 100.0)]
+    lr, _ = O.price_greeks(opts, mk, 1 << 14, 32, O.config(method=1, construction=0))
+    runs = {}
+    for constr in (0, 1, 2):
+        runs[(constr, 0)] = O.price_greeks(opts, mk, N, L, O.config(construction=constr))[0]
+    runs[(2, 1)] = O.price_greeks(opts[:2], mk, N, L, O.config(construction=2, conditioning=1))[0]
+    for key, res in runs.items():
+        for o in range(len(res)):
+            _agree(res[o], lr[o])
+            _agree(res[o], runs[(1, 0)][o])
+
+
+PAPER_VRF_K100_D64 = {
+    # (option, method) -> (delta, vega, gamma); Table 1,
+    # Table 2, Table 3
+    (0, "QMC-CPW"): (903, 7770, 5427), (0, "QMC+BB-CPW"): (52689, 376285, 75020),
+    (1, "QMC-CPW"): (58, 1176, 126), (1, "QMC+BB-CPW"): (830, 12571, 784),
+    (2, "QMC-CPW"): (21857, 6580, 89333), (2, "QMC+BB-CPW"): (40682, 35370, 212928),
+}
+
+
+@pytest.mark.slow
+def test_vrf_magnitudes_match_paper_tables(O):
+    d, P, L = 64, 1 << 15, 24
+    mk = O.market(d=d)
+    opts = [(0, 100.0), (1, 100.0), (2, 100.0)]
+    lr, _ = O.price_greeks(opts, mk, P, L, O.config(method=1, construction=0))
+    qmc, _ = O.price_greeks(opts, mk, P, L, O.config(construction=0))
+    bb, _ = O.price_greeks(opts, mk, P, L, O.config(construction=1))
+    for o in range(3):
+        for name, res in (("QMC-CPW", qmc), ("QMC+BB-CPW", bb)):
+            for i, q in enumerate((1, 2, 3)):
+                vrf = (lr[o]["sigma_run"][q] / res[o]["sigma_run"][q]) ** 2
+                paper = PAPER_VRF_K100_D64[(o, name)][i]
+                assert paper / 20 <= vrf <= paper * 20, (o, name, q, vrf, paper)
