@@ -1,0 +1,320 @@
+#!/usr/bin/env python
+"""bench.py -- QMC paths/s with price+delta+vega+gamma (d=64) on 1..8 B200.
+
+Contract (task statement + BASELINE.json):
+  python bench.py --gpus N --steps K --warmup W            (N > 1 under torchrun)
+  python bench.py --impl reference ...                     (the oracle on host cores)
+prints ONE JSON line on rank 0.
+
+Workload: BASELINE.json configs[3] = SURVEY.md C4 -- arithmetic Asian, binary
+Asian and lookback calls fused on the same paths, S0 = K = 100, sigma = 0.2,
+r = 0.1, T = 1, d = 64, Brownian bridge + W(t_1) conditioning (the paper's
+QMC+BB-CPW), 2^20 Sobol' points x 64 randomisations PER GPU (weak scaling: N
+GPUs price 64 N replicates; rank g owns replicates [64 g, 64 g + 64)).
+
+A step = one full estimator run: randomisation tables, the fused path kernel
+over every cell, per-replicate reduction, one NCCL all-reduce (N > 1), the
+device->host read of the replicate sums and the host finalize.  value =
+underlying QMC paths (points x replicates, each delivering the 4 outputs of
+all 3 options) per second over all ranks, timed with CUDA events on the
+launching stream, max over ranks; L2 is flushed (256 MiB write) before every
+timed step, outside the events.
+"""
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import workloads as W  # noqa: E402
+
+METRIC = "QMC paths/sec with price+delta+vega+gamma (d=64) at 1/2/4/8 B200; % FP64 roof"
+UNIT = "paths/s"
+SM_COUNT = 148
+FP64_LANES_PER_SM = 64          # FP64 FMA lanes per SM per clock (B200)
+SM_MAX_MHZ_FALLBACK = 1965.0    # B200_PROFILING.md / MEASURED_PEAKS.json sm_max_mhz
+
+
+def fp64_model_per_path(d, constr, cond, n_opt, arith_x1=0):
+    """Algorithmic FP64 lane-instructions per underlying path (SURVEY.md 8(d)
+    planning model, fixed constants -- independent of how the kernel is written):
+    c_icdf = 50 (branch-light FP64 inverse normal), c_exp = 17, c_tail = 160
+    per option (log + 2 erfc + exp + ~30 FMA), c_W = 1 (STD) / 2 (BB) / d (PCA)."""
+    c_icdf, c_exp, c_tail = 50, 17, 160
+    c_w = {0: 1, 1: 2, 2: d}[constr]
+    d_icdf = d - 1 if (cond == 1 or constr == 0) else d
+    if cond == 0:
+        return d_icdf * c_icdf + d * (c_exp + c_w + 6) + n_opt * c_tail
+    newton = 4 * d * (c_exp + 3)
+    return d_icdf * c_icdf + d * c_w + n_opt * (newton + d * (c_exp + 3) + c_tail) + arith_x1 * d * (c_exp + 60 + 4)
+
+
+def measured_peaks():
+    try:
+        return json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    except Exception:
+        return {}
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index):
+        self.gpu = gpu_index
+        self.samples = []
+        self._stop = threading.Event()
+        self._th = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.FIELDS}",
+                                      "--format=csv,noheader,nounits"], capture_output=True, text=True,
+                                     timeout=5).stdout.strip()
+                if out:
+                    self.samples.append([x.strip() for x in out.split(",")])
+            except Exception:
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self._th = threading.Thread(target=self._run, daemon=True)
+        self._th.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        self._th.join(timeout=10)
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"], "samples": 0}
+        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for s in self.samples for i in range(4) if len(s) > 2 + i and
+                          s[2 + i].lower().startswith("active")})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.samples)}
+
+
+def cpu_baseline_oracle(options, d, constr, cond, budget_s=12.0):
+    """The oracle (plain C, never tuned) on this host's cores, on a bounded
+    sample of the same workload: replicates 0..R-1 x the first n points."""
+    import oracle as O
+    cores = os.cpu_count() or 1
+    opts = [(t, 100.0) for t in options]
+    mk = O.market(W.S0, W.R, W.SIGMA, W.T, d)
+    cfg = O.config(construction=constr, conditioning=cond, seed=W.SEED)
+    reps = max(1, min(64, cores))
+    t0 = time.perf_counter()
+    O.price_greeks(opts, mk, 256, reps, cfg, n_threads=cores)
+    pilot = (time.perf_counter() - t0) / (256 * reps)
+    n = int(max(256, min(1 << 20, budget_s / max(pilot, 1e-9) / reps)))
+    t0 = time.perf_counter()
+    O.price_greeks(opts, mk, n, reps, cfg, n_threads=cores)
+    dt = time.perf_counter() - t0
+    return {"value": n * reps / dt, "unit": UNIT, "cores": min(cores, reps), "kind": "oracle",
+            "sample": f"C4 replicates 0..{reps - 1} x first {n} Sobol' points, {len(options)} options fused, "
+                      f"d={d}, {dt:.1f} s wall on {min(cores, reps)} threads"}
+
+
+def run_reference(args):
+    """--impl reference: the oracle as it stands, on the host cores, same metric/config."""
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    import oracle as O
+    c = W.CONFIGS[W.HEADLINE]
+    options, d = c["options"], c["d"]
+    cores = os.cpu_count() or 1
+    reps = max(1, min(64, cores))
+    opts = [(t, 100.0) for t in options]
+    mk = O.market(W.S0, W.R, W.SIGMA, W.T, d)
+    cfg = O.config(construction=W.BB, conditioning=W.W1, seed=W.SEED)
+    n = 4096
+    for _ in range(args.warmup):
+        O.price_greeks(opts, mk, 512, reps, cfg, n_threads=cores)
+    times = []
+    for _ in range(args.steps):
+        t0 = time.perf_counter()
+        O.price_greeks(opts, mk, n, reps, cfg, n_threads=cores)
+        times.append(time.perf_counter() - t0)
+    tot = sum(times)
+    value = n * reps * args.steps / tot
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * tot / args.steps,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (seeded Sobol'/Philox; no datasets)",
+            "config": {"workload": "C4: arith+binary+lookback Asian calls fused, d=64, BB-W1 (QMC+BB-CPW)",
+                       "sample_per_step": f"{reps} replicates x {n} points", "global_batch": n * reps,
+                       "seq_len": d, "parallelism": "host threads"},
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": min(cores, reps), "kind": "oracle",
+                             "sample": f"{reps} replicates x {n} points per step"},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--construction", type=int, default=W.BB)
+    ap.add_argument("--conditioning", type=int, default=W.W1)
+    ap.add_argument("--points", type=int, default=W.CONFIGS["C4"]["n_points"])
+    ap.add_argument("--reps-per-gpu", type=int, default=W.CONFIGS["C4"]["n_replicates"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--e2e-steps", type=int, default=None)
+    args = ap.parse_args()
+    if args.impl == "reference":
+        return run_reference(args)
+
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    import paper_2209_11337_b200 as q
+    from paper_2209_11337_b200.distributed import DistributedPricer
+
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+
+    c = W.CONFIGS[W.HEADLINE]
+    options, d = c["options"], c["d"]
+    if args.conditioning == W.X1:
+        options = [W.ARITH, W.BINARY]
+    N = args.points
+    L = args.reps_per_gpu * world
+    plist = [q.params(S0=W.S0, K=100.0, r=W.R, sigma=W.SIGMA, T=W.T, d=d) for _ in options]
+    cfg = q.config(construction=args.construction, conditioning=args.conditioning, seed=W.SEED, device=local)
+    pricer = DistributedPricer(options, plist, N, L, cfg, dev, rank, world)
+
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)  # > 126 MB L2
+    q.qmccpw_launch_count(reset=True)
+    for _ in range(args.warmup):
+        pricer.step()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+
+    q.qmccpw_launch_count(reset=True)
+    step_ms, kern_ms = [], []
+    stream = torch.cuda.current_stream(dev)
+    results = None
+    with ClockSampler(local) as clk:
+        for _ in range(args.steps):
+            flush.fill_(1)
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            k0, k1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            pricer.enqueue_device_work((k0, k1))
+            pricer.all_reduce()
+            e1.record(stream)
+            results = pricer.fetch_and_finalize()
+            step_ms.append(e0.elapsed_time(e1))
+            kern_ms.append(k0.elapsed_time(k1))
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    launches = q.qmccpw_launch_count(reset=True)
+    total_ms = sum(step_ms)
+    kernel_avg_ms = sum(kern_ms) / len(kern_ms)
+    if world > 1:
+        t = torch.tensor([total_ms, kernel_avg_ms], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        total_ms, kernel_avg_ms = t.tolist()
+    paths = N * L * args.steps
+    value = paths / (total_ms / 1e3)
+
+    # e2e: the public host API call per step (host buffers in, host results out)
+    e2e_steps = args.e2e_steps or args.steps
+    # clean e2e measurement (host wall time around each public call, max over ranks)
+    e2e_total = 0.0
+    for _ in range(e2e_steps):
+        flush.fill_(1)
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        t1 = time.perf_counter()
+        if world == 1:
+            q.qmccpw_price_greeks_batch(options, plist, N, L, q.config(construction=args.construction,
+                                                                       conditioning=args.conditioning, seed=W.SEED,
+                                                                       device=local))
+        else:
+            pricer.step()
+        e2e_total += time.perf_counter() - t1
+    if world > 1:
+        t = torch.tensor([e2e_total], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_total = t.item()
+    e2e_value = N * L * e2e_steps / e2e_total
+
+    # roofline of the dominant kernel (tables + fused path kernel), FP64-ALU bound
+    peaks = measured_peaks()
+    sm_max = float(peaks.get("sm_max_mhz", SM_MAX_MHZ_FALLBACK))
+    peak_tflops = SM_COUNT * FP64_LANES_PER_SM * 2 * sm_max * 1e6 / 1e12
+    per_path = fp64_model_per_path(d, args.construction, args.conditioning, len(options),
+                                   arith_x1=int(args.conditioning == W.X1))
+    launch_paths = N * (L // world)
+    achieved = 2.0 * per_path * launch_paths / (kernel_avg_ms / 1e3) / 1e12
+    traffic = None
+    tpath = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if os.path.exists(tpath):
+        try:
+            traffic = json.load(open(tpath)).get("bytes_per_launch")
+        except Exception:
+            traffic = None
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (seeded Sobol'/Philox; no datasets or weights)",
+            "config": {
+                "workload": "C4: arithmetic+binary+lookback Asian calls fused on shared paths, S0=K=100, sigma=0.2, "
+                            "r=0.1, T=1, d=64, " + {(1, 0): "BB-W1 (QMC+BB-CPW)", (0, 0): "STD-W1 (QMC-CPW)",
+                                                    (2, 0): "PCA-W1", (2, 1): "PCA-X1 (Newton)"}.get(
+                                (args.construction, args.conditioning), "custom"),
+                "points_per_replicate": N, "replicates_per_gpu": L // world, "replicates_total": L,
+                "global_batch": N * L, "seq_len": d, "parallelism": f"dp{world} (replicate-partitioned)",
+                "option_paths_per_s": value * len(options), "greek_sets_per_s": value * len(options),
+                "l2": "flushed (256 MiB write) before every timed step",
+                "kernel_ms_avg": kernel_avg_ms,
+            },
+            "roofline": {"bound": "alu", "achieved": achieved, "peak": peak_tflops, "unit": "TFLOP/s",
+                         "frac": achieved / peak_tflops, "traffic": traffic,
+                         "note": f"FP64 pipe: {SM_COUNT} SMs x {FP64_LANES_PER_SM} FMA lanes x 2 x {sm_max:.0f} MHz; "
+                                 f"algorithmic work {per_path} FP64 lane-instr/path (SURVEY 8(d) model)"},
+            "clocks": clk.summary(),
+            "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": pricer.h2d_bytes,
+                    "d2h_bytes_per_step": pricer.d2h_bytes},
+            "gpu_launches": int(launches),
+            "results_sample": {"price": [r.mean[0] for r in results], "delta": [r.mean[1] for r in results],
+                               "vega": [r.mean[2] for r in results], "gamma": [r.mean[3] for r in results]},
+        }
+        if world == 1 and not args.no_cpu_baseline:
+            line["cpu_baseline"] = cpu_baseline_oracle(options, d, args.construction, args.conditioning)
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,714 @@
+// qmccpw_api.cu -- host side of the C ABI declared in include/qmccpw.h.
+//
+// Validation, device-table cache, launch orchestration and the final
+// statistics.  All per-path arithmetic runs in the
+// kernels of qmccpw_kernels.cu; the host only builds launch parameters, the
+// d = 1 Black-Scholes pivots and the replicate summary.
+#include <cuda_runtime.h>
+#include <curand.h>
+
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "../../include/qmccpw.h"
+#include "qmccpw_internal.h"
+
+using namespace qmccpw;
+
+namespace {
+
+thread_local std::string g_last_error;
+
+int fail(int code, const std::string& msg) {
+    g_last_error = msg;
+    return code;
+}
+
+#define CUDA_TRY(expr)                                                                          \
+    do {                                                                                        \
+        cudaError_t _e = (expr);                                                                \
+        if (_e != cudaSuccess)                                                                  \
+            return fail(QMCCPW_ECUDA, std::string(#expr) + ": " + cudaGetErrorString(_e));     \
+    } while (0)
+
+constexpr int kTableDims = 1024;
+
+// Per-device cache: base direction numbers (cuRAND JOEKUO6, the paper's
+// generator P:440) and grow-only scratch.
+struct DeviceCache {
+    bool ready = false;
+    uint32_t* base_v = nullptr;        // [1024][32] JOEKUO6
+    uint32_t* base_v_scr = nullptr;    // [1024][32] cuRAND pre-scrambled
+    uint32_t* base_shift = nullptr;    // [1024] cuRAND scramble constants
+    uint32_t* zero_shift = nullptr;    // [1024] zeros
+    void* scratch = nullptr;
+    size_t scratch_bytes = 0;
+    double* h_pinned = nullptr;
+    size_t pinned_bytes = 0;
+};
+
+std::mutex g_mu;
+DeviceCache g_cache[64];
+
+int ensure_device(int device, DeviceCache** out) {
+    if (device < 0 || device >= 64) return fail(QMCCPW_EINVAL, "device ordinal out of range");
+    cudaDeviceProp prop;
+    CUDA_TRY(cudaGetDeviceProperties(&prop, device));
+    if (prop.major != 10) return fail(QMCCPW_ECUDA, "libqmccpw is built for sm_100a (B200); device is not sm_10x");
+    std::lock_guard<std::mutex> lk(g_mu);
+    DeviceCache& c = g_cache[device];
+    if (!c.ready) {
+        curandDirectionVectors32_t* vec = nullptr;
+        unsigned int* consts = nullptr;
+        if (curandGetDirectionVectors32(&vec, CURAND_DIRECTION_VECTORS_32_JOEKUO6) != CURAND_STATUS_SUCCESS)
+            return fail(QMCCPW_ECUDA, "curandGetDirectionVectors32(JOEKUO6) failed");
+        CUDA_TRY(cudaMalloc(&c.base_v, kTableDims * 32 * sizeof(uint32_t)));
+        CUDA_TRY(cudaMemcpy(c.base_v, vec, kTableDims * 32 * sizeof(uint32_t), cudaMemcpyHostToDevice));
+        if (curandGetDirectionVectors32(&vec, CURAND_SCRAMBLED_DIRECTION_VECTORS_32_JOEKUO6) != CURAND_STATUS_SUCCESS)
+            return fail(QMCCPW_ECUDA, "curandGetDirectionVectors32(SCRAMBLED_JOEKUO6) failed");
+        CUDA_TRY(cudaMalloc(&c.base_v_scr, kTableDims * 32 * sizeof(uint32_t)));
+        CUDA_TRY(cudaMemcpy(c.base_v_scr, vec, kTableDims * 32 * sizeof(uint32_t), cudaMemcpyHostToDevice));
+        if (curandGetScrambleConstants32(&consts) != CURAND_STATUS_SUCCESS)
+            return fail(QMCCPW_ECUDA, "curandGetScrambleConstants32 failed");
+        CUDA_TRY(cudaMalloc(&c.base_shift, kTableDims * sizeof(uint32_t)));
+        CUDA_TRY(cudaMemcpy(c.base_shift, consts, kTableDims * sizeof(uint32_t), cudaMemcpyHostToDevice));
+        CUDA_TRY(cudaMalloc(&c.zero_shift, kTableDims * sizeof(uint32_t)));
+        CUDA_TRY(cudaMemset(c.zero_shift, 0, kTableDims * sizeof(uint32_t)));
+        c.ready = true;
+    }
+    *out = &c;
+    return QMCCPW_OK;
+}
+
+int ensure_scratch(DeviceCache* c, size_t bytes) {
+    if (c->scratch_bytes >= bytes) return QMCCPW_OK;
+    if (c->scratch) cudaFree(c->scratch);
+    c->scratch = nullptr;
+    c->scratch_bytes = 0;
+    size_t want = bytes + bytes / 4;
+    if (cudaMalloc(&c->scratch, want) != cudaSuccess) return fail(QMCCPW_ENOMEM, "device scratch allocation failed");
+    c->scratch_bytes = want;
+    return QMCCPW_OK;
+}
+
+int ensure_pinned(DeviceCache* c, size_t bytes) {
+    if (c->pinned_bytes >= bytes) return QMCCPW_OK;
+    if (c->h_pinned) cudaFreeHost(c->h_pinned);
+    c->h_pinned = nullptr;
+    c->pinned_bytes = 0;
+    if (cudaMallocHost(&c->h_pinned, bytes) != cudaSuccess) return fail(QMCCPW_ENOMEM, "pinned allocation failed");
+    c->pinned_bytes = bytes;
+    return QMCCPW_OK;
+}
+
+bool is_pow2(int d) { return d > 0 && (d & (d - 1)) == 0; }
+
+qmccpw_config resolve(const qmccpw_config* cfg, int d) {
+    qmccpw_config c;
+    if (cfg) {
+        c = *cfg;
+    } else {
+        c.method = QMCCPW_QMC_CPW;
+        c.construction = is_pow2(d) ? QMCCPW_BB : QMCCPW_STD;
+        c.conditioning = QMCCPW_COND_W1;
+        c.randomization = QMCCPW_RAND_LMS_SHIFT;
+        c.seed = 2209113370ull;
+        c.point_offset = 0;
+        c.device = -1;
+        c.stream = nullptr;
+    }
+    if (c.device < 0) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        c.device = dev;
+    }
+    return c;
+}
+
+int validate_params(const qmccpw_params* p) {
+    if (!p) return fail(QMCCPW_EINVAL, "NULL params");
+    auto bad = [](double x) { return !std::isfinite(x) || !(x > 0.0); };
+    if (bad(p->S0) || bad(p->K) || bad(p->sigma) || bad(p->T) || !std::isfinite(p->r))
+        return fail(QMCCPW_EINVAL, "S0, K, sigma, T must be finite and > 0, r finite");
+    if (p->d < 1 || p->d > kTableDims) return fail(QMCCPW_EINVAL, "d must be in [1, 1024]");
+    return QMCCPW_OK;
+}
+
+int validate_config(const qmccpw_config& c, int d, uint64_t n_points, uint32_t n_reps) {
+    if (c.method != QMCCPW_QMC_CPW && c.method != QMCCPW_LR_MC) return fail(QMCCPW_EINVAL, "unknown method");
+    if (c.construction < 0 || c.construction > 2) return fail(QMCCPW_EINVAL, "unknown construction");
+    if (c.conditioning < 0 || c.conditioning > 1) return fail(QMCCPW_EINVAL, "unknown conditioning");
+    if (c.randomization < 0 || c.randomization > 3) return fail(QMCCPW_EINVAL, "unknown randomization");
+    if (n_points == 0) return fail(QMCCPW_EINVAL, "n_points must be >= 1");
+    if (c.point_offset + n_points > (1ull << 32)) return fail(QMCCPW_EINVAL, "point_offset + n_points > 2^32");
+    if (n_reps == 0 || n_reps >= (1u << 24)) return fail(QMCCPW_EINVAL, "n_replicates must be in [1, 2^24)");
+    if (c.construction == QMCCPW_BB && !is_pow2(d))
+        return fail(QMCCPW_EUNSUPPORTED, "Brownian bridge needs d = 2^m (Alg. 4, P:504)");
+    if (c.method == QMCCPW_LR_MC && c.construction != QMCCPW_STD)
+        return fail(QMCCPW_EUNSUPPORTED, "LR+MC uses the standard construction");
+    if (d > kMaxDimGpu) return fail(QMCCPW_EUNSUPPORTED, "d > 256 is not supported by the sm_100a kernels");
+    return QMCCPW_OK;
+}
+
+// d = 1 Black-Scholes values of each output (call, or cash-or-nothing digital): pivots
+void bs_pivots(int type, const qmccpw_params& p, double out[4]) {
+    const double sT = p.sigma * std::sqrt(p.T), D = std::exp(-p.r * p.T);
+    const double d1 = (std::log(p.S0 / p.K) + (p.r + 0.5 * p.sigma * p.sigma) * p.T) / sT, d2 = d1 - sT;
+    auto cdf = [](double x) { return 0.5 * std::erfc(-x / std::sqrt(2.0)); };
+    auto pdf = [](double x) { return std::exp(-0.5 * x * x) / std::sqrt(2.0 * M_PI); };
+    if (type == QMCCPW_BINARY_ASIAN_CALL) {
+        out[0] = D * cdf(d2);
+        out[1] = D * pdf(d2) / (p.S0 * sT);
+        out[2] = -D * pdf(d2) * d1 / p.sigma;
+        out[3] = -D * pdf(d2) * d1 / (p.S0 * p.S0 * p.sigma * p.sigma * p.T);
+    } else {
+        out[0] = p.S0 * cdf(d1) - p.K * D * cdf(d2);
+        out[1] = cdf(d1);
+        out[2] = p.S0 * pdf(d1) * std::sqrt(p.T);
+        out[3] = pdf(d1) / (p.S0 * sT);
+    }
+}
+
+int tpb_log2_for(const qmccpw_config& c, int d) {
+    const bool need_buf = c.method == QMCCPW_QMC_CPW && (c.construction == QMCCPW_PCA || c.conditioning == QMCCPW_COND_X1);
+    const bool two_buf = c.method == QMCCPW_QMC_CPW && c.construction == QMCCPW_PCA && c.conditioning == QMCCPW_COND_X1;
+    for (int lg = 7; lg >= 5; --lg) {
+        size_t tpb = (size_t)1 << lg, b = 1024;
+        if (need_buf) b += (size_t)d * tpb * 8;
+        if (two_buf) b += (size_t)d * tpb * 8;
+        b += (size_t)d * tpb * 4 + (size_t)d * 128;
+        if (b <= 200 * 1024) return lg;
+    }
+    return 5;
+}
+
+// mean of the first path-matrix column a_j (only seeds Newton's start, X1)
+double mean_first_column(int construction, int d, double T) {
+    const double dt = T / d;
+    double s = 0.0;
+    for (int j = 1; j <= d; ++j) {
+        if (construction == QMCCPW_STD) s += std::sqrt(dt);
+        else if (construction == QMCCPW_BB) s += j * dt / std::sqrt(T);
+        else {
+            const double den = 2.0 * d + 1.0, sh = std::sin(M_PI / (2.0 * den));
+            s += std::sqrt(dt / (4.0 * sh * sh)) * std::sqrt(4.0 / den) * std::sin(j * M_PI / den);
+        }
+    }
+    return s / d;
+}
+
+// Everything a call needs, resolved and validated.
+struct Plan {
+    qmccpw_config cfg;
+    int n_opt;
+    int d;
+    uint64_t N;
+    uint32_t L;
+    uint32_t cells_per_rep;
+    uint64_t n_cells;
+    int stride;
+    int types[kMaxOpt];
+    qmccpw_params p[kMaxOpt];
+};
+
+int make_plan(const int32_t* options, const qmccpw_params* p, int32_t n_options, uint64_t n_points,
+              uint32_t n_reps, const qmccpw_config* cfg, Plan* pl) {
+    if (!options || !p) return fail(QMCCPW_EINVAL, "NULL options or params");
+    if (n_options < 1 || n_options > kMaxOpt) return fail(QMCCPW_EUNSUPPORTED, "1..3 options per call");
+    for (int o = 0; o < n_options; ++o) {
+        int rc = validate_params(&p[o]);
+        if (rc) return rc;
+        if (options[o] < 0 || options[o] > 2) return fail(QMCCPW_EINVAL, "unknown option type");
+        if (p[o].S0 != p[0].S0 || p[o].r != p[0].r || p[o].sigma != p[0].sigma || p[o].T != p[0].T || p[o].d != p[0].d)
+            return fail(QMCCPW_EUNSUPPORTED, "batched options must share S0, r, sigma, T and d");
+    }
+    pl->cfg = resolve(cfg, p[0].d);
+    int rc = validate_config(pl->cfg, p[0].d, n_points, n_reps);
+    if (rc) return rc;
+    for (int o = 0; o < n_options; ++o)
+        if (pl->cfg.method == QMCCPW_QMC_CPW && pl->cfg.conditioning == QMCCPW_COND_X1 &&
+            options[o] == QMCCPW_LOOKBACK_CALL)
+            return fail(QMCCPW_EUNSUPPORTED, "X1 conditioning supports arithmetic and binary Asian calls only");
+    pl->n_opt = n_options;
+    pl->d = p[0].d;
+    pl->N = n_points;
+    pl->L = n_reps;
+    pl->cells_per_rep = (uint32_t)((n_points + kCellPoints - 1) / kCellPoints);
+    pl->n_cells = (uint64_t)n_reps * pl->cells_per_rep;
+    pl->stride = n_options * 8 + 2;
+    for (int o = 0; o < n_options; ++o) {
+        pl->types[o] = options[o];
+        pl->p[o] = p[o];
+    }
+    return QMCCPW_OK;
+}
+
+// scratch layout
+struct Scratch {
+    uint32_t* vscr;
+    uint32_t* shift;
+    double* M;
+    double* a;
+    double* inv_sa;
+    double* partials;
+    double* rep_sums;
+};
+
+size_t align_up(size_t x) { return (x + 255) & ~(size_t)255; }
+
+int carve(DeviceCache* c, const Plan& pl, bool own_partials, uint32_t table_reps, Scratch* s) {
+    const int d = pl.d;
+    size_t off = 0;
+    size_t o_vscr = off; off = align_up(off + (size_t)table_reps * d * 32 * 4);
+    size_t o_shift = off; off = align_up(off + (size_t)table_reps * d * 4);
+    size_t o_M = off; off = align_up(off + (size_t)d * d * 8);
+    size_t o_a = off; off = align_up(off + (size_t)d * 8);
+    size_t o_isa = off; off = align_up(off + (size_t)d * 8);
+    size_t o_part = off; off = align_up(off + (own_partials ? (size_t)pl.n_cells * pl.stride * 8 : 0));
+    size_t o_rs = off; off = align_up(off + (size_t)pl.L * pl.stride * 8);
+    int rc = ensure_scratch(c, off);
+    if (rc) return rc;
+    char* b = static_cast<char*>(c->scratch);
+    s->vscr = reinterpret_cast<uint32_t*>(b + o_vscr);
+    s->shift = reinterpret_cast<uint32_t*>(b + o_shift);
+    s->M = reinterpret_cast<double*>(b + o_M);
+    s->a = reinterpret_cast<double*>(b + o_a);
+    s->inv_sa = reinterpret_cast<double*>(b + o_isa);
+    s->partials = own_partials ? reinterpret_cast<double*>(b + o_part) : nullptr;
+    s->rep_sums = reinterpret_cast<double*>(b + o_rs);
+    return QMCCPW_OK;
+}
+
+int build_tables(DeviceCache* c, const Plan& pl, uint32_t rep_base, uint32_t table_reps, const Scratch& s,
+                 cudaStream_t st) {
+    const qmccpw_config& cfg = pl.cfg;
+    if (cfg.method == QMCCPW_QMC_CPW) {
+        const uint32_t* base_v = c->base_v;
+        const uint32_t* base_shift = c->zero_shift;
+        int mode = 0;
+        if (cfg.randomization == QMCCPW_RAND_SHIFT) mode = 1;
+        if (cfg.randomization == QMCCPW_RAND_NONE) mode = 2;
+        if (cfg.randomization == QMCCPW_RAND_CURAND_COMPAT) {
+            mode = 2;
+            base_v = c->base_v_scr;
+            base_shift = c->base_shift;
+        }
+        CUDA_TRY(launch_randomization(base_v, base_shift, pl.d, table_reps, rep_base, cfg.seed, mode, s.vscr,
+                                      s.shift, st));
+    }
+    if (cfg.method == QMCCPW_QMC_CPW && (cfg.construction == QMCCPW_PCA || cfg.conditioning == QMCCPW_COND_X1))
+        CUDA_TRY(launch_path_matrix(cfg.construction, pl.d, pl.p[0].T, pl.p[0].sigma,
+                                    cfg.construction == QMCCPW_PCA ? s.M : nullptr, s.a, s.inv_sa, st));
+    return QMCCPW_OK;
+}
+
+PathArgs make_args(const Plan& pl, const Scratch& s) {
+    PathArgs a;
+    std::memset(&a, 0, sizeof a);
+    const qmccpw_params& p = pl.p[0];
+    const int d = pl.d;
+    a.d = d;
+    a.n_opt = pl.n_opt;
+    a.tpb_log2 = tpb_log2_for(pl.cfg, d);
+    const bool skip_x1 = pl.cfg.method == QMCCPW_QMC_CPW &&
+                         ((pl.cfg.construction == QMCCPW_STD && pl.cfg.conditioning == QMCCPW_COND_W1) ||
+                          pl.cfg.conditioning == QMCCPW_COND_X1);
+    a.dim_begin = (skip_x1 && d > 1) ? 1 : 0;
+    a.n_points = pl.N;
+    a.point_offset = pl.cfg.point_offset;
+    a.n_reps = pl.L;
+    a.cells_per_rep = pl.cells_per_rep;
+    a.S0 = p.S0;
+    a.r = p.r;
+    a.sigma = p.sigma;
+    a.T = p.T;
+    a.omega = p.r - 0.5 * p.sigma * p.sigma;
+    a.t1 = p.T / d;
+    a.sqrt_t1 = std::sqrt(a.t1);
+    a.s = p.sigma * a.sqrt_t1;
+    a.inv_s = 1.0 / a.s;
+    a.inv_sigma = 1.0 / p.sigma;
+    a.Dfac = std::exp(-p.r * p.T);
+    a.Afac = std::exp(p.r * (a.t1 - p.T));
+    a.lnS0 = std::log(p.S0);
+    a.sqrtT = std::sqrt(p.T);
+    int m = 0;
+    while ((1 << m) < d) ++m;
+    a.bb_m = m;
+    for (int k = 1; k <= m && k < 16; ++k) a.bb_b[k] = std::sqrt(p.T / std::ldexp(1.0, k + 1));
+    for (int o = 0; o < pl.n_opt; ++o) {
+        a.type[o] = pl.types[o];
+        a.K[o] = pl.p[o].K;
+        a.lnK[o] = std::log(pl.p[o].K);
+        a.lndK[o] = std::log((double)d * pl.p[o].K);
+        bs_pivots(pl.types[o], pl.p[o], a.piv[o]);
+    }
+    a.mean_a = mean_first_column(pl.cfg.construction, d, p.T);
+    a.vscr = s.vscr;
+    a.shift = s.shift;
+    a.M = s.M;
+    a.a = s.a;
+    a.inv_sa = s.inv_sa;
+    a.seed = pl.cfg.seed;
+    a.partial_stride = pl.stride;
+    a.path_out = nullptr;
+    a.hook_option = -1;
+    return a;
+}
+
+// P:643-652 replicate summary from per-replicate sums [L][stride]
+void finalize_host(const Plan& pl, const double* rs, qmccpw_result* out) {
+    const double N = (double)pl.N;
+    const int L = (int)pl.L;
+    double unconv = 0.0, ties = 0.0;
+    for (int l = 0; l < L; ++l) {
+        unconv += rs[(size_t)l * pl.stride + pl.n_opt * 8 + 0];
+        ties += rs[(size_t)l * pl.stride + pl.n_opt * 8 + 1];
+    }
+    std::vector<double> Cl(L);
+    for (int o = 0; o < pl.n_opt; ++o) {
+        qmccpw_result r;
+        std::memset(&r, 0, sizeof r);
+        double piv[4];
+        bs_pivots(pl.types[o], pl.p[o], piv);
+        for (int q = 0; q < 4; ++q) {
+            double sumC = 0.0, sumV = 0.0;
+            for (int l = 0; l < L; ++l) {
+                const double s1 = rs[(size_t)l * pl.stride + o * 8 + q * 2 + 0];
+                const double s2 = rs[(size_t)l * pl.stride + o * 8 + q * 2 + 1];
+                Cl[l] = piv[q] + s1 / N;
+                sumC += Cl[l];
+                sumV += s2 / N - (s1 / N) * (s1 / N);
+            }
+            const double C = sumC / L;
+            double dev2 = 0.0;
+            for (int l = 0; l < L; ++l) dev2 += (Cl[l] - C) * (Cl[l] - C);
+            r.mean[q] = C;
+            r.sigma_run[q] = L > 1 ? std::sqrt(dev2 / L) : NAN;
+            r.se[q] = L > 1 ? std::sqrt(dev2 / ((double)L * (L - 1))) : NAN;
+            r.within_var[q] = sumV / L;
+        }
+        r.n_points = pl.N;
+        r.n_replicates = pl.L;
+        r.newton_unconverged = (uint64_t)unconv;
+        r.argmax_near_ties = (uint64_t)ties;
+        out[o] = r;
+    }
+}
+
+struct DeviceGuard {
+    int prev = -1;
+    explicit DeviceGuard(int dev) {
+        cudaGetDevice(&prev);
+        if (prev != dev) cudaSetDevice(dev);
+    }
+    ~DeviceGuard() {
+        int cur = -1;
+        cudaGetDevice(&cur);
+        if (prev >= 0 && cur != prev) cudaSetDevice(prev);
+    }
+};
+
+int run_full(const Plan& pl, qmccpw_result* out) {
+    DeviceGuard g(pl.cfg.device);
+    DeviceCache* c = nullptr;
+    int rc = ensure_device(pl.cfg.device, &c);
+    if (rc) return rc;
+    Scratch s;
+    rc = carve(c, pl, true, pl.L, &s);
+    if (rc) return rc;
+    cudaStream_t st = static_cast<cudaStream_t>(pl.cfg.stream);
+    rc = build_tables(c, pl, 0, pl.L, s, st);
+    if (rc) return rc;
+    PathArgs a = make_args(pl, s);
+    a.partials = s.partials;
+    a.cell_begin = 0;
+    a.cell_end = pl.n_cells;
+    CUDA_TRY(launch_paths(a, pl.cfg.construction, pl.cfg.conditioning, pl.cfg.method, st, nullptr));
+    CUDA_TRY(launch_reduce_cells(s.partials, pl.stride, 0, pl.L, pl.cells_per_rep, s.rep_sums, st));
+    const size_t rs_bytes = (size_t)pl.L * pl.stride * 8;
+    rc = ensure_pinned(c, rs_bytes);
+    if (rc) return rc;
+    CUDA_TRY(cudaMemcpyAsync(c->h_pinned, s.rep_sums, rs_bytes, cudaMemcpyDeviceToHost, st));
+    CUDA_TRY(cudaStreamSynchronize(st));
+    finalize_host(pl, c->h_pinned, out);
+    return QMCCPW_OK;
+}
+
+}  // namespace
+
+// ============================================================================
+extern "C" {
+
+int qmccpw_price_greeks(int32_t option, const qmccpw_params* p, uint64_t n_points, uint32_t n_replicates,
+                        const qmccpw_config* cfg, qmccpw_result* out) {
+    if (!out) return fail(QMCCPW_EINVAL, "NULL out");
+    return qmccpw_price_greeks_batch(&option, p, 1, n_points, n_replicates, cfg, out);
+}
+
+int qmccpw_price_greeks_batch(const int32_t* options, const qmccpw_params* p, int32_t n_options, uint64_t n_points,
+                              uint32_t n_replicates, const qmccpw_config* cfg, qmccpw_result* out) {
+    if (!out) return fail(QMCCPW_EINVAL, "NULL out");
+    Plan pl;
+    int rc = make_plan(options, p, n_options, n_points, n_replicates, cfg, &pl);
+    if (rc) return rc;
+    std::vector<qmccpw_result> tmp(pl.n_opt);
+    rc = run_full(pl, tmp.data());
+    if (rc) return rc;
+    for (int o = 0; o < pl.n_opt; ++o) out[o] = tmp[o];
+    return QMCCPW_OK;
+}
+
+int qmccpw_cell_count(const qmccpw_params* p, int32_t n_options, uint64_t n_points, uint32_t n_replicates,
+                      const qmccpw_config* cfg, uint64_t* n_cells, uint64_t* partial_doubles_per_cell) {
+    if (!n_cells || !partial_doubles_per_cell) return fail(QMCCPW_EINVAL, "NULL output");
+    int rc = validate_params(p);
+    if (rc) return rc;
+    if (n_options < 1 || n_options > kMaxOpt) return fail(QMCCPW_EUNSUPPORTED, "1..3 options per call");
+    qmccpw_config c = resolve(cfg, p->d);
+    rc = validate_config(c, p->d, n_points, n_replicates);
+    if (rc) return rc;
+    *n_cells = (uint64_t)n_replicates * ((n_points + kCellPoints - 1) / kCellPoints);
+    *partial_doubles_per_cell = (uint64_t)n_options * 8 + 2;
+    return QMCCPW_OK;
+}
+
+int qmccpw_partials(const int32_t* options, const qmccpw_params* p, int32_t n_options, uint64_t n_points,
+                    uint32_t n_replicates, const qmccpw_config* cfg, uint64_t cell_begin, uint64_t cell_end,
+                    double* d_partials) {
+    if (!d_partials) return fail(QMCCPW_EINVAL, "NULL d_partials");
+    Plan pl;
+    int rc = make_plan(options, p, n_options, n_points, n_replicates, cfg, &pl);
+    if (rc) return rc;
+    if (cell_begin > cell_end || cell_end > pl.n_cells) return fail(QMCCPW_EINVAL, "cell range out of bounds");
+    DeviceGuard g(pl.cfg.device);
+    DeviceCache* c = nullptr;
+    rc = ensure_device(pl.cfg.device, &c);
+    if (rc) return rc;
+    Scratch s;
+    rc = carve(c, pl, false, pl.L, &s);
+    if (rc) return rc;
+    cudaStream_t st = static_cast<cudaStream_t>(pl.cfg.stream);
+    rc = build_tables(c, pl, 0, pl.L, s, st);
+    if (rc) return rc;
+    PathArgs a = make_args(pl, s);
+    a.partials = d_partials;
+    a.cell_begin = cell_begin;
+    a.cell_end = cell_end;
+    CUDA_TRY(launch_paths(a, pl.cfg.construction, pl.cfg.conditioning, pl.cfg.method, st, nullptr));
+    return QMCCPW_OK;
+}
+
+int qmccpw_replicate_sums(const double* d_partials, const qmccpw_params* p, int32_t n_options, uint64_t n_points,
+                          uint32_t n_replicates, const qmccpw_config* cfg, uint32_t rep_begin, uint32_t rep_end,
+                          double* d_rep_sums) {
+    if (!d_partials || !d_rep_sums) return fail(QMCCPW_EINVAL, "NULL pointer");
+    int rc = validate_params(p);
+    if (rc) return rc;
+    if (n_options < 1 || n_options > kMaxOpt) return fail(QMCCPW_EUNSUPPORTED, "1..3 options per call");
+    qmccpw_config c = resolve(cfg, p->d);
+    rc = validate_config(c, p->d, n_points, n_replicates);
+    if (rc) return rc;
+    if (rep_begin > rep_end || rep_end > n_replicates) return fail(QMCCPW_EINVAL, "replicate range out of bounds");
+    DeviceGuard g(c.device);
+    const uint32_t cpr = (uint32_t)((n_points + kCellPoints - 1) / kCellPoints);
+    CUDA_TRY(launch_reduce_cells(d_partials, n_options * 8 + 2, rep_begin, rep_end, cpr, d_rep_sums,
+                                 static_cast<cudaStream_t>(c.stream)));
+    return QMCCPW_OK;
+}
+
+int qmccpw_finalize(const double* h_rep_sums, const int32_t* options, const qmccpw_params* p, int32_t n_options,
+                    uint64_t n_points, uint32_t n_replicates, const qmccpw_config* cfg, qmccpw_result* out) {
+    if (!h_rep_sums || !out) return fail(QMCCPW_EINVAL, "NULL pointer");
+    Plan pl;
+    qmccpw_config c0;
+    if (cfg) {
+        c0 = *cfg;
+    } else {
+        c0 = resolve(nullptr, p ? p->d : 1);
+    }
+    c0.device = 0;  // host-only: never touches a device
+    int rc = make_plan(options, p, n_options, n_points, n_replicates, &c0, &pl);
+    if (rc) return rc;
+    std::vector<qmccpw_result> tmp(pl.n_opt);
+    finalize_host(pl, h_rep_sums, tmp.data());
+    for (int o = 0; o < pl.n_opt; ++o) out[o] = tmp[o];
+    return QMCCPW_OK;
+}
+
+int qmccpw_finalize_device(const double* d_partials, const int32_t* options, const qmccpw_params* p,
+                           int32_t n_options, uint64_t n_points, uint32_t n_replicates, const qmccpw_config* cfg,
+                           qmccpw_result* out) {
+    if (!d_partials || !out) return fail(QMCCPW_EINVAL, "NULL pointer");
+    Plan pl;
+    int rc = make_plan(options, p, n_options, n_points, n_replicates, cfg, &pl);
+    if (rc) return rc;
+    DeviceGuard g(pl.cfg.device);
+    DeviceCache* c = nullptr;
+    rc = ensure_device(pl.cfg.device, &c);
+    if (rc) return rc;
+    Scratch s;
+    rc = carve(c, pl, false, 0, &s);
+    if (rc) return rc;
+    cudaStream_t st = static_cast<cudaStream_t>(pl.cfg.stream);
+    CUDA_TRY(launch_reduce_cells(d_partials, pl.stride, 0, pl.L, pl.cells_per_rep, s.rep_sums, st));
+    const size_t rs_bytes = (size_t)pl.L * pl.stride * 8;
+    rc = ensure_pinned(c, rs_bytes);
+    if (rc) return rc;
+    CUDA_TRY(cudaMemcpyAsync(c->h_pinned, s.rep_sums, rs_bytes, cudaMemcpyDeviceToHost, st));
+    CUDA_TRY(cudaStreamSynchronize(st));
+    std::vector<qmccpw_result> tmp(pl.n_opt);
+    finalize_host(pl, c->h_pinned, tmp.data());
+    for (int o = 0; o < pl.n_opt; ++o) out[o] = tmp[o];
+    return QMCCPW_OK;
+}
+
+int qmccpw_sobol_u32(uint32_t replicate, uint32_t dim_begin, uint32_t dim_end, uint64_t k_begin, uint64_t k_end,
+                     const qmccpw_config* cfg, uint32_t* out) {
+    if (!out) return fail(QMCCPW_EINVAL, "NULL out");
+    if (dim_end < dim_begin || dim_end > (uint32_t)kTableDims || dim_end == 0)
+        return fail(QMCCPW_EINVAL, "dimension range");
+    if (k_end < k_begin || k_end > (1ull << 32)) return fail(QMCCPW_EINVAL, "point range");
+    if (replicate >= (1u << 24)) return fail(QMCCPW_EINVAL, "replicate >= 2^24");
+    if (k_end == k_begin || dim_end == dim_begin) return QMCCPW_OK;
+    Plan pl;
+    std::memset(&pl, 0, sizeof pl);
+    pl.d = (int)dim_end;
+    pl.cfg = resolve(cfg, pl.d);
+    pl.cfg.method = QMCCPW_QMC_CPW;
+    pl.cfg.conditioning = QMCCPW_COND_W1;
+    pl.cfg.construction = QMCCPW_STD;
+    pl.p[0].T = 1.0;
+    pl.p[0].sigma = 1.0;
+    pl.L = 1;
+    DeviceGuard g(pl.cfg.device);
+    DeviceCache* c = nullptr;
+    int rc = ensure_device(pl.cfg.device, &c);
+    if (rc) return rc;
+    Scratch s;
+    rc = carve(c, pl, false, 1, &s);
+    if (rc) return rc;
+    cudaStream_t st = static_cast<cudaStream_t>(pl.cfg.stream);
+    rc = build_tables(c, pl, replicate, 1, s, st);
+    if (rc) return rc;
+    const size_t n = (size_t)(dim_end - dim_begin) * (k_end - k_begin);
+    uint32_t* d_out = nullptr;
+    CUDA_TRY(cudaMalloc(&d_out, n * 4));
+    cudaError_t e = launch_sobol_hook(s.vscr, s.shift, pl.d, dim_begin, dim_end, k_begin, k_end, d_out, st);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(out, d_out, n * 4, cudaMemcpyDeviceToHost, st);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+    cudaFree(d_out);
+    if (e != cudaSuccess) return fail(QMCCPW_ECUDA, std::string("sobol hook: ") + cudaGetErrorString(e));
+    return QMCCPW_OK;
+}
+
+int qmccpw_normals(uint32_t replicate, int32_t d, uint64_t k_begin, uint64_t k_end, const qmccpw_config* cfg,
+                   double* out) {
+    if (!out) return fail(QMCCPW_EINVAL, "NULL out");
+    if (d < 1 || d > kMaxDimGpu) return fail(QMCCPW_EINVAL, "d must be in [1, 256]");
+    if (k_end < k_begin || k_end > (1ull << 32)) return fail(QMCCPW_EINVAL, "point range");
+    if (replicate >= (1u << 24)) return fail(QMCCPW_EINVAL, "replicate >= 2^24");
+    if (k_end == k_begin) return QMCCPW_OK;
+    Plan pl;
+    std::memset(&pl, 0, sizeof pl);
+    pl.d = d;
+    pl.cfg = resolve(cfg, d);
+    const int method = pl.cfg.method;
+    pl.cfg.conditioning = QMCCPW_COND_W1;
+    pl.cfg.construction = QMCCPW_STD;
+    pl.p[0].T = 1.0;
+    pl.p[0].sigma = 1.0;
+    pl.L = 1;
+    DeviceGuard g(pl.cfg.device);
+    DeviceCache* c = nullptr;
+    int rc = ensure_device(pl.cfg.device, &c);
+    if (rc) return rc;
+    Scratch s;
+    rc = carve(c, pl, false, 1, &s);
+    if (rc) return rc;
+    cudaStream_t st = static_cast<cudaStream_t>(pl.cfg.stream);
+    rc = build_tables(c, pl, replicate, 1, s, st);
+    if (rc) return rc;
+    const size_t n = (size_t)d * (k_end - k_begin);
+    double* d_out = nullptr;
+    CUDA_TRY(cudaMalloc(&d_out, n * 8));
+    cudaError_t e = launch_normals_hook(s.vscr, s.shift, d, k_begin, k_end, method, pl.cfg.seed, replicate, d_out, st);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(out, d_out, n * 8, cudaMemcpyDeviceToHost, st);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+    cudaFree(d_out);
+    if (e != cudaSuccess) return fail(QMCCPW_ECUDA, std::string("normals hook: ") + cudaGetErrorString(e));
+    return QMCCPW_OK;
+}
+
+int qmccpw_path_values(int32_t option, const qmccpw_params* p, uint32_t replicate, uint64_t k_begin, uint64_t k_end,
+                       const qmccpw_config* cfg, double* out) {
+    if (!out) return fail(QMCCPW_EINVAL, "NULL out");
+    if (k_end < k_begin || k_end > (1ull << 32)) return fail(QMCCPW_EINVAL, "point range");
+    if (k_end == k_begin) return QMCCPW_OK;
+    qmccpw_config c0 = resolve(cfg, p ? p->d : 1);
+    c0.point_offset = k_begin;
+    Plan pl;
+    int rc = make_plan(&option, p, 1, k_end - k_begin, 1, &c0, &pl);
+    if (rc) return rc;
+    if (replicate >= (1u << 24)) return fail(QMCCPW_EINVAL, "replicate >= 2^24");
+    DeviceGuard g(pl.cfg.device);
+    DeviceCache* c = nullptr;
+    rc = ensure_device(pl.cfg.device, &c);
+    if (rc) return rc;
+    Scratch s;
+    rc = carve(c, pl, true, 1, &s);
+    if (rc) return rc;
+    cudaStream_t st = static_cast<cudaStream_t>(pl.cfg.stream);
+    rc = build_tables(c, pl, replicate, 1, s, st);
+    if (rc) return rc;
+    PathArgs a = make_args(pl, s);
+    a.rep_base = replicate;
+    a.partials = s.partials;
+    a.cell_begin = 0;
+    a.cell_end = pl.n_cells;
+    const size_t n = (size_t)(k_end - k_begin) * 4;
+    double* d_out = nullptr;
+    CUDA_TRY(cudaMalloc(&d_out, n * 8));
+    a.path_out = d_out;
+    a.hook_option = 0;
+    cudaError_t e = launch_paths(a, pl.cfg.construction, pl.cfg.conditioning, pl.cfg.method, st, nullptr);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(out, d_out, n * 8, cudaMemcpyDeviceToHost, st);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+    cudaFree(d_out);
+    if (e != cudaSuccess) return fail(QMCCPW_ECUDA, std::string("path values hook: ") + cudaGetErrorString(e));
+    return QMCCPW_OK;
+}
+
+const char* qmccpw_last_error(void) { return g_last_error.c_str(); }
+
+void qmccpw_release(int32_t device) {
+    std::lock_guard<std::mutex> lk(g_mu);
+    for (int dev = 0; dev < 64; ++dev) {
+        if (device >= 0 && dev != device) continue;
+        DeviceCache& c = g_cache[dev];
+        if (!c.ready && !c.scratch && !c.h_pinned) continue;
+        int prev = -1;
+        cudaGetDevice(&prev);
+        cudaSetDevice(dev);
+        cudaFree(c.base_v);
+        cudaFree(c.base_v_scr);
+        cudaFree(c.base_shift);
+        cudaFree(c.zero_shift);
+        cudaFree(c.scratch);
+        if (c.h_pinned) cudaFreeHost(c.h_pinned);
+        c = DeviceCache();
+        if (prev >= 0) cudaSetDevice(prev);
+    }
+}
+
+uint64_t qmccpw_launch_count(int32_t reset) {
+    uint64_t n = launch_counter();
+    if (reset) launch_counter() = 0;
+    return n;
+}
+
+}  // extern "C"

@@ -1,0 +1,92 @@
+// qmccpw_internal.h -- structures shared by the host API (qmccpw_api.cu) and
+// the sm_100a kernels (qmccpw_kernels.cu).  Not part of the public ABI.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace qmccpw {
+
+constexpr int kMaxOpt = 3;            // options fused on one path per launch
+constexpr int kCellPoints = 4096;     // points of one replicate per cell (block)
+constexpr int kMaxDimGpu = 256;       // largest d the kernels support
+constexpr int kNewtonIt = 4;          // fixed Newton updates (X1), then up to kNewtonMax
+constexpr int kNewtonMax = 8;
+
+enum Construction { kStd = 0, kBB = 1, kPca = 2 };
+enum Conditioning { kW1 = 0, kX1 = 1 };
+enum Method { kQmc = 0, kLr = 1 };
+enum OptType { kArith = 0, kBinary = 1, kLookback = 2 };
+
+// Everything one launch of the path kernel needs, passed BY VALUE as the
+// kernel argument (no per-call host->device copy).
+struct PathArgs {
+    // geometry
+    int d;
+    int n_opt;
+    int tpb_log2;            // threads per block = 2^tpb_log2
+    int dim_begin;           // first Sobol' dimension consumed (1 when x_1 is not needed)
+    uint64_t n_points;       // points per replicate
+    uint64_t point_offset;   // first Sobol' index
+    uint32_t n_reps;
+    uint32_t rep_base;       // global index of local replicate 0 (LR counters; hooks)
+    uint32_t cells_per_rep;
+    uint64_t cell_begin;     // first global cell of this launch
+    uint64_t cell_end;
+    // market (shared by all options of the launch)
+    double S0, r, sigma, T;
+    double omega;            // r - sigma^2/2 (reading 1)
+    double t1;               // T/d
+    double sqrt_t1;          // sqrt(T/d) = sqrt(dt)
+    double s;                // sigma sqrt(t1)
+    double inv_s;            // 1/s
+    double inv_sigma;
+    double Dfac;             // e^{-rT}
+    double Afac;             // e^{r(t1 - T)}
+    double lnS0;
+    double sqrtT;
+    double bb_b[16];         // b_k = sqrt(T / 2^{k+1}), k = 1..m (index k)
+    int bb_m;
+    // options
+    int type[kMaxOpt];
+    double K[kMaxOpt];
+    double lnK[kMaxOpt];
+    double lndK[kMaxOpt];    // ln(d K)
+    double piv[kMaxOpt][4];  // pivots p_{o,q}
+    // X1
+    double mean_a;           // (1/d) sum_j a_j
+    // tables (device pointers)
+    const uint32_t* vscr;    // [n_reps][d][32] scrambled direction numbers
+    const uint32_t* shift;   // [n_reps][d]
+    const double* M;         // [d][d] path matrix (PCA, and X1 for PCA)
+    const double* a;         // [d] first column a_j of the path matrix (X1)
+    const double* inv_sa;    // [d] 1/(sigma a_j)   (X1)
+    // LR
+    uint64_t seed;
+    // outputs
+    double* partials;        // [cell][partial_doubles_per_cell]
+    int partial_stride;      // doubles per cell = n_opt*8 + 2
+    // parity hook: per-path values out[(point index within range)][4] (NULL in production)
+    double* path_out;
+    int hook_option;         // option index whose values go to path_out
+};
+
+// Launchers (qmccpw_kernels.cu).  All return cudaError_t of the launch.
+cudaError_t launch_randomization(const uint32_t* d_base_v, const uint32_t* d_base_shift, int d, uint32_t n_reps,
+                                 uint32_t rep_base, uint64_t seed, int mode, uint32_t* d_vscr, uint32_t* d_shift,
+                                 cudaStream_t st);
+cudaError_t launch_path_matrix(int construction, int d, double T, double sigma, double* d_M, double* d_a,
+                               double* d_inv_sa, cudaStream_t st);
+cudaError_t launch_paths(const PathArgs& args, int construction, int conditioning, int method, cudaStream_t st,
+                         int* smem_bytes_out);
+cudaError_t launch_reduce_cells(const double* d_partials, int stride, uint32_t rep_begin, uint32_t rep_end,
+                                uint32_t cells_per_rep, double* d_rep_sums, cudaStream_t st);
+cudaError_t launch_sobol_hook(const uint32_t* d_vscr, const uint32_t* d_shift, int d, uint32_t dim_begin,
+                              uint32_t dim_end, uint64_t k_begin, uint64_t k_end, uint32_t* d_out,
+                              cudaStream_t st);
+cudaError_t launch_normals_hook(const uint32_t* d_vscr, const uint32_t* d_shift, int d, uint64_t k_begin,
+                                uint64_t k_end, int method, uint64_t seed, uint32_t rep, double* d_out,
+                                cudaStream_t st);
+
+uint64_t& launch_counter();  // thread-local count of kernel launches
+
+}  // namespace qmccpw

@@ -1,0 +1,687 @@
+// qmccpw_kernels.cu -- sm_100a kernels of the QMC-CPW hot path (arXiv 2209.11337).
+//
+// One thread carries one path at a time through the whole pipeline in FP64
+// ("each thread will be responsible for the simulation of one
+// path"), but nothing is materialised in HBM: Sobol' integers live in
+// per-thread shared-memory state advanced by the Gray-code stride rule, the
+// normals are consumed as they are produced, the Brownian bridge is generated
+// in time order from a log2(d)-deep stack, and each block reduces its cell of
+// 4096 points to one row of partial sums.  The paper instead materialises
+// normals and the bridge in global memory and names that round trip as its
+// 4x slowdown.
+//
+// Device code here is independent of oracle/: it is written from the paper
+// and SURVEY.md Sec. 8(a); tests compare the two on the same points.
+
+#include <cuda_runtime.h>
+#include <math_constants.h>
+#include <stdint.h>
+
+#include "qmccpw_internal.h"
+#include "qmccpw_math.cuh"
+
+namespace qmccpw {
+
+uint64_t& launch_counter() {
+    static thread_local uint64_t n = 0;
+    return n;
+}
+
+// ---------------------------------------------------------------------------
+// (a1) randomisation tables on the device: per (replicate, dimension) a
+// Matousek left-matrix scramble L (unit lower-triangular in MSB-first digit
+// order) and a digital shift, both from Philox4x32-10 keyed by the seed with
+// counter (j, w, 0, (rep<<8)|0x01).  v'_b = L v_b is formed column-wise:
+// v' = XOR over the set digits t of v of column t of L.
+// ---------------------------------------------------------------------------
+__global__ void randomization_kernel(const uint32_t* __restrict__ base_v, const uint32_t* __restrict__ base_shift,
+                                     int d, uint32_t n_reps, uint32_t rep_base, uint32_t key0, uint32_t key1, int mode,
+                                     uint32_t* __restrict__ vscr, uint32_t* __restrict__ shift) {
+    const uint64_t gid = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const uint64_t total = (uint64_t)n_reps * d * 32;
+    if (gid >= total) return;
+    const int b = (int)(gid & 31);
+    const uint64_t rj = gid >> 5;
+    const int j = (int)(rj % d);
+    const uint32_t rep = rep_base + (uint32_t)(rj / d);
+    const uint32_t v = base_v[j * 32 + b];
+    if (mode == 2) {  // tables used as given (cuRAND-compatible / plain)
+        vscr[gid] = v;
+        if (b == 0) shift[rj] = base_shift[j];
+        return;
+    }
+    uint32_t w[32];
+#pragma unroll
+    for (uint32_t blk = 0; blk < 8; ++blk) {
+        uint32_t c[4] = {(uint32_t)j, blk, 0u, (rep << 8) | 0x01u};
+        philox4x32_10(c, key0, key1);
+        w[4 * blk + 0] = c[0];
+        w[4 * blk + 1] = c[1];
+        w[4 * blk + 2] = c[2];
+        w[4 * blk + 3] = c[3];
+    }
+    if (b == 0) shift[rj] = w[0];
+    if (mode == 1) {  // shift only
+        vscr[gid] = v;
+        return;
+    }
+    uint32_t out = 0;
+    for (int t = 0; t < 32; ++t) {           // digit t <-> bit 31-t
+        if (!((v >> (31 - t)) & 1u)) continue;
+        uint32_t col = 1u << (31 - t);       // unit diagonal
+        for (int i = t + 1; i < 32; ++i)     // row i has random digits 0..i-1 (bits 31..32-i)
+            col |= ((w[i] >> (31 - t)) & 1u) << (31 - i);
+        out ^= col;
+    }
+    vscr[gid] = out;
+}
+
+cudaError_t launch_randomization(const uint32_t* d_base_v, const uint32_t* d_base_shift, int d, uint32_t n_reps,
+                                 uint32_t rep_base, uint64_t seed, int mode, uint32_t* d_vscr, uint32_t* d_shift,
+                                 cudaStream_t st) {
+    const uint64_t total = (uint64_t)n_reps * d * 32;
+    const int tpb = 256;
+    const unsigned grid = (unsigned)((total + tpb - 1) / tpb);
+    randomization_kernel<<<grid, tpb, 0, st>>>(d_base_v, d_base_shift, d, n_reps, rep_base, (uint32_t)seed,
+                                               (uint32_t)(seed >> 32), mode, d_vscr, d_shift);
+    ++launch_counter();
+    return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------------------
+// (a1) path-matrix tables.  PCA of C = [min(t_i,t_j)] in closed form:
+// theta_k = (2k-1) pi/(2d+1), lambda_k = dt/(4 sin^2(theta_k/2)),
+// M_jk = sqrt(lambda_k) sqrt(4/(2d+1)) sin(j theta_k) (1-based), evaluated
+// with sinpi on exactly reduced rational arguments.  a_j = M_j1 for every
+// construction (STD: sqrt(dt); BB: t_j/sqrt(T)).
+// ---------------------------------------------------------------------------
+__global__ void path_matrix_kernel(int construction, int d, double T, double sigma, double* __restrict__ M,
+                                   double* __restrict__ a, double* __restrict__ inv_sa) {
+    const int idx = blockIdx.x * blockDim.x + threadIdx.x;
+    const double dt = T / d;
+    const long long den = 2LL * d + 1;
+    if (construction == kPca && M != nullptr && idx < d * d) {
+        const int j = idx / d + 1, k = idx % d + 1;
+        const double sh = sinpi((double)(2 * k - 1) / (double)(2 * den));        // sin(theta_k / 2)
+        const long long num = ((long long)j * (2 * k - 1)) % (2 * den);           // j theta_k / pi mod 2
+        const double s = sinpi((double)num / (double)den);
+        M[idx] = sqrt(dt / (4.0 * sh * sh)) * sqrt(4.0 / (double)den) * s;
+    }
+    if (idx < d) {
+        const int j = idx + 1;
+        double aj;
+        if (construction == kStd) {
+            aj = sqrt(dt);
+        } else if (construction == kBB) {
+            aj = (double)j * dt / sqrt(T);
+        } else {
+            const double sh = sinpi(1.0 / (double)(2 * den));
+            const long long num = (long long)j % (2 * den);
+            aj = sqrt(dt / (4.0 * sh * sh)) * sqrt(4.0 / (double)den) * sinpi((double)num / (double)den);
+        }
+        a[idx] = aj;
+        inv_sa[idx] = 1.0 / (sigma * aj);
+    }
+}
+
+cudaError_t launch_path_matrix(int construction, int d, double T, double sigma, double* d_M, double* d_a,
+                               double* d_inv_sa, cudaStream_t st) {
+    const int n = (construction == kPca && d_M) ? d * d : d;
+    const int tpb = 256;
+    path_matrix_kernel<<<(n + tpb - 1) / tpb, tpb, 0, st>>>(construction, d, T, sigma, d_M, d_a, d_inv_sa);
+    ++launch_counter();
+    return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------------------
+// Per-thread Sobol' state (a2).  Thread tau of a 2^p-thread block visits the
+// points k, k + 2^p, k + 2^(p+1), ...; with A = k >> p the Gray code satisfies
+// g(k + 2^p) = g(k) ^ (1 << (p-1)) ^ (1 << (p + ctz(A+1))), so each dimension
+// advances by two XORs of the replicate's direction numbers.
+// ---------------------------------------------------------------------------
+struct SobolState {
+    uint32_t* ys;        // smem [d][tpb]
+    const uint32_t* vt;  // smem [d][32]
+    int tpb_log2;
+    int tid;
+    __device__ __forceinline__ uint32_t get(int j) const { return ys[(j << tpb_log2) + tid]; }
+    __device__ __forceinline__ void init(int j0, int d, uint64_t k, const uint32_t* __restrict__ shift) {
+        const uint32_t g = (uint32_t)(k ^ (k >> 1));
+        for (int j = j0; j < d; ++j) {
+            uint32_t y = shift[j];
+            uint32_t gg = g;
+            while (gg) {
+                const int b = __ffs(gg) - 1;
+                y ^= vt[j * 32 + b];
+                gg &= gg - 1;
+            }
+            ys[(j << tpb_log2) + tid] = y;
+        }
+    }
+    __device__ __forceinline__ void advance(int j0, int d, uint64_t k) {
+        const uint64_t A = k >> tpb_log2;
+        int c = __ffsll((long long)(A + 1)) - 1;
+        if (tpb_log2 + c > 31) c = 31 - tpb_log2;  // only reached past the last valid point
+        const int b0 = tpb_log2 - 1, b1 = tpb_log2 + c;
+        for (int j = j0; j < d; ++j) ys[(j << tpb_log2) + tid] ^= vt[j * 32 + b0] ^ vt[j * 32 + b1];
+    }
+};
+
+// ---------------------------------------------------------------------------
+// (a5) W1-mode accumulators over the separated path S~(t_j):
+// S~_A, I_A (vega inner sum), and the lookback's S~_max with the
+// lowest argmax j* and I_max = S~_{j*}(W~_{j*} - sigma(t_{j*} - t_1))
+// (P:599 with the 1/d removed, reading 3).  Near-ties are tracked with the
+// runner-up exponent.
+// ---------------------------------------------------------------------------
+struct W1Acc {
+    double sumS, sumI, Smax, Imax, emax, esec;
+    __device__ __forceinline__ void reset() {
+        sumS = 0.0; sumI = 0.0; Smax = 0.0; Imax = 0.0; emax = -CUDART_INF; esec = -CUDART_INF;
+    }
+    // date index j (0-based, t_{j+1} - t_1 = j dt), Wt = W~(t_{j+1} - t_1)
+    __device__ __forceinline__ void push(const PathArgs& P, int j, double Wt) {
+        const double tt = (double)j * P.t1;
+        const double e = fma(P.sigma, Wt, P.omega * tt);
+        const double St = P.S0 * exp(e);
+        const double I = St * fma(-P.sigma, tt, Wt);
+        sumS += St;
+        sumI += I;
+        if (e > emax) {
+            esec = emax;
+            emax = e;
+            Smax = St;
+            Imax = I;
+        } else if (e > esec) {
+            esec = e;
+        }
+    }
+};
+
+// (a6)+(a7) W1 threshold psi_d and the closed-form smoothed
+// payoff and Greeks (readings 1-5).
+__device__ __forceinline__ void tail_w1(const PathArgs& P, int o, const W1Acc& acc, double f[4]) {
+    const int type = P.type[o];
+    const double inv_d = 1.0 / (double)P.d;
+    const double stat = (type == kLookback) ? acc.Smax : acc.sumS * inv_d;
+    const double I = (type == kLookback) ? acc.Imax : acc.sumI * inv_d;
+    const double psi = (P.lnK[o] - log(stat) - P.omega * P.t1) * P.inv_s;
+    const double ph = normal_pdf(psi);
+    const double P0 = normal_sf(psi);
+    const double K = P.K[o], D = P.Dfac, S0 = P.S0;
+    if (type == kBinary) {
+        f[0] = D * P0;
+        f[1] = D * ph * P.inv_s / S0;
+        f[2] = D * ph * (I * P.inv_s / stat + psi * P.inv_sigma - P.sqrt_t1);
+        f[3] = D * ph * P.inv_s / (S0 * S0) * (psi * P.inv_s - 1.0);
+    } else {
+        const double P1 = normal_sf(psi - P.s);
+        f[0] = P.Afac * stat * P1 - D * K * P0;
+        f[1] = P.Afac * (stat / S0) * P1;
+        f[2] = P.Afac * P1 * I + K * D * ph * P.sqrt_t1;
+        f[3] = K * D * ph * P.inv_s / (S0 * S0);
+    }
+}
+
+// (a6)+(a7) X1 mode: u* solves sum_j exp(c_j + sigma a_j u) = dK
+// by Newton from the AM-GM start, warp-uniform iteration count, clamped to the
+// bracket; then the conditional payoff and Greeks.  cb = per-thread c_j column.
+__device__ __forceinline__ void tail_x1(const PathArgs& P, int o, const double* cb, int stride, double f[4],
+                                        unsigned& unconverged) {
+    const int d = P.d;
+    const double lnK = P.lnK[o], lndK = P.lndK[o], sg = P.sigma;
+    double u_lo = CUDART_INF, u_hi = CUDART_INF, sumc = 0.0;
+    for (int j = 0; j < d; ++j) {
+        const double cj = cb[j * stride];
+        const double isa = P.inv_sa[j];
+        u_lo = fmin(u_lo, (lnK - cj) * isa);
+        u_hi = fmin(u_hi, (lndK - cj) * isa);
+        sumc += cj;
+    }
+    double u = fmin(u_hi, (lnK - sumc / d) / (sg * P.mean_a));
+    bool conv = false;
+    for (int it = 0; it < kNewtonMax; ++it) {
+        double S = 0.0, SA = 0.0;
+        for (int j = 0; j < d; ++j) {
+            const double aj = P.a[j];
+            const double E = exp(fma(sg * aj, u, cb[j * stride]));
+            S += E;
+            SA = fma(aj, E, SA);
+        }
+        const double h = log(S) - lndK;
+        const double du = h * S / (sg * SA);
+        conv = fabs(du) <= 1e-13 * fmax(1.0, fabs(u));
+        u = fmin(fmax(u - du, u_lo), u_hi);
+        if (it + 1 >= kNewtonIt && __all_sync(__activemask(), conv)) break;
+    }
+    unconverged += conv ? 0u : 1u;
+    double Dst = 0.0, Qst = 0.0, Vst = 0.0, sumW = 0.0, sumWv = 0.0;
+    const bool arith = P.type[o] == kArith;
+    for (int j = 0; j < d; ++j) {
+        const double aj = P.a[j], cj = cb[j * stride];
+        const double tj = (double)(j + 1) * P.t1;
+        const double Rj = (cj - P.lnS0 - P.omega * tj) * P.inv_sigma;
+        const double E = exp(fma(sg * aj, u, cj));
+        Dst = fma(aj, E, Dst);
+        Qst = fma(aj * aj, E, Qst);
+        Vst = fma(E, Rj - sg * tj + aj * u, Vst);
+        if (arith) {
+            const double w = exp(fma(0.5 * sg * sg * aj, aj, cj));
+            const double Pj = normal_cdf(sg * aj - u);
+            sumW = fma(w, Pj, sumW);
+            sumWv = fma(w * (Rj - sg * tj + sg * aj * aj), Pj, sumWv);
+        }
+    }
+    const double D = P.Dfac, S0 = P.S0, K = P.K[o], dd = (double)d;
+    const double ph = normal_pdf(u);
+    if (arith) {
+        f[0] = D * (sumW / dd - K * normal_sf(u));
+        f[1] = D * sumW / (dd * S0);
+        f[2] = D * (sumWv / dd + ph * Dst / dd);
+        f[3] = D * dd * K * K * ph / (S0 * S0 * sg * Dst);
+    } else {
+        const double up = -dd * K / (S0 * sg * Dst);
+        f[0] = D * normal_sf(u);
+        f[1] = D * ph * dd * K / (S0 * sg * Dst);
+        f[2] = D * ph * Vst / (sg * Dst);
+        f[3] = D * (dd * K / sg) * ph / (S0 * Dst) * (-u * up - 2.0 / S0 - sg * up * Qst / Dst);
+    }
+}
+
+// (a9) LR+MC: Philox normals (counter (k_lo, k_hi, j/4, (rep<<8)|0x02)),
+// STD path of full prices, payoff x score.
+__device__ __forceinline__ void lr_path(const PathArgs& P, uint32_t rep, uint64_t k, double f[kMaxOpt][4]) {
+    const int d = P.d;
+    double W = 0.0, sumS = 0.0, Smax = 0.0, vscore = 0.0, Z1 = 0.0;
+    for (int jq = 0; jq < d; jq += 4) {
+        uint32_t c[4] = {(uint32_t)k, (uint32_t)(k >> 32), (uint32_t)(jq >> 2), (rep << 8) | 0x02u};
+        philox4x32_10(c, (uint32_t)P.seed, (uint32_t)(P.seed >> 32));
+#pragma unroll
+        for (int w = 0; w < 4; ++w) {
+            const int j = jq + w;
+            if (j < d) {
+                const double x = normal_from_u32(c[w]);
+                if (j == 0) Z1 = x;
+                W = fma(P.sqrt_t1, x, W);
+                const double S = P.S0 * exp(fma(P.sigma, W, P.omega * (double)(j + 1) * P.t1));
+                sumS += S;
+                Smax = fmax(Smax, S);
+                vscore += (x * x - 1.0) * P.inv_sigma - x * P.sqrt_t1;
+            }
+        }
+    }
+    const double SA = sumS / d, S0 = P.S0, sg = P.sigma, t1 = P.t1;
+    const double sd = Z1 / (S0 * sg * P.sqrt_t1);
+    const double sgm = (Z1 * Z1 - 1.0) / (S0 * S0 * sg * sg * t1) - Z1 / (S0 * S0 * sg * P.sqrt_t1);
+#pragma unroll
+    for (int o = 0; o < kMaxOpt; ++o) {
+        if (o >= P.n_opt) break;
+        double pay;
+        if (P.type[o] == kArith) pay = P.Dfac * fmax(SA - P.K[o], 0.0);
+        else if (P.type[o] == kBinary) pay = (SA > P.K[o]) ? P.Dfac : 0.0;
+        else pay = P.Dfac * fmax(Smax - P.K[o], 0.0);
+        f[o][0] = pay;
+        f[o][1] = pay * sd;
+        f[o][2] = pay * vscore;
+        f[o][3] = pay * sgm;
+    }
+}
+
+// ---------------------------------------------------------------------------
+// The fused path kernel: one block = one cell (replicate, 4096 points).
+// ---------------------------------------------------------------------------
+template <int CONSTR, int COND, int METHOD>
+__global__ void __launch_bounds__(128) paths_kernel(const PathArgs P) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    const int tpb_log2 = P.tpb_log2;
+    const int tpb = 1 << tpb_log2;
+    const int tid = threadIdx.x;
+    const int d = P.d;
+    const uint64_t cell = P.cell_begin + blockIdx.x;
+    const uint32_t rep_local = (uint32_t)(cell / P.cells_per_rep);
+    const uint64_t blk = cell % P.cells_per_rep;
+    const uint64_t i0 = blk * (uint64_t)kCellPoints;
+    const int ppt = kCellPoints >> tpb_log2;
+    constexpr bool kNeedBuf = (METHOD == kQmc) && (CONSTR == kPca || COND == kX1);
+    constexpr bool kTwoBuf = (METHOD == kQmc) && (CONSTR == kPca && COND == kX1);
+
+    // shared memory carve-up: [red: 4 warps x 32 doubles][buf0][buf1][ys][vt]
+    double* red = reinterpret_cast<double*>(smem_raw);
+    double* buf0 = red + 4 * 32;
+    double* buf1 = buf0 + (kNeedBuf ? (size_t)d * tpb : 0);
+    uint32_t* ys = reinterpret_cast<uint32_t*>(buf1 + (kTwoBuf ? (size_t)d * tpb : 0));
+    uint32_t* vt = ys + (METHOD == kQmc ? (size_t)d * tpb : 0);
+
+    SobolState sob{ys, vt, tpb_log2, tid};
+    if (METHOD == kQmc) {
+        const uint32_t* src = P.vscr + (size_t)rep_local * d * 32;
+        for (int idx = tid; idx < d * 32; idx += tpb) vt[idx] = src[idx];
+        __syncthreads();
+        sob.init(P.dim_begin, d, P.point_offset + i0 + tid, P.shift + (size_t)rep_local * d);
+    }
+
+    double acc1[kMaxOpt][4], acc2[kMaxOpt][4];
+#pragma unroll
+    for (int o = 0; o < kMaxOpt; ++o)
+#pragma unroll
+        for (int q = 0; q < 4; ++q) acc1[o][q] = acc2[o][q] = 0.0;
+    unsigned unconverged = 0, ties = 0;
+
+    for (int a = 0; a < ppt; ++a) {
+        const uint64_t i = i0 + tid + ((uint64_t)a << tpb_log2);
+        if (i >= P.n_points) break;
+        const uint64_t k = P.point_offset + i;
+        double f[kMaxOpt][4];
+
+        if (METHOD == kLr) {
+            lr_path(P, P.rep_base + rep_local, k, f);
+        } else if (COND == kW1) {
+            W1Acc w1;
+            w1.reset();
+            if (CONSTR == kStd) {
+                // Alg. 3: W~ accumulates sqrt(dt) x_j for j >= 2; x_1 cancels in W - W(t_1)
+                double Wt = 0.0;
+                w1.push(P, 0, 0.0);
+                for (int j = 1; j < d; ++j) {
+                    Wt = fma(P.sqrt_t1, normal_from_u32(sob.get(j)), Wt);
+                    w1.push(P, j, Wt);
+                }
+            } else if (CONSTR == kBB) {
+                // Alg. 4 generated in time order: W(mid) = (W(l) + W(r))/2 + b_k x_dim(mid)
+                // with dim(mid) = 2^k - 1 - (mid >> (ctz(mid)+1)), the consumption order of Alg. 4.
+                int stT[12];
+                double stW[12];
+                int sp = 0;
+                stT[0] = d;
+                stW[0] = P.sqrtT * normal_from_u32(sob.get(0));
+                double Wl = 0.0, W1 = 0.0;
+                int tl = 0;
+                for (int j = 1; j <= d; ++j) {
+                    while (stT[sp] != j) {
+                        const int mid = (tl + stT[sp]) >> 1;
+                        const int c = __ffs(mid) - 1;
+                        const int lev = P.bb_m - c;
+                        const int dim = (1 << lev) - 1 - (mid >> (c + 1));
+                        const double x = normal_from_u32(sob.get(dim));
+                        const double Wm = fma(P.bb_b[lev], x, 0.5 * (Wl + stW[sp]));
+                        ++sp;
+                        stT[sp] = mid;
+                        stW[sp] = Wm;
+                    }
+                    const double Wj = stW[sp];
+                    --sp;
+                    if (j == 1) W1 = Wj;
+                    w1.push(P, j - 1, Wj - W1);
+                    Wl = Wj;
+                    tl = j;
+                }
+            } else {
+                // PCA: W = M x (the dense contraction), x staged per thread in shared memory
+                double* xb = buf0 + tid;
+                for (int kk = 0; kk < d; ++kk) xb[kk * tpb] = normal_from_u32(sob.get(kk));
+                double W1 = 0.0;
+                for (int j = 0; j < d; ++j) {
+                    const double* Mr = P.M + (size_t)j * d;
+                    double W = 0.0;
+                    for (int kk = 0; kk < d; ++kk) W = fma(__ldg(Mr + kk), xb[kk * tpb], W);
+                    if (j == 0) W1 = W;
+                    w1.push(P, j, W - W1);
+                }
+            }
+            if (w1.emax - w1.esec < 1e-12) ++ties;  // only meaningful for the lookback
+#pragma unroll
+            for (int o = 0; o < kMaxOpt; ++o)
+                if (o < P.n_opt) tail_w1(P, o, w1, f[o]);
+        } else {
+            // X1: c_j = ln S0 + omega t_j + sigma R_j, R = M x with x_1 := 0
+            double* cb = (CONSTR == kPca ? buf1 : buf0) + tid;
+            if (CONSTR == kStd) {
+                double R = 0.0;
+                for (int j = 0; j < d; ++j) {
+                    if (j > 0) R = fma(P.sqrt_t1, normal_from_u32(sob.get(j)), R);
+                    cb[j * tpb] = P.lnS0 + P.omega * (double)(j + 1) * P.t1 + P.sigma * R;
+                }
+            } else if (CONSTR == kBB) {
+                int stT[12];
+                double stW[12];
+                int sp = 0;
+                stT[0] = d;
+                stW[0] = 0.0;  // terminal loading of x_1 removed
+                double Wl = 0.0;
+                int tl = 0;
+                for (int j = 1; j <= d; ++j) {
+                    while (stT[sp] != j) {
+                        const int mid = (tl + stT[sp]) >> 1;
+                        const int c = __ffs(mid) - 1;
+                        const int lev = P.bb_m - c;
+                        const int dim = (1 << lev) - 1 - (mid >> (c + 1));
+                        const double x = normal_from_u32(sob.get(dim));
+                        const double Wm = fma(P.bb_b[lev], x, 0.5 * (Wl + stW[sp]));
+                        ++sp;
+                        stT[sp] = mid;
+                        stW[sp] = Wm;
+                    }
+                    const double Rj = stW[sp];
+                    --sp;
+                    cb[(j - 1) * tpb] = P.lnS0 + P.omega * (double)j * P.t1 + P.sigma * Rj;
+                    Wl = Rj;
+                    tl = j;
+                }
+            } else {
+                double* xb = buf0 + tid;
+                for (int kk = 1; kk < d; ++kk) xb[kk * tpb] = normal_from_u32(sob.get(kk));
+                for (int j = 0; j < d; ++j) {
+                    const double* Mr = P.M + (size_t)j * d;
+                    double R = 0.0;
+                    for (int kk = 1; kk < d; ++kk) R = fma(__ldg(Mr + kk), xb[kk * tpb], R);
+                    cb[j * tpb] = P.lnS0 + P.omega * (double)(j + 1) * P.t1 + P.sigma * R;
+                }
+            }
+#pragma unroll
+            for (int o = 0; o < kMaxOpt; ++o)
+                if (o < P.n_opt) tail_x1(P, o, cb, tpb, f[o], unconverged);
+        }
+
+        if (P.path_out != nullptr) {
+#pragma unroll
+            for (int o = 0; o < kMaxOpt; ++o)
+                if (o == P.hook_option)
+                    for (int q = 0; q < 4; ++q) P.path_out[i * 4 + q] = f[o][q];
+        }
+#pragma unroll
+        for (int o = 0; o < kMaxOpt; ++o) {
+            if (o < P.n_opt) {
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                    const double y = f[o][q] - P.piv[o][q];
+                    acc1[o][q] += y;
+                    acc2[o][q] = fma(y, y, acc2[o][q]);
+                }
+            }
+        }
+        if (METHOD == kQmc) sob.advance(P.dim_begin, d, k);
+    }
+
+    // (a8) fixed-shape reduction: warp butterfly, then the warps in order.
+    const int lane = tid & 31, warp = tid >> 5, nwarps = tpb >> 5;
+    const int n_out = P.partial_stride;
+#pragma unroll
+    for (int o = 0; o < kMaxOpt; ++o) {
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            double s1 = acc1[o][q], s2 = acc2[o][q];
+#pragma unroll
+            for (int off = 16; off > 0; off >>= 1) {
+                s1 += __shfl_xor_sync(0xffffffffu, s1, off);
+                s2 += __shfl_xor_sync(0xffffffffu, s2, off);
+            }
+            if (lane == 0 && o < P.n_opt) {
+                red[warp * 32 + o * 8 + q * 2 + 0] = s1;
+                red[warp * 32 + o * 8 + q * 2 + 1] = s2;
+            }
+        }
+    }
+    unsigned uc = unconverged, tc = ties;
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) {
+        uc += __shfl_xor_sync(0xffffffffu, uc, off);
+        tc += __shfl_xor_sync(0xffffffffu, tc, off);
+    }
+    if (lane == 0) {
+        red[warp * 32 + P.n_opt * 8 + 0] = (double)uc;
+        red[warp * 32 + P.n_opt * 8 + 1] = (double)tc;
+    }
+    __syncthreads();
+    if (tid < n_out) {
+        double s = 0.0;
+        for (int w = 0; w < nwarps; ++w) s += red[w * 32 + tid];
+        P.partials[(size_t)cell * n_out + tid] = s;
+    }
+}
+
+static size_t path_smem_bytes(const PathArgs& a, int constr, int cond, int method) {
+    const size_t tpb = (size_t)1 << a.tpb_log2;
+    const bool need_buf = method == kQmc && (constr == kPca || cond == kX1);
+    const bool two_buf = method == kQmc && constr == kPca && cond == kX1;
+    size_t b = 4 * 32 * sizeof(double);
+    if (need_buf) b += (size_t)a.d * tpb * sizeof(double);
+    if (two_buf) b += (size_t)a.d * tpb * sizeof(double);
+    if (method == kQmc) b += (size_t)a.d * tpb * sizeof(uint32_t) + (size_t)a.d * 32 * sizeof(uint32_t);
+    return b;
+}
+
+template <int C, int K, int M>
+static cudaError_t launch_paths_t(const PathArgs& args, cudaStream_t st, int* smem_out) {
+    const size_t smem = path_smem_bytes(args, C, K, M);
+    if (smem_out) *smem_out = (int)smem;
+    cudaError_t e = cudaFuncSetAttribute(paths_kernel<C, K, M>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)smem);
+    if (e != cudaSuccess) return e;
+    const uint64_t nblocks = args.cell_end - args.cell_begin;
+    if (nblocks == 0) return cudaSuccess;
+    paths_kernel<C, K, M><<<(unsigned)nblocks, 1 << args.tpb_log2, smem, st>>>(args);
+    ++launch_counter();
+    return cudaGetLastError();
+}
+
+cudaError_t launch_paths(const PathArgs& args, int construction, int conditioning, int method, cudaStream_t st,
+                         int* smem_out) {
+    if (method == kLr) return launch_paths_t<kStd, kW1, kLr>(args, st, smem_out);
+    if (conditioning == kW1) {
+        if (construction == kStd) return launch_paths_t<kStd, kW1, kQmc>(args, st, smem_out);
+        if (construction == kBB) return launch_paths_t<kBB, kW1, kQmc>(args, st, smem_out);
+        return launch_paths_t<kPca, kW1, kQmc>(args, st, smem_out);
+    }
+    if (construction == kStd) return launch_paths_t<kStd, kX1, kQmc>(args, st, smem_out);
+    if (construction == kBB) return launch_paths_t<kBB, kX1, kQmc>(args, st, smem_out);
+    return launch_paths_t<kPca, kX1, kQmc>(args, st, smem_out);
+}
+
+// ---------------------------------------------------------------------------
+// (a8) per-replicate reduction over cells, fixed sequential order (so that a
+// multi-GPU all-reduced partial buffer reduces to identical bits).
+// ---------------------------------------------------------------------------
+__global__ void reduce_cells_kernel(const double* __restrict__ partials, int stride, uint32_t rep_begin,
+                                    uint32_t cells_per_rep, double* __restrict__ rep_sums) {
+    const uint32_t rep = rep_begin + blockIdx.x;
+    const int t = threadIdx.x;
+    if (t >= stride) return;
+    const double* p = partials + (size_t)rep * cells_per_rep * stride + t;
+    double s = 0.0;
+    for (uint32_t c = 0; c < cells_per_rep; ++c) s += p[(size_t)c * stride];
+    rep_sums[(size_t)rep * stride + t] = s;
+}
+
+cudaError_t launch_reduce_cells(const double* d_partials, int stride, uint32_t rep_begin, uint32_t rep_end,
+                                uint32_t cells_per_rep, double* d_rep_sums, cudaStream_t st) {
+    if (rep_end <= rep_begin) return cudaSuccess;
+    reduce_cells_kernel<<<rep_end - rep_begin, 32, 0, st>>>(d_partials, stride, rep_begin, cells_per_rep, d_rep_sums);
+    ++launch_counter();
+    return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------------------
+// Parity hooks: the same SobolState / normal code the path kernel runs.
+// One block of 2^p threads walks [k_begin, k_end) exactly like a cell.
+// ---------------------------------------------------------------------------
+__global__ void sobol_hook_kernel(const uint32_t* __restrict__ vscr, const uint32_t* __restrict__ shift, int d,
+                                  uint32_t dim_begin, uint32_t dim_end, uint64_t k_begin, uint64_t k_end,
+                                  uint32_t* __restrict__ out) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    const int tpb_log2 = 7, tpb = 128, tid = threadIdx.x;
+    uint32_t* ys = reinterpret_cast<uint32_t*>(smem_raw);
+    uint32_t* vt = ys + (size_t)d * tpb;
+    for (int idx = tid; idx < d * 32; idx += tpb) vt[idx] = vscr[idx];
+    __syncthreads();
+    SobolState sob{ys, vt, tpb_log2, tid};
+    const uint64_t nk = k_end - k_begin;
+    const uint64_t base = k_begin + (uint64_t)blockIdx.x * kCellPoints;
+    sob.init(0, d, base + tid, shift);
+    for (int a = 0; a < kCellPoints / tpb; ++a) {
+        const uint64_t k = base + tid + ((uint64_t)a << tpb_log2);
+        if (k >= k_end) break;
+        for (uint32_t j = dim_begin; j < dim_end; ++j) out[(size_t)(j - dim_begin) * nk + (k - k_begin)] = sob.get(j);
+        sob.advance(0, d, k);
+    }
+}
+
+__global__ void normals_hook_kernel(const uint32_t* __restrict__ vscr, const uint32_t* __restrict__ shift, int d,
+                                    uint64_t k_begin, uint64_t k_end, int method, uint64_t seed, uint32_t rep,
+                                    double* __restrict__ out) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    const int tpb_log2 = 7, tpb = 128, tid = threadIdx.x;
+    const uint64_t base = k_begin + (uint64_t)blockIdx.x * kCellPoints;
+    if (method == kLr) {
+        for (int a = 0; a < kCellPoints / tpb; ++a) {
+            const uint64_t k = base + tid + ((uint64_t)a << tpb_log2);
+            if (k >= k_end) break;
+            for (int jq = 0; jq < d; jq += 4) {
+                uint32_t c[4] = {(uint32_t)k, (uint32_t)(k >> 32), (uint32_t)(jq >> 2), (rep << 8) | 0x02u};
+                philox4x32_10(c, (uint32_t)seed, (uint32_t)(seed >> 32));
+                for (int w = 0; w < 4 && jq + w < d; ++w) out[(k - k_begin) * d + jq + w] = normal_from_u32(c[w]);
+            }
+        }
+        return;
+    }
+    uint32_t* ys = reinterpret_cast<uint32_t*>(smem_raw);
+    uint32_t* vt = ys + (size_t)d * tpb;
+    for (int idx = tid; idx < d * 32; idx += tpb) vt[idx] = vscr[idx];
+    __syncthreads();
+    SobolState sob{ys, vt, tpb_log2, tid};
+    sob.init(0, d, base + tid, shift);
+    for (int a = 0; a < kCellPoints / tpb; ++a) {
+        const uint64_t k = base + tid + ((uint64_t)a << tpb_log2);
+        if (k >= k_end) break;
+        for (int j = 0; j < d; ++j) out[(k - k_begin) * d + j] = normal_from_u32(sob.get(j));
+        sob.advance(0, d, k);
+    }
+}
+
+cudaError_t launch_sobol_hook(const uint32_t* d_vscr, const uint32_t* d_shift, int d, uint32_t dim_begin,
+                              uint32_t dim_end, uint64_t k_begin, uint64_t k_end, uint32_t* d_out,
+                              cudaStream_t st) {
+    const uint64_t nk = k_end - k_begin;
+    const unsigned grid = (unsigned)((nk + kCellPoints - 1) / kCellPoints);
+    const size_t smem = (size_t)d * 128 * 4 + (size_t)d * 32 * 4;
+    cudaError_t e = cudaFuncSetAttribute(sobol_hook_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    sobol_hook_kernel<<<grid, 128, smem, st>>>(d_vscr, d_shift, d, dim_begin, dim_end, k_begin, k_end, d_out);
+    ++launch_counter();
+    return cudaGetLastError();
+}
+
+cudaError_t launch_normals_hook(const uint32_t* d_vscr, const uint32_t* d_shift, int d, uint64_t k_begin,
+                                uint64_t k_end, int method, uint64_t seed, uint32_t rep, double* d_out,
+                                cudaStream_t st) {
+    const uint64_t nk = k_end - k_begin;
+    const unsigned grid = (unsigned)((nk + kCellPoints - 1) / kCellPoints);
+    const size_t smem = method == kLr ? 0 : (size_t)d * 128 * 4 + (size_t)d * 32 * 4;
+    cudaError_t e =
+        cudaFuncSetAttribute(normals_hook_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    normals_hook_kernel<<<grid, 128, smem, st>>>(d_vscr, d_shift, d, k_begin, k_end, method, seed, rep, d_out);
+    ++launch_counter();
+    return cudaGetLastError();
+}
+
+}  // namespace qmccpw
