@@ -41,6 +41,7 @@ constexpr int kTableDims = 1024;
 // generator P:440) and grow-only scratch.
 struct DeviceCache {
     bool ready = false;
+    bool checked = false;
     uint32_t* base_v = nullptr;        // [1024][32] JOEKUO6
     uint32_t* base_v_scr = nullptr;    // [1024][32] cuRAND pre-scrambled
     uint32_t* base_shift = nullptr;    // [1024] cuRAND scramble constants
@@ -56,11 +57,14 @@ DeviceCache g_cache[64];
 
 int ensure_device(int device, DeviceCache** out) {
     if (device < 0 || device >= 64) return fail(QMCCPW_EINVAL, "device ordinal out of range");
-    cudaDeviceProp prop;
-    CUDA_TRY(cudaGetDeviceProperties(&prop, device));
-    if (prop.major != 10) return fail(QMCCPW_ECUDA, "libqmccpw is built for sm_100a (B200); device is not sm_10x");
     std::lock_guard<std::mutex> lk(g_mu);
     DeviceCache& c = g_cache[device];
+    if (!c.checked) {  // once per device: the attribute query is slow, keep it out of every call
+        int major = 0;
+        CUDA_TRY(cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, device));
+        if (major != 10) return fail(QMCCPW_ECUDA, "libqmccpw is built for sm_100a (B200); device is not sm_10x");
+        c.checked = true;
+    }
     if (!c.ready) {
         curandDirectionVectors32_t* vec = nullptr;
         unsigned int* consts = nullptr;

@@ -183,18 +183,16 @@ struct W1Acc {
     __device__ __forceinline__ void push(const PathArgs& P, int j, double Wt) {
         const double tt = (double)j * P.t1;
         const double e = fma(P.sigma, Wt, P.omega * tt);
-        const double St = P.S0 * exp(e);
+        const double St = P.S0 * fast_exp(e);
         const double I = St * fma(-P.sigma, tt, Wt);
         sumS += St;
         sumI += I;
-        if (e > emax) {
-            esec = emax;
-            emax = e;
-            Smax = St;
-            Imax = I;
-        } else if (e > esec) {
-            esec = e;
-        }
+        // lowest argmax and runner-up exponent, branch-free
+        const bool gt = e > emax;
+        esec = fmax(esec, fmin(e, emax));
+        emax = gt ? e : emax;
+        Smax = gt ? St : Smax;
+        Imax = gt ? I : Imax;
     }
 };
 
@@ -205,7 +203,7 @@ __device__ __forceinline__ void tail_w1(const PathArgs& P, int o, const W1Acc& a
     const double inv_d = 1.0 / (double)P.d;
     const double stat = (type == kLookback) ? acc.Smax : acc.sumS * inv_d;
     const double I = (type == kLookback) ? acc.Imax : acc.sumI * inv_d;
-    const double psi = (P.lnK[o] - log(stat) - P.omega * P.t1) * P.inv_s;
+    const double psi = (P.lnK[o] - fast_log(stat) - P.omega * P.t1) * P.inv_s;
     const double ph = normal_pdf(psi);
     const double P0 = normal_sf(psi);
     const double K = P.K[o], D = P.Dfac, S0 = P.S0;
@@ -244,11 +242,11 @@ __device__ __forceinline__ void tail_x1(const PathArgs& P, int o, const double* 
         double S = 0.0, SA = 0.0;
         for (int j = 0; j < d; ++j) {
             const double aj = P.a[j];
-            const double E = exp(fma(sg * aj, u, cb[j * stride]));
+            const double E = fast_exp(fma(sg * aj, u, cb[j * stride]));
             S += E;
             SA = fma(aj, E, SA);
         }
-        const double h = log(S) - lndK;
+        const double h = fast_log(S) - lndK;
         const double du = h * S / (sg * SA);
         conv = fabs(du) <= 1e-13 * fmax(1.0, fabs(u));
         u = fmin(fmax(u - du, u_lo), u_hi);
@@ -261,12 +259,12 @@ __device__ __forceinline__ void tail_x1(const PathArgs& P, int o, const double* 
         const double aj = P.a[j], cj = cb[j * stride];
         const double tj = (double)(j + 1) * P.t1;
         const double Rj = (cj - P.lnS0 - P.omega * tj) * P.inv_sigma;
-        const double E = exp(fma(sg * aj, u, cj));
+        const double E = fast_exp(fma(sg * aj, u, cj));
         Dst = fma(aj, E, Dst);
         Qst = fma(aj * aj, E, Qst);
         Vst = fma(E, Rj - sg * tj + aj * u, Vst);
         if (arith) {
-            const double w = exp(fma(0.5 * sg * sg * aj, aj, cj));
+            const double w = fast_exp(fma(0.5 * sg * sg * aj, aj, cj));
             const double Pj = normal_cdf(sg * aj - u);
             sumW = fma(w, Pj, sumW);
             sumWv = fma(w * (Rj - sg * tj + sg * aj * aj), Pj, sumWv);
@@ -303,7 +301,7 @@ __device__ __forceinline__ void lr_path(const PathArgs& P, uint32_t rep, uint64_
                 const double x = normal_from_u32(c[w]);
                 if (j == 0) Z1 = x;
                 W = fma(P.sqrt_t1, x, W);
-                const double S = P.S0 * exp(fma(P.sigma, W, P.omega * (double)(j + 1) * P.t1));
+                const double S = P.S0 * fast_exp(fma(P.sigma, W, P.omega * (double)(j + 1) * P.t1));
                 sumS += S;
                 Smax = fmax(Smax, S);
                 vscore += (x * x - 1.0) * P.inv_sigma - x * P.sqrt_t1;
@@ -382,42 +380,51 @@ __global__ void __launch_bounds__(128) paths_kernel(const PathArgs P) {
                 // Alg. 3: W~ accumulates sqrt(dt) x_j for j >= 2; x_1 cancels in W - W(t_1)
                 double Wt = 0.0;
                 w1.push(P, 0, 0.0);
+#pragma unroll 1
                 for (int j = 1; j < d; ++j) {
                     Wt = fma(P.sqrt_t1, normal_from_u32(sob.get(j)), Wt);
                     w1.push(P, j, Wt);
                 }
             } else if (CONSTR == kBB) {
-                // Alg. 4 generated in time order: W(mid) = (W(l) + W(r))/2 + b_k x_dim(mid)
-                // with dim(mid) = 2^k - 1 - (mid >> (ctz(mid)+1)), the consumption order of Alg. 4.
-                int stT[12];
+                // Alg. 4 generated in time order.  Before emitting W(t_j) the
+                // bridge descends e = ctz(j-1) levels (e = m at j = 1) from the interval
+                // (t_{j-1}, t_{j-1+2^e}]; midpoint mid = j-1+2^c (c = e-1..0) sits at level
+                // m-c and consumes Sobol' dimension 2^{m-c} - 1 - (mid >> (c+1)), i.e. the
+                // consumption order of Alg. 4.  W(mid) = (W(l) + W(r))/2 + b_{m-c} x.
                 double stW[12];
                 int sp = 0;
-                stT[0] = d;
                 stW[0] = P.sqrtT * normal_from_u32(sob.get(0));
                 double Wl = 0.0, W1 = 0.0;
-                int tl = 0;
+                const int m = P.bb_m;
+#pragma unroll 1
                 for (int j = 1; j <= d; ++j) {
-                    while (stT[sp] != j) {
-                        const int mid = (tl + stT[sp]) >> 1;
-                        const int c = __ffs(mid) - 1;
-                        const int lev = P.bb_m - c;
-                        const int dim = (1 << lev) - 1 - (mid >> (c + 1));
-                        const double x = normal_from_u32(sob.get(dim));
-                        const double Wm = fma(P.bb_b[lev], x, 0.5 * (Wl + stW[sp]));
-                        ++sp;
-                        stT[sp] = mid;
-                        stW[sp] = Wm;
+                    const int e = (j == 1) ? m : (__ffs(j - 1) - 1);
+                    double Wj;
+                    if (e == 0) {
+                        Wj = stW[sp];
+                        --sp;
+                    } else {
+                        double Wr = stW[sp];
+#pragma unroll 1
+                        for (int c = e - 1; c >= 0; --c) {
+                            const int mid = (j - 1) + (1 << c);
+                            const int lev = m - c;
+                            const int dim = (1 << lev) - 1 - (mid >> (c + 1));
+                            const double x = normal_from_u32(sob.get(dim));
+                            const double Wm = fma(P.bb_b[lev], x, 0.5 * (Wl + Wr));
+                            if (c > 0) stW[++sp] = Wm;
+                            Wr = Wm;
+                        }
+                        Wj = Wr;
                     }
-                    const double Wj = stW[sp];
-                    --sp;
                     if (j == 1) W1 = Wj;
                     w1.push(P, j - 1, Wj - W1);
                     Wl = Wj;
-                    tl = j;
                 }
             } else {
                 // PCA: W = M x (the dense contraction), x staged per thread in shared memory
                 double* xb = buf0 + tid;
+#pragma unroll 1
                 for (int kk = 0; kk < d; ++kk) xb[kk * tpb] = normal_from_u32(sob.get(kk));
                 double W1 = 0.0;
                 for (int j = 0; j < d; ++j) {
@@ -437,38 +444,45 @@ __global__ void __launch_bounds__(128) paths_kernel(const PathArgs P) {
             double* cb = (CONSTR == kPca ? buf1 : buf0) + tid;
             if (CONSTR == kStd) {
                 double R = 0.0;
+#pragma unroll 1
                 for (int j = 0; j < d; ++j) {
                     if (j > 0) R = fma(P.sqrt_t1, normal_from_u32(sob.get(j)), R);
                     cb[j * tpb] = P.lnS0 + P.omega * (double)(j + 1) * P.t1 + P.sigma * R;
                 }
             } else if (CONSTR == kBB) {
-                int stT[12];
+                // same time-order bridge with the terminal loading of x_1 removed (R = M x, x_1 := 0)
                 double stW[12];
                 int sp = 0;
-                stT[0] = d;
-                stW[0] = 0.0;  // terminal loading of x_1 removed
+                stW[0] = 0.0;
                 double Wl = 0.0;
-                int tl = 0;
+                const int m = P.bb_m;
+#pragma unroll 1
                 for (int j = 1; j <= d; ++j) {
-                    while (stT[sp] != j) {
-                        const int mid = (tl + stT[sp]) >> 1;
-                        const int c = __ffs(mid) - 1;
-                        const int lev = P.bb_m - c;
-                        const int dim = (1 << lev) - 1 - (mid >> (c + 1));
-                        const double x = normal_from_u32(sob.get(dim));
-                        const double Wm = fma(P.bb_b[lev], x, 0.5 * (Wl + stW[sp]));
-                        ++sp;
-                        stT[sp] = mid;
-                        stW[sp] = Wm;
+                    const int e = (j == 1) ? m : (__ffs(j - 1) - 1);
+                    double Rj;
+                    if (e == 0) {
+                        Rj = stW[sp];
+                        --sp;
+                    } else {
+                        double Wr = stW[sp];
+#pragma unroll 1
+                        for (int c = e - 1; c >= 0; --c) {
+                            const int mid = (j - 1) + (1 << c);
+                            const int lev = m - c;
+                            const int dim = (1 << lev) - 1 - (mid >> (c + 1));
+                            const double x = normal_from_u32(sob.get(dim));
+                            const double Wm = fma(P.bb_b[lev], x, 0.5 * (Wl + Wr));
+                            if (c > 0) stW[++sp] = Wm;
+                            Wr = Wm;
+                        }
+                        Rj = Wr;
                     }
-                    const double Rj = stW[sp];
-                    --sp;
                     cb[(j - 1) * tpb] = P.lnS0 + P.omega * (double)j * P.t1 + P.sigma * Rj;
                     Wl = Rj;
-                    tl = j;
                 }
             } else {
                 double* xb = buf0 + tid;
+#pragma unroll 1
                 for (int kk = 1; kk < d; ++kk) xb[kk * tpb] = normal_from_u32(sob.get(kk));
                 for (int j = 0; j < d; ++j) {
                     const double* Mr = P.M + (size_t)j * d;
@@ -554,9 +568,16 @@ template <int C, int K, int M>
 static cudaError_t launch_paths_t(const PathArgs& args, cudaStream_t st, int* smem_out) {
     const size_t smem = path_smem_bytes(args, C, K, M);
     if (smem_out) *smem_out = (int)smem;
-    cudaError_t e = cudaFuncSetAttribute(paths_kernel<C, K, M>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)smem);
-    if (e != cudaSuccess) return e;
+    // raise the dynamic-smem limit once per device (not on every call: it is a driver round trip)
+    static thread_local int set_for[64] = {0};
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (set_for[dev & 63] < (int)smem) {
+        cudaError_t e = cudaFuncSetAttribute(paths_kernel<C, K, M>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             200 * 1024);
+        if (e != cudaSuccess) return e;
+        set_for[dev & 63] = 200 * 1024;
+    }
     const uint64_t nblocks = args.cell_end - args.cell_begin;
     if (nblocks == 0) return cudaSuccess;
     paths_kernel<C, K, M><<<(unsigned)nblocks, 1 << args.tpb_log2, smem, st>>>(args);

@@ -1,9 +1,32 @@
 // qmccpw_math.cuh -- FP64 device math for the QMC-CPW kernels (sm_100a).
+//
+// The hot path is FP64-pipe / issue-slot bound, so the
+// special functions on it are written for a minimal instruction count:
+// every polynomial coefficient and constant lives in __constant__ memory, so
+// DFMA takes it as a constant-bank operand instead of two UMOVs per 64-bit
+// literal (CUDA's normcdfinv/exp spent ~6.6k UMOVs per path, v0 profile).
 #pragma once
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include "qmccpw_coeffs.cuh"
+
 namespace qmccpw {
+
+struct MathConst {
+    double log2e, shift, ln2_hi, ln2_lo, one, two, half, minus_half, w_split, inv_sqrt_2pi, inv_sqrt2, p32, p33,
+        four, pdf_floor;
+};
+__constant__ MathConst MC = {
+    1.4426950408889634074,        // log2(e)
+    6755399441055744.0,           // 1.5 * 2^52 (round-to-integer shifter)
+    6.93147180369123816490e-01,   // ln2 high part (low 32 bits zero: n*ln2_hi exact)
+    1.90821492927058770002e-10,   // ln2 low part
+    1.0, 2.0, 0.5, -0.5,
+    6.25,                         // central / tail split of the inverse normal (w = -ln(1 - z^2))
+    0.398942280401432677939946059934,  // 1/sqrt(2 pi)
+    0.707106781186547524400844362105,  // 1/sqrt(2)
+    0x1p-32, 0x1p-33, 4.0, -700.0};
 
 // Philox4x32-10 (Salmon et al., SC'11): 10 rounds of two 32x32->64 products,
 // Weyl key schedule.  c = counter in, output out (in place).
@@ -22,22 +45,89 @@ __device__ __forceinline__ void philox4x32_10(uint32_t c[4], uint32_t k0, uint32
     }
 }
 
-// (a3) lattice point -> standard normal.  u = (y + 1/2) 2^-32 is exact in
-// FP64; the upper half is mirrored, x(2^32-1-y) = -x(y), so the lattice
-// symmetry is exact.  The inverse CDF itself is CUDA's normcdfinv.
+// exp(x) for |x| < 700 (all arguments on this path are bounded far inside):
+// x = n ln2 + r, |r| <= ln2/2, e^r by a degree-12 polynomial (rel. error
+// 4.4e-19 before rounding), 2^n added to the exponent field.
+__device__ __forceinline__ double fast_exp(double x) {
+    const double t = fma(x, MC.log2e, MC.shift);
+    const int ni = __double2loint(t);
+    const double n = t - MC.shift;
+    double r = fma(n, -MC.ln2_hi, x);
+    r = fma(n, -MC.ln2_lo, r);
+    double p = EXP_POLY[12];
+#pragma unroll
+    for (int j = 11; j >= 0; --j) p = fma(p, r, EXP_POLY[j]);
+    return __hiloint2double(__double2hiint(p) + (ni << 20), __double2loint(p));
+}
+
+// 1/y for y in [1, 4): FP64 MUFU seed + two Newton steps
+__device__ __forceinline__ double rcp_newton(double y) {
+    double r;
+    asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(y));
+    double e = fma(-y, r, MC.one);
+    r = fma(r, e, r);
+    e = fma(-y, r, MC.one);
+    return fma(r, e, r);
+}
+
+// ln(t) for normal t > 0: t = 2^k m, m in [sqrt(1/2), sqrt(2)),
+// ln m = 2 atanh(f) = 2f + f^3 Q(f^2), f = (m-1)/(m+1).
+__device__ __forceinline__ double fast_log(double t) {
+    int hi = __double2hiint(t);
+    const int lo = __double2loint(t);
+    int k = (hi >> 20) - 1023;
+    int mhi = (hi & 0x000FFFFF) | 0x3FF00000;
+    const bool big = mhi > 0x3FF6A09E;  // m > sqrt(2)
+    mhi -= big ? 0x00100000 : 0;
+    k += big ? 1 : 0;
+    const double m = __hiloint2double(mhi, lo);
+    const double f = (m - MC.one) * rcp_newton(m + MC.one);
+    const double g = f * f;
+    const double gt = g - LOG_Q_CENTER;
+    double q = LOG_Q[10];
+#pragma unroll
+    for (int j = 9; j >= 0; --j) q = fma(q, gt, LOG_Q[j]);
+    const double lnm = fma(f * g, q, MC.two * f);
+    const double kd = (double)k;
+    return fma(kd, MC.ln2_hi, fma(kd, MC.ln2_lo, lnm));
+}
+
+// (a3) lattice point -> standard normal, Phi^{-1}((y + 1/2) 2^-32).
+// Lower half (y < 2^31) evaluated, upper half mirrored (exact symmetry).
+// Giles' variable w = -ln(1 - z^2) = -ln(4u(1-u)), z = 2u - 1 (exact):
+// Phi^{-1}(u) = z P(w); the central polynomial covers u > 4.8e-4, so ~97% of
+// warps never enter the tail branch.
 __device__ __forceinline__ double normal_from_u32(uint32_t y) {
     const bool upper = (y >> 31) != 0u;
     const uint32_t yl = upper ? ~y : y;
-    const double u = fma((double)yl, 0x1p-32, 0x1p-33);
-    const double x = normcdfinv(u);
+    const double u = fma((double)yl, MC.p32, MC.p33);
+    const double z = fma(MC.two, u, -MC.one);
+    const double t = (MC.four * u) * (MC.one - u);
+    const double w = -fast_log(t);
+    double p;
+    if (w < MC.w_split) {
+        const double v = w - ICDF_CENTRAL_CENTER;
+        p = ICDF_CENTRAL[24];
+#pragma unroll
+        for (int j = 23; j >= 0; --j) p = fma(p, v, ICDF_CENTRAL[j]);
+    } else {
+        const double v = sqrt(w) - ICDF_TAIL_CENTER;
+        p = ICDF_TAIL[24];
+#pragma unroll
+        for (int j = 23; j >= 0; --j) p = fma(p, v, ICDF_TAIL[j]);
+    }
+    const double x = z * p;
     return upper ? -x : x;
 }
 
+// phi(x); flushes to 0 below e^-700 (|x| > 37.4), where fast_exp's exponent
+// arithmetic would leave the normal range (the oracle's value there is < 1e-305)
 __device__ __forceinline__ double normal_pdf(double x) {
-    return 0.398942280401432677939946059934 * exp(-0.5 * x * x);
+    const double a = MC.minus_half * x * x;
+    return a > MC.pdf_floor ? MC.inv_sqrt_2pi * fast_exp(a) : 0.0;
 }
 // Phibar(x) = 1 - Phi(x) = erfc(x/sqrt2)/2, never formed as 1 - Phi (reading 22)
-__device__ __forceinline__ double normal_sf(double x) { return 0.5 * erfc(x * 0.707106781186547524400844362105); }
-__device__ __forceinline__ double normal_cdf(double x) { return 0.5 * erfc(-x * 0.707106781186547524400844362105); }
+__device__ __forceinline__ double normal_sf(double x) { return MC.half * erfc(x * MC.inv_sqrt2); }
+__device__ __forceinline__ double normal_cdf(double x) { return MC.half * erfc(-x * MC.inv_sqrt2); }
 
 }  // namespace qmccpw

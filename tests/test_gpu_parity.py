@@ -2,9 +2,13 @@
 seeded points.  Tolerances:
   Sobol' integers        bit-exact
   normals                |dx| <= 2e-15 max(1, |x|)
-  per-path values        |df| <= 1e-12 (|f| + |pivot|)
+  per-path values        |df| <= 1e-12 (|f| + |pivot|); gamma x max(1, 0.03/(sigma^2 t_1))
+                         (the threshold psi / u* carries an absolute rounding of
+                         ~c eps / (sigma sqrt t_1), c <~ 30 measured, and gamma
+                         differentiates it once more -> relative ~ c eps / s^2)
   replicate / run means  |dC| <= 1e-9 sqrt(within_var + C^2)   (>= mean|f|)
-  SE, sigma_run          <= 1e-6 relative
+  SE, sigma_run          <= 1e-6 relative (+ a 1e-12 x scale floor: at d = 1 the
+                         estimator is exact per path and the spread is rounding)
   counters               equal
 """
 import math
@@ -84,8 +88,10 @@ def _pv_check(q, O, otype, K, d, constr, cond, method, rep, k0, k1, S0=W.S0, sig
     o = O.path_values(otype, K, mk, ocfg(O, constr, cond, method), rep, k0, k1)
     piv = np.abs(O.pivots(otype, K, mk))
     err = np.abs(g - o) / (np.abs(o) + piv)
-    assert np.all(err <= 1e-12), (otype, K, d, constr, cond, method, float(err.max()),
-                                  np.unravel_index(np.argmax(err), err.shape))
+    s2 = sigma * sigma * T / d
+    tol = np.array([1e-12, 1e-12, 1e-12, 1e-12 * max(1.0, 0.03 / s2)])
+    assert np.all(err <= tol), (otype, K, d, constr, cond, method, err.max(axis=0),
+                                np.unravel_index(np.argmax(err / tol), err.shape))
 
 
 @pytest.mark.parametrize("constr,cond", MODES_ALL)
@@ -119,8 +125,8 @@ def _means_check(gres, ores):
         scale = np.sqrt(np.maximum(orr["within_var"], 0) + orr["mean"] ** 2)
         assert np.all(np.abs(g["mean"] - orr["mean"]) <= 1e-9 * scale), (g["mean"], orr["mean"])
         if orr["n_replicates"] > 1:
-            assert np.allclose(g["se"], orr["se"], rtol=1e-6, atol=1e-300)
-            assert np.allclose(g["sigma_run"], orr["sigma_run"], rtol=1e-6, atol=1e-300)
+            assert np.all(np.abs(g["se"] - orr["se"]) <= 1e-6 * orr["se"] + 1e-12 * scale), (g["se"], orr["se"])
+            assert np.all(np.abs(g["sigma_run"] - orr["sigma_run"]) <= 1e-6 * orr["sigma_run"] + 1e-12 * scale)
         else:
             assert np.all(np.isnan(g["se"]))
         assert np.allclose(g["within_var"], orr["within_var"], rtol=1e-7, atol=1e-12 * scale ** 2)
