@@ -184,6 +184,14 @@ int qmccpw_normals(uint32_t replicate, int32_t d, uint64_t k_begin, uint64_t k_e
 int qmccpw_path_values(int32_t option, const qmccpw_params* p, uint32_t replicate, uint64_t k_begin,
                        uint64_t k_end, const qmccpw_config* cfg, double* out);
 
+/* ---- measurement -------------------------------------------------------- */
+/* FP64 roof microbenchmarks on `device`: DFMA TFLOP/s at
+ * full occupancy (independent chains), dependent-DFMA latency in SM cycles,
+ * FP64 tensor-core (mma.sync m8n8k4, SASS DMMA) TFLOP/s, and the device's
+ * nominal SM clock in MHz.  Outputs are host pointers. */
+int qmccpw_fp64_roof(int32_t device, double* dfma_tflops, double* dfma_latency_cycles, double* dmma_tflops,
+                     double* sm_clock_mhz);
+
 /* ---- housekeeping ----------------------------------------------------- */
 const char* qmccpw_last_error(void); /* thread-local; valid until the next call on this thread */
 void qmccpw_release(int32_t device);  /* frees cached device tables/scratch (-1: all devices) */

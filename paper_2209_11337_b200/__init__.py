@@ -99,6 +99,7 @@ def lib():
                                      f64p]
         L.qmccpw_path_values.argtypes = [ctypes.c_int32, P(Params), ctypes.c_uint32, ctypes.c_uint64,
                                          ctypes.c_uint64, P(Config), f64p]
+        L.qmccpw_fp64_roof.argtypes = [ctypes.c_int32, f64p, f64p, f64p, f64p]
         L.qmccpw_last_error.restype = ctypes.c_char_p
         L.qmccpw_release.argtypes = [ctypes.c_int32]
         L.qmccpw_release.restype = None
@@ -187,6 +188,13 @@ def qmccpw_path_values(option, p, replicate, k_begin, k_end, cfg=None):
     _check(lib().qmccpw_path_values(option, ctypes.byref(p), replicate, k_begin, k_end, _cfg(cfg),
                                     out.ctypes.data_as(ctypes.POINTER(ctypes.c_double))))
     return out
+
+
+def qmccpw_fp64_roof(device=0):
+    vals = [ctypes.c_double() for _ in range(4)]
+    _check(lib().qmccpw_fp64_roof(device, *[ctypes.byref(v) for v in vals]))
+    return dict(dfma_tflops=vals[0].value, dfma_latency_cycles=vals[1].value, dmma_tflops=vals[2].value,
+                sm_clock_mhz=vals[3].value)
 
 
 def qmccpw_last_error():

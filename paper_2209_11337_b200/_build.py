@@ -5,7 +5,7 @@ import subprocess
 PKG = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
-SOURCES = [os.path.join(CSRC, f) for f in ("qmccpw_kernels.cu", "qmccpw_api.cu")]
+SOURCES = [os.path.join(CSRC, f) for f in ("qmccpw_kernels.cu", "qmccpw_api.cu", "qmccpw_microbench.cu")]
 HEADERS = [os.path.join(CSRC, f) for f in ("qmccpw_internal.h", "qmccpw_math.cuh")] + \
     [os.path.join(ROOT, "include", "qmccpw.h")]
 LIB = os.path.join(PKG, "libqmccpw.so")

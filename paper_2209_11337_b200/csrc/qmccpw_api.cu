@@ -177,14 +177,16 @@ void bs_pivots(int type, const qmccpw_params& p, double out[4]) {
     }
 }
 
-int tpb_log2_for(const qmccpw_config& c, int d) {
+int tpb_log2_for(const qmccpw_config& c, int d, int n_opt) {
     const bool need_buf = c.method == QMCCPW_QMC_CPW && (c.construction == QMCCPW_PCA || c.conditioning == QMCCPW_COND_X1);
     const bool two_buf = c.method == QMCCPW_QMC_CPW && c.construction == QMCCPW_PCA && c.conditioning == QMCCPW_COND_X1;
     for (int lg = 7; lg >= 5; --lg) {
-        size_t tpb = (size_t)1 << lg, b = 1024;
+        size_t tpb = (size_t)1 << lg, nw = tpb / 32;
+        size_t b = (size_t)n_opt * 8 * tpb * 8;
         if (need_buf) b += (size_t)d * tpb * 8;
         if (two_buf) b += (size_t)d * tpb * 8;
-        b += (size_t)d * tpb * 4 + (size_t)d * 128;
+        const size_t hw = 4 * nw * d * 4;
+        b += ((size_t)d * 64 + d) * 4 + 4 + (hw > 1024 ? hw : 1024);
         if (b <= 200 * 1024) return lg;
     }
     return 5;
@@ -317,7 +319,7 @@ PathArgs make_args(const Plan& pl, const Scratch& s) {
     const int d = pl.d;
     a.d = d;
     a.n_opt = pl.n_opt;
-    a.tpb_log2 = tpb_log2_for(pl.cfg, d);
+    a.tpb_log2 = tpb_log2_for(pl.cfg, d, pl.n_opt);
     const bool skip_x1 = pl.cfg.method == QMCCPW_QMC_CPW &&
                          ((pl.cfg.construction == QMCCPW_STD && pl.cfg.conditioning == QMCCPW_COND_W1) ||
                           pl.cfg.conditioning == QMCCPW_COND_X1);
@@ -344,6 +346,22 @@ PathArgs make_args(const Plan& pl, const Scratch& s) {
     while ((1 << m) < d) ++m;
     a.bb_m = m;
     for (int k = 1; k <= m && k < 16; ++k) a.bb_b[k] = std::sqrt(p.T / std::ldexp(1.0, k + 1));
+    if ((1 << m) == d) {
+        // Alg. 4: dimension 0 is the terminal; at level k the 2^{k-1} intervals are
+        // filled right to left, interval jj consuming dimension 2^k - 1 - jj.  The time-order
+        // generator meets midpoint mid = (2 jj + 1) 2^{m-k} when it first needs W(mid).
+        int n = 0;
+        a.bb_seq[n++] = 0;
+        for (int j = 1; j <= d; ++j) {
+            const int e = (j == 1) ? m : __builtin_ctz(j - 1);
+            for (int c = e - 1; c >= 0; --c) {
+                const int mid = (j - 1) + (1 << c);
+                const int lev = m - c;
+                a.bb_seq[n++] = (uint8_t)((1 << lev) - 1 - (mid >> (c + 1)));
+            }
+        }
+        for (; n < kMaxDimGpu + 2; ++n) a.bb_seq[n] = a.bb_seq[n - 1];
+    }
     for (int o = 0; o < pl.n_opt; ++o) {
         a.type[o] = pl.types[o];
         a.K[o] = pl.p[o].K;

@@ -46,6 +46,8 @@ struct PathArgs {
     double sqrtT;
     double bb_b[16];         // b_k = sqrt(T / 2^{k+1}), k = 1..m (index k)
     int bb_m;
+    uint8_t bb_seq[kMaxDimGpu + 2];  // Sobol' dimension of the i-th normal consumed by the time-order
+                                     // bridge (Alg. 4's consumption order), padded by repetition
     // options
     int type[kMaxOpt];
     double K[kMaxOpt];

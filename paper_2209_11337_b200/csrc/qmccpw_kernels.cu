@@ -134,38 +134,62 @@ cudaError_t launch_path_matrix(int construction, int d, double T, double sigma, 
 }
 
 // ---------------------------------------------------------------------------
-// Per-thread Sobol' state (a2).  Thread tau of a 2^p-thread block visits the
-// points k, k + 2^p, k + 2^(p+1), ...; with A = k >> p the Gray code satisfies
-// g(k + 2^p) = g(k) ^ (1 << (p-1)) ^ (1 << (p + ctz(A+1))), so each dimension
-// advances by two XORs of the replicate's direction numbers.
+// (a2) Sobol' integers without per-thread state.  A block of 2^p threads visits
+// the points k = K0 + tid + a 2^p (a = 0, 1, ...).  With k = A 2^p + tau and
+// tau = 32 w + l (l the lane slot), the Gray code g(k) = k ^ (k >> 1) splits as
+//   g(k) = (g(A) << p) ^ ((A & 1) << (p-1)) ^ g(l) ^ ((w & 1) << 4) ^ (g(w) << 5)
+// (P:147-151 XOR form), so y_j(k) = HW_j(A, w) ^ G_j(l) with
+//   G_j(l)    = XOR_{b in g(l)} v'_{j,b}                       (per block,  [d][32])
+//   HW_j(A,w) = c_j ^ XOR_{b in g(A)} v'_{j,p+b} ^ (A&1) v'_{j,p-1}
+//               ^ (w&1) v'_{j,4} ^ XOR_{b in g(w)} v'_{j,5+b}      (per point iteration)
+// Threads of a block share A up to +1 (first index not 2^p-aligned), so HW is
+// built for A and A+1 (f = 0, 1).  Per dimension a thread does two
+// shared-memory loads and one XOR; nothing is stored per thread.
 // ---------------------------------------------------------------------------
-struct SobolState {
-    uint32_t* ys;        // smem [d][tpb]
-    const uint32_t* vt;  // smem [d][32]
-    int tpb_log2;
-    int tid;
-    __device__ __forceinline__ uint32_t get(int j) const { return ys[(j << tpb_log2) + tid]; }
-    __device__ __forceinline__ void init(int j0, int d, uint64_t k, const uint32_t* __restrict__ shift) {
-        const uint32_t g = (uint32_t)(k ^ (k >> 1));
-        for (int j = j0; j < d; ++j) {
-            uint32_t y = shift[j];
-            uint32_t gg = g;
-            while (gg) {
-                const int b = __ffs(gg) - 1;
-                y ^= vt[j * 32 + b];
-                gg &= gg - 1;
-            }
-            ys[(j << tpb_log2) + tid] = y;
-        }
-    }
-    __device__ __forceinline__ void advance(int j0, int d, uint64_t k) {
-        const uint64_t A = k >> tpb_log2;
-        int c = __ffsll((long long)(A + 1)) - 1;
-        if (tpb_log2 + c > 31) c = 31 - tpb_log2;  // only reached past the last valid point
-        const int b0 = tpb_log2 - 1, b1 = tpb_log2 + c;
-        for (int j = j0; j < d; ++j) ys[(j << tpb_log2) + tid] ^= vt[j * 32 + b0] ^ vt[j * 32 + b1];
-    }
+struct SobolBlock {
+    const uint32_t* G;   // smem [d][32]
+    const uint32_t* HW;  // smem, current buffer [2][nw][d]
+    int d, nw;
+    int lane_t, w_t, f_t;
+    __device__ __forceinline__ uint32_t get(int j) const { return HW[(f_t * nw + w_t) * d + j] ^ G[j * 32 + lane_t]; }
 };
+
+__device__ __forceinline__ void sobol_build_g(const uint32_t* vt, int d, uint32_t* G, int tid, int tpb) {
+    for (int idx = tid; idx < d * 32; idx += tpb) {
+        const int j = idx >> 5, l = idx & 31;
+        const int g = l ^ (l >> 1);
+        uint32_t y = 0;
+#pragma unroll
+        for (int b = 0; b < 5; ++b)
+            if ((g >> b) & 1) y ^= vt[j * 32 + b];
+        G[idx] = y;
+    }
+}
+
+__device__ __forceinline__ void sobol_build_hw(const uint32_t* vt, const uint32_t* sh, int d, int j0, int p, int nw,
+                                               uint64_t A0, uint32_t* HW, int tid, int tpb) {
+    const int n = 2 * nw * d;
+    for (int idx = tid; idx < n; idx += tpb) {
+        const int j = idx % d, rest = idx / d;
+        if (j < j0) continue;
+        const int w = rest % nw, f = rest / nw;
+        const uint64_t A = A0 + (uint64_t)f;
+        const uint32_t* v = vt + j * 32;
+        uint32_t y = sh[j];
+        if (A & 1) y ^= v[p - 1];
+        if (w & 1) y ^= v[4];
+        const int gw = w ^ (w >> 1);
+        if (gw & 1) y ^= v[5];
+        if (gw & 2) y ^= v[6];
+        uint32_t gA = (uint32_t)(A ^ (A >> 1)) & ((p >= 32) ? 0u : (0xFFFFFFFFu >> p));
+        while (gA) {
+            const int b = __ffs(gA) - 1;
+            y ^= v[p + b];
+            gA &= gA - 1;
+        }
+        HW[idx] = y;
+    }
+}
 
 // ---------------------------------------------------------------------------
 // (a5) W1-mode accumulators over the separated path S~(t_j):
@@ -193,6 +217,44 @@ struct W1Acc {
         emax = gt ? e : emax;
         Smax = gt ? St : Smax;
         Imax = gt ? I : Imax;
+    }
+    __device__ __forceinline__ void take(double e, double St, double I) {
+        sumS += St;
+        sumI += I;
+        const bool gt = e > emax;
+        esec = fmax(esec, fmin(e, emax));
+        emax = gt ? e : emax;
+        Smax = gt ? St : Smax;
+        Imax = gt ? I : Imax;
+    }
+    // dates j and j+1 together (paired exp)
+    __device__ __forceinline__ void push2(const PathArgs& P, int j, double Wa, double Wb) {
+        const double ta = (double)j * P.t1, tb = (double)(j + 1) * P.t1;
+        const double ea = fma(P.sigma, Wa, P.omega * ta), eb = fma(P.sigma, Wb, P.omega * tb);
+        double Xa, Xb;
+        fast_exp_x2(ea, eb, Xa, Xb);
+        const double Sa = P.S0 * Xa, Sb = P.S0 * Xb;
+        take(ea, Sa, Sa * fma(-P.sigma, ta, Wa));
+        take(eb, Sb, Sb * fma(-P.sigma, tb, Wb));
+    }
+};
+
+// Two-slot FIFO of standard normals drawn in a fixed dimension order, two
+// lattice points per refill (normal_from_u32_x2): the construction loops
+// consume one normal at a time while the special functions run paired.
+struct NormalFifo {
+    double x0, x1;
+    int have;
+    __device__ __forceinline__ void reset() { have = 0; }
+    template <class DimAt>
+    __device__ __forceinline__ double next(const SobolBlock& sob, DimAt dim_at) {
+        if (have == 0) {
+            normal_from_u32_x2(sob.get(dim_at(0)), sob.get(dim_at(1)), x0, x1);
+            have = 2;
+        }
+        const double r = (have == 2) ? x0 : x1;
+        --have;
+        return r;
     }
 };
 
@@ -240,7 +302,18 @@ __device__ __forceinline__ void tail_x1(const PathArgs& P, int o, const double* 
     bool conv = false;
     for (int it = 0; it < kNewtonMax; ++it) {
         double S = 0.0, SA = 0.0;
-        for (int j = 0; j < d; ++j) {
+        int j = 0;
+#pragma unroll 1
+        for (; j + 1 < d; j += 2) {
+            const double aa = P.a[j], ab = P.a[j + 1];
+            double Ea, Eb;
+            fast_exp_x2(fma(sg * aa, u, cb[j * stride]), fma(sg * ab, u, cb[(j + 1) * stride]), Ea, Eb);
+            S += Ea;
+            SA = fma(aa, Ea, SA);
+            S += Eb;
+            SA = fma(ab, Eb, SA);
+        }
+        if (j < d) {
             const double aj = P.a[j];
             const double E = fast_exp(fma(sg * aj, u, cb[j * stride]));
             S += E;
@@ -294,11 +367,14 @@ __device__ __forceinline__ void lr_path(const PathArgs& P, uint32_t rep, uint64_
     for (int jq = 0; jq < d; jq += 4) {
         uint32_t c[4] = {(uint32_t)k, (uint32_t)(k >> 32), (uint32_t)(jq >> 2), (rep << 8) | 0x02u};
         philox4x32_10(c, (uint32_t)P.seed, (uint32_t)(P.seed >> 32));
+        double xs[4];
+        normal_from_u32_x2(c[0], c[1], xs[0], xs[1]);
+        if (jq + 2 < d) normal_from_u32_x2(c[2], c[3], xs[2], xs[3]);
 #pragma unroll
         for (int w = 0; w < 4; ++w) {
             const int j = jq + w;
             if (j < d) {
-                const double x = normal_from_u32(c[w]);
+                const double x = xs[w];
                 if (j == 0) Z1 = x;
                 W = fma(P.sqrt_t1, x, W);
                 const double S = P.S0 * fast_exp(fma(P.sigma, W, P.omega * (double)(j + 1) * P.t1));
@@ -343,31 +419,46 @@ __global__ void __launch_bounds__(128) paths_kernel(const PathArgs P) {
     constexpr bool kNeedBuf = (METHOD == kQmc) && (CONSTR == kPca || COND == kX1);
     constexpr bool kTwoBuf = (METHOD == kQmc) && (CONSTR == kPca && COND == kX1);
 
-    // shared memory carve-up: [red: 4 warps x 32 doubles][buf0][buf1][ys][vt]
-    double* red = reinterpret_cast<double*>(smem_raw);
-    double* buf0 = red + 4 * 32;
+    // shared memory carve-up (8-byte aligned first):
+    //   acc [n_opt*8][tpb] | buf0, buf1 [d][tpb] | vt [d][32] | sh [d] | G [d][32] | pad | HW [2][2][nw][d] (>= 1 KB)
+    // the reduction scratch red [4 warps][32] aliases HW after the point loop.
+    const int nw = tpb >> 5;
+    const int n_acc = P.n_opt * 8;
+    double* accs = reinterpret_cast<double*>(smem_raw);
+    double* buf0 = accs + (size_t)n_acc * tpb;
     double* buf1 = buf0 + (kNeedBuf ? (size_t)d * tpb : 0);
-    uint32_t* ys = reinterpret_cast<uint32_t*>(buf1 + (kTwoBuf ? (size_t)d * tpb : 0));
-    uint32_t* vt = ys + (METHOD == kQmc ? (size_t)d * tpb : 0);
+    uint32_t* vt = reinterpret_cast<uint32_t*>(buf1 + (kTwoBuf ? (size_t)d * tpb : 0));
+    uint32_t* sh = vt + (METHOD == kQmc ? (size_t)d * 32 : 0);
+    uint32_t* G = sh + (METHOD == kQmc ? d : 0);
+    uint32_t* HW = G + (METHOD == kQmc ? (size_t)d * 32 : 0);
+    HW += ((uintptr_t)HW & 7) ? 1 : 0;
+    double* red = reinterpret_cast<double*>(HW);
+    const int hw_size = 2 * nw * d;
 
-    SobolState sob{ys, vt, tpb_log2, tid};
+    const uint64_t K0 = P.point_offset + i0;
+    const uint64_t Ab = K0 >> tpb_log2;
+    const uint64_t kt = K0 + (uint64_t)tid;
+    SobolBlock sob{G, HW, d, nw, (int)(kt & 31), (int)((kt >> 5) & (uint64_t)(nw - 1)), (int)((kt >> tpb_log2) - Ab)};
     if (METHOD == kQmc) {
         const uint32_t* src = P.vscr + (size_t)rep_local * d * 32;
         for (int idx = tid; idx < d * 32; idx += tpb) vt[idx] = src[idx];
+        for (int idx = tid; idx < d; idx += tpb) sh[idx] = P.shift[(size_t)rep_local * d + idx];
         __syncthreads();
-        sob.init(P.dim_begin, d, P.point_offset + i0 + tid, P.shift + (size_t)rep_local * d);
+        sobol_build_g(vt, d, G, tid, tpb);
     }
-
-    double acc1[kMaxOpt][4], acc2[kMaxOpt][4];
-#pragma unroll
-    for (int o = 0; o < kMaxOpt; ++o)
-#pragma unroll
-        for (int q = 0; q < 4; ++q) acc1[o][q] = acc2[o][q] = 0.0;
+    for (int v = 0; v < n_acc; ++v) accs[v * tpb + tid] = 0.0;
     unsigned unconverged = 0, ties = 0;
 
     for (int a = 0; a < ppt; ++a) {
+        if (i0 + ((uint64_t)a << tpb_log2) >= P.n_points) break;  // block-uniform: ragged last cell
+        if (METHOD == kQmc) {
+            uint32_t* HWb = HW + (a & 1) * hw_size;  // double-buffered: one barrier per iteration
+            sobol_build_hw(vt, sh, d, P.dim_begin, tpb_log2, nw, Ab + (uint64_t)a, HWb, tid, tpb);
+            __syncthreads();
+            sob.HW = HWb;
+        }
         const uint64_t i = i0 + tid + ((uint64_t)a << tpb_log2);
-        if (i >= P.n_points) break;
+        if (i >= P.n_points) continue;
         const uint64_t k = P.point_offset + i;
         double f[kMaxOpt][4];
 
@@ -377,11 +468,20 @@ __global__ void __launch_bounds__(128) paths_kernel(const PathArgs P) {
             W1Acc w1;
             w1.reset();
             if (CONSTR == kStd) {
-                // Alg. 3: W~ accumulates sqrt(dt) x_j for j >= 2; x_1 cancels in W - W(t_1)
+                // Alg. 3: W~ accumulates sqrt(dt) x_j for j >= 2; x_1 cancels in
+                // W - W(t_1).  Normals and exps two dates at a time.
                 double Wt = 0.0;
                 w1.push(P, 0, 0.0);
+                int j = 1;
 #pragma unroll 1
-                for (int j = 1; j < d; ++j) {
+                for (; j + 1 < d; j += 2) {
+                    double xa, xb;
+                    normal_from_u32_x2(sob.get(j), sob.get(j + 1), xa, xb);
+                    const double Wa = fma(P.sqrt_t1, xa, Wt);
+                    Wt = fma(P.sqrt_t1, xb, Wa);
+                    w1.push2(P, j, Wa, Wt);
+                }
+                if (j < d) {
                     Wt = fma(P.sqrt_t1, normal_from_u32(sob.get(j)), Wt);
                     w1.push(P, j, Wt);
                 }
@@ -389,12 +489,17 @@ __global__ void __launch_bounds__(128) paths_kernel(const PathArgs P) {
                 // Alg. 4 generated in time order.  Before emitting W(t_j) the
                 // bridge descends e = ctz(j-1) levels (e = m at j = 1) from the interval
                 // (t_{j-1}, t_{j-1+2^e}]; midpoint mid = j-1+2^c (c = e-1..0) sits at level
-                // m-c and consumes Sobol' dimension 2^{m-c} - 1 - (mid >> (c+1)), i.e. the
-                // consumption order of Alg. 4.  W(mid) = (W(l) + W(r))/2 + b_{m-c} x.
+                // m-c and consumes the next Sobol' dimension of Alg. 4's order (bb_seq, built
+                // on the host); W(mid) = (W(l) + W(r))/2 + b_{m-c} x.
+                NormalFifo fifo;
+                fifo.reset();
+                int pos = 0;
+                auto dim_at = [&](int o) { return (int)P.bb_seq[pos + o]; };
                 double stW[12];
                 int sp = 0;
-                stW[0] = P.sqrtT * normal_from_u32(sob.get(0));
-                double Wl = 0.0, W1 = 0.0;
+                stW[0] = P.sqrtT * fifo.next(sob, dim_at);
+                pos += 2;
+                double Wl = 0.0, W1 = 0.0, Wpend = 0.0;
                 const int m = P.bb_m;
 #pragma unroll 1
                 for (int j = 1; j <= d; ++j) {
@@ -407,32 +512,59 @@ __global__ void __launch_bounds__(128) paths_kernel(const PathArgs P) {
                         double Wr = stW[sp];
 #pragma unroll 1
                         for (int c = e - 1; c >= 0; --c) {
-                            const int mid = (j - 1) + (1 << c);
-                            const int lev = m - c;
-                            const int dim = (1 << lev) - 1 - (mid >> (c + 1));
-                            const double x = normal_from_u32(sob.get(dim));
-                            const double Wm = fma(P.bb_b[lev], x, 0.5 * (Wl + Wr));
+                            const bool refill = fifo.have == 0;
+                            const double x = fifo.next(sob, dim_at);
+                            pos += refill ? 2 : 0;
+                            const double Wm = fma(P.bb_b[m - c], x, 0.5 * (Wl + Wr));
                             if (c > 0) stW[++sp] = Wm;
                             Wr = Wm;
                         }
                         Wj = Wr;
                     }
                     if (j == 1) W1 = Wj;
-                    w1.push(P, j - 1, Wj - W1);
+                    if (j & 1) {
+                        Wpend = Wj - W1;
+                    } else {
+                        w1.push2(P, j - 2, Wpend, Wj - W1);
+                    }
                     Wl = Wj;
                 }
+                if (d & 1) w1.push(P, d - 1, Wpend);
             } else {
-                // PCA: W = M x (the dense contraction), x staged per thread in shared memory
+                // PCA: W = M x (the dense contraction), x staged per thread in shared memory,
+                // two rows of M per pass so every x load feeds two DFMAs
                 double* xb = buf0 + tid;
+                int kk = 0;
 #pragma unroll 1
-                for (int kk = 0; kk < d; ++kk) xb[kk * tpb] = normal_from_u32(sob.get(kk));
+                for (; kk + 1 < d; kk += 2) {
+                    double xa, xc;
+                    normal_from_u32_x2(sob.get(kk), sob.get(kk + 1), xa, xc);
+                    xb[kk * tpb] = xa;
+                    xb[(kk + 1) * tpb] = xc;
+                }
+                if (kk < d) xb[kk * tpb] = normal_from_u32(sob.get(kk));
                 double W1 = 0.0;
-                for (int j = 0; j < d; ++j) {
-                    const double* Mr = P.M + (size_t)j * d;
-                    double W = 0.0;
-                    for (int kk = 0; kk < d; ++kk) W = fma(__ldg(Mr + kk), xb[kk * tpb], W);
-                    if (j == 0) W1 = W;
-                    w1.push(P, j, W - W1);
+                int j = 0;
+#pragma unroll 1
+                for (; j + 1 < d; j += 2) {
+                    const double* Ma = P.M + (size_t)j * d;
+                    const double* Mb = Ma + d;
+                    double Wa = 0.0, Wb = 0.0;
+#pragma unroll 4
+                    for (int q = 0; q < d; ++q) {
+                        const double xq = xb[q * tpb];
+                        Wa = fma(__ldg(Ma + q), xq, Wa);
+                        Wb = fma(__ldg(Mb + q), xq, Wb);
+                    }
+                    if (j == 0) W1 = Wa;
+                    w1.push2(P, j, Wa - W1, Wb - W1);
+                }
+                if (j < d) {
+                    const double* Ma = P.M + (size_t)j * d;
+                    double Wa = 0.0;
+                    for (int q = 0; q < d; ++q) Wa = fma(__ldg(Ma + q), xb[q * tpb], Wa);
+                    if (j == 0) W1 = Wa;
+                    w1.push(P, j, Wa - W1);
                 }
             }
             if (w1.emax - w1.esec < 1e-12) ++ties;  // only meaningful for the lookback
@@ -444,13 +576,28 @@ __global__ void __launch_bounds__(128) paths_kernel(const PathArgs P) {
             double* cb = (CONSTR == kPca ? buf1 : buf0) + tid;
             if (CONSTR == kStd) {
                 double R = 0.0;
+                cb[0] = P.lnS0 + P.omega * P.t1;
+                int j = 1;
 #pragma unroll 1
-                for (int j = 0; j < d; ++j) {
-                    if (j > 0) R = fma(P.sqrt_t1, normal_from_u32(sob.get(j)), R);
+                for (; j + 1 < d; j += 2) {
+                    double xa, xb2;
+                    normal_from_u32_x2(sob.get(j), sob.get(j + 1), xa, xb2);
+                    R = fma(P.sqrt_t1, xa, R);
+                    cb[j * tpb] = P.lnS0 + P.omega * (double)(j + 1) * P.t1 + P.sigma * R;
+                    R = fma(P.sqrt_t1, xb2, R);
+                    cb[(j + 1) * tpb] = P.lnS0 + P.omega * (double)(j + 2) * P.t1 + P.sigma * R;
+                }
+                if (j < d) {
+                    R = fma(P.sqrt_t1, normal_from_u32(sob.get(j)), R);
                     cb[j * tpb] = P.lnS0 + P.omega * (double)(j + 1) * P.t1 + P.sigma * R;
                 }
             } else if (CONSTR == kBB) {
-                // same time-order bridge with the terminal loading of x_1 removed (R = M x, x_1 := 0)
+                // same time-order bridge with the terminal loading of x_1 removed (R = M x, x_1 := 0);
+                // normals in Alg. 4 order from bb_seq[1..]
+                NormalFifo fifo;
+                fifo.reset();
+                int pos = 1;
+                auto dim_at = [&](int o) { return (int)P.bb_seq[pos + o]; };
                 double stW[12];
                 int sp = 0;
                 stW[0] = 0.0;
@@ -467,11 +614,10 @@ __global__ void __launch_bounds__(128) paths_kernel(const PathArgs P) {
                         double Wr = stW[sp];
 #pragma unroll 1
                         for (int c = e - 1; c >= 0; --c) {
-                            const int mid = (j - 1) + (1 << c);
-                            const int lev = m - c;
-                            const int dim = (1 << lev) - 1 - (mid >> (c + 1));
-                            const double x = normal_from_u32(sob.get(dim));
-                            const double Wm = fma(P.bb_b[lev], x, 0.5 * (Wl + Wr));
+                            const bool refill = fifo.have == 0;
+                            const double x = fifo.next(sob, dim_at);
+                            pos += refill ? 2 : 0;
+                            const double Wm = fma(P.bb_b[m - c], x, 0.5 * (Wl + Wr));
                             if (c > 0) stW[++sp] = Wm;
                             Wr = Wm;
                         }
@@ -482,13 +628,35 @@ __global__ void __launch_bounds__(128) paths_kernel(const PathArgs P) {
                 }
             } else {
                 double* xb = buf0 + tid;
+                int kk = 1;
 #pragma unroll 1
-                for (int kk = 1; kk < d; ++kk) xb[kk * tpb] = normal_from_u32(sob.get(kk));
-                for (int j = 0; j < d; ++j) {
-                    const double* Mr = P.M + (size_t)j * d;
-                    double R = 0.0;
-                    for (int kk = 1; kk < d; ++kk) R = fma(__ldg(Mr + kk), xb[kk * tpb], R);
-                    cb[j * tpb] = P.lnS0 + P.omega * (double)(j + 1) * P.t1 + P.sigma * R;
+                for (; kk + 1 < d; kk += 2) {
+                    double xa, xc;
+                    normal_from_u32_x2(sob.get(kk), sob.get(kk + 1), xa, xc);
+                    xb[kk * tpb] = xa;
+                    xb[(kk + 1) * tpb] = xc;
+                }
+                if (kk < d) xb[kk * tpb] = normal_from_u32(sob.get(kk));
+                int j = 0;
+#pragma unroll 1
+                for (; j + 1 < d; j += 2) {
+                    const double* Ma = P.M + (size_t)j * d;
+                    const double* Mb = Ma + d;
+                    double Ra = 0.0, Rb = 0.0;
+#pragma unroll 4
+                    for (int q = 1; q < d; ++q) {
+                        const double xq = xb[q * tpb];
+                        Ra = fma(__ldg(Ma + q), xq, Ra);
+                        Rb = fma(__ldg(Mb + q), xq, Rb);
+                    }
+                    cb[j * tpb] = P.lnS0 + P.omega * (double)(j + 1) * P.t1 + P.sigma * Ra;
+                    cb[(j + 1) * tpb] = P.lnS0 + P.omega * (double)(j + 2) * P.t1 + P.sigma * Rb;
+                }
+                if (j < d) {
+                    const double* Ma = P.M + (size_t)j * d;
+                    double Ra = 0.0;
+                    for (int q = 1; q < d; ++q) Ra = fma(__ldg(Ma + q), xb[q * tpb], Ra);
+                    cb[j * tpb] = P.lnS0 + P.omega * (double)(j + 1) * P.t1 + P.sigma * Ra;
                 }
             }
 #pragma unroll
@@ -508,32 +676,24 @@ __global__ void __launch_bounds__(128) paths_kernel(const PathArgs P) {
 #pragma unroll
                 for (int q = 0; q < 4; ++q) {
                     const double y = f[o][q] - P.piv[o][q];
-                    acc1[o][q] += y;
-                    acc2[o][q] = fma(y, y, acc2[o][q]);
+                    double* a1 = accs + (size_t)(o * 8 + q * 2) * tpb + tid;
+                    a1[0] += y;
+                    a1[tpb] = fma(y, y, a1[tpb]);
                 }
             }
         }
-        if (METHOD == kQmc) sob.advance(P.dim_begin, d, k);
+        (void)k;
     }
 
     // (a8) fixed-shape reduction: warp butterfly, then the warps in order.
     const int lane = tid & 31, warp = tid >> 5, nwarps = tpb >> 5;
     const int n_out = P.partial_stride;
+    __syncthreads();  // red aliases the Sobol' tables
+    for (int v = 0; v < n_acc; ++v) {
+        double s1 = accs[v * tpb + tid];
 #pragma unroll
-    for (int o = 0; o < kMaxOpt; ++o) {
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-            double s1 = acc1[o][q], s2 = acc2[o][q];
-#pragma unroll
-            for (int off = 16; off > 0; off >>= 1) {
-                s1 += __shfl_xor_sync(0xffffffffu, s1, off);
-                s2 += __shfl_xor_sync(0xffffffffu, s2, off);
-            }
-            if (lane == 0 && o < P.n_opt) {
-                red[warp * 32 + o * 8 + q * 2 + 0] = s1;
-                red[warp * 32 + o * 8 + q * 2 + 1] = s2;
-            }
-        }
+        for (int off = 16; off > 0; off >>= 1) s1 += __shfl_xor_sync(0xffffffffu, s1, off);
+        if (lane == 0) red[warp * 32 + v] = s1;
     }
     unsigned uc = unconverged, tc = ties;
 #pragma unroll
@@ -554,14 +714,19 @@ __global__ void __launch_bounds__(128) paths_kernel(const PathArgs P) {
 }
 
 static size_t path_smem_bytes(const PathArgs& a, int constr, int cond, int method) {
-    const size_t tpb = (size_t)1 << a.tpb_log2;
+    const size_t tpb = (size_t)1 << a.tpb_log2, nw = tpb / 32;
     const bool need_buf = method == kQmc && (constr == kPca || cond == kX1);
     const bool two_buf = method == kQmc && constr == kPca && cond == kX1;
-    size_t b = 4 * 32 * sizeof(double);
+    size_t b = (size_t)a.n_opt * 8 * tpb * sizeof(double);
     if (need_buf) b += (size_t)a.d * tpb * sizeof(double);
     if (two_buf) b += (size_t)a.d * tpb * sizeof(double);
-    if (method == kQmc) b += (size_t)a.d * tpb * sizeof(uint32_t) + (size_t)a.d * 32 * sizeof(uint32_t);
-    return b;
+    size_t hw = 0;
+    if (method == kQmc) {
+        b += ((size_t)a.d * 32 * 2 + a.d) * sizeof(uint32_t) + 4;  // vt, sh, G, alignment pad
+        hw = 2 * 2 * nw * a.d * sizeof(uint32_t);
+    }
+    const size_t red = 4 * 32 * sizeof(double);
+    return b + (hw > red ? hw : red);
 }
 
 template <int C, int K, int M>
@@ -622,27 +787,45 @@ cudaError_t launch_reduce_cells(const double* d_partials, int stride, uint32_t r
 }
 
 // ---------------------------------------------------------------------------
-// Parity hooks: the same SobolState / normal code the path kernel runs.
-// One block of 2^p threads walks [k_begin, k_end) exactly like a cell.
+// Parity hooks: the same SobolBlock / normal code the path kernel runs.
+// One block of 128 threads walks 4096 points of [k_begin, k_end) like a cell.
 // ---------------------------------------------------------------------------
+struct HookSmem {
+    uint32_t *vt, *sh, *G, *HW;
+};
+__device__ __forceinline__ HookSmem hook_setup(unsigned char* raw, const uint32_t* vscr, const uint32_t* shift, int d,
+                                               int tid, int tpb) {
+    HookSmem h;
+    h.vt = reinterpret_cast<uint32_t*>(raw);
+    h.sh = h.vt + (size_t)d * 32;
+    h.G = h.sh + d;
+    h.HW = h.G + (size_t)d * 32;
+    for (int idx = tid; idx < d * 32; idx += tpb) h.vt[idx] = vscr[idx];
+    for (int idx = tid; idx < d; idx += tpb) h.sh[idx] = shift[idx];
+    __syncthreads();
+    sobol_build_g(h.vt, d, h.G, tid, tpb);
+    return h;
+}
+
 __global__ void sobol_hook_kernel(const uint32_t* __restrict__ vscr, const uint32_t* __restrict__ shift, int d,
                                   uint32_t dim_begin, uint32_t dim_end, uint64_t k_begin, uint64_t k_end,
                                   uint32_t* __restrict__ out) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
-    const int tpb_log2 = 7, tpb = 128, tid = threadIdx.x;
-    uint32_t* ys = reinterpret_cast<uint32_t*>(smem_raw);
-    uint32_t* vt = ys + (size_t)d * tpb;
-    for (int idx = tid; idx < d * 32; idx += tpb) vt[idx] = vscr[idx];
-    __syncthreads();
-    SobolState sob{ys, vt, tpb_log2, tid};
+    const int tpb_log2 = 7, tpb = 128, tid = threadIdx.x, nw = 4;
+    HookSmem h = hook_setup(smem_raw, vscr, shift, d, tid, tpb);
     const uint64_t nk = k_end - k_begin;
-    const uint64_t base = k_begin + (uint64_t)blockIdx.x * kCellPoints;
-    sob.init(0, d, base + tid, shift);
+    const uint64_t K0 = k_begin + (uint64_t)blockIdx.x * kCellPoints;
+    const uint64_t Ab = K0 >> tpb_log2, kt = K0 + tid;
+    SobolBlock sob{h.G, h.HW, d, nw, (int)(kt & 31), (int)((kt >> 5) & 3), (int)((kt >> tpb_log2) - Ab)};
     for (int a = 0; a < kCellPoints / tpb; ++a) {
-        const uint64_t k = base + tid + ((uint64_t)a << tpb_log2);
-        if (k >= k_end) break;
+        if (K0 + ((uint64_t)a << tpb_log2) >= k_end) break;
+        uint32_t* HWb = h.HW + (a & 1) * 2 * nw * d;
+        sobol_build_hw(h.vt, h.sh, d, 0, tpb_log2, nw, Ab + (uint64_t)a, HWb, tid, tpb);
+        __syncthreads();
+        sob.HW = HWb;
+        const uint64_t k = K0 + tid + ((uint64_t)a << tpb_log2);
+        if (k >= k_end) continue;
         for (uint32_t j = dim_begin; j < dim_end; ++j) out[(size_t)(j - dim_begin) * nk + (k - k_begin)] = sob.get(j);
-        sob.advance(0, d, k);
     }
 }
 
@@ -650,31 +833,42 @@ __global__ void normals_hook_kernel(const uint32_t* __restrict__ vscr, const uin
                                     uint64_t k_begin, uint64_t k_end, int method, uint64_t seed, uint32_t rep,
                                     double* __restrict__ out) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
-    const int tpb_log2 = 7, tpb = 128, tid = threadIdx.x;
-    const uint64_t base = k_begin + (uint64_t)blockIdx.x * kCellPoints;
+    const int tpb_log2 = 7, tpb = 128, tid = threadIdx.x, nw = 4;
+    const uint64_t K0 = k_begin + (uint64_t)blockIdx.x * kCellPoints;
     if (method == kLr) {
         for (int a = 0; a < kCellPoints / tpb; ++a) {
-            const uint64_t k = base + tid + ((uint64_t)a << tpb_log2);
+            const uint64_t k = K0 + tid + ((uint64_t)a << tpb_log2);
             if (k >= k_end) break;
             for (int jq = 0; jq < d; jq += 4) {
                 uint32_t c[4] = {(uint32_t)k, (uint32_t)(k >> 32), (uint32_t)(jq >> 2), (rep << 8) | 0x02u};
                 philox4x32_10(c, (uint32_t)seed, (uint32_t)(seed >> 32));
-                for (int w = 0; w < 4 && jq + w < d; ++w) out[(k - k_begin) * d + jq + w] = normal_from_u32(c[w]);
+                double xs[4];
+                normal_from_u32_x2(c[0], c[1], xs[0], xs[1]);
+                normal_from_u32_x2(c[2], c[3], xs[2], xs[3]);
+                for (int w = 0; w < 4 && jq + w < d; ++w) out[(k - k_begin) * d + jq + w] = xs[w];
             }
         }
         return;
     }
-    uint32_t* ys = reinterpret_cast<uint32_t*>(smem_raw);
-    uint32_t* vt = ys + (size_t)d * tpb;
-    for (int idx = tid; idx < d * 32; idx += tpb) vt[idx] = vscr[idx];
-    __syncthreads();
-    SobolState sob{ys, vt, tpb_log2, tid};
-    sob.init(0, d, base + tid, shift);
+    HookSmem h = hook_setup(smem_raw, vscr, shift, d, tid, tpb);
+    const uint64_t Ab = K0 >> tpb_log2, kt = K0 + tid;
+    SobolBlock sob{h.G, h.HW, d, nw, (int)(kt & 31), (int)((kt >> 5) & 3), (int)((kt >> tpb_log2) - Ab)};
     for (int a = 0; a < kCellPoints / tpb; ++a) {
-        const uint64_t k = base + tid + ((uint64_t)a << tpb_log2);
-        if (k >= k_end) break;
-        for (int j = 0; j < d; ++j) out[(k - k_begin) * d + j] = normal_from_u32(sob.get(j));
-        sob.advance(0, d, k);
+        if (K0 + ((uint64_t)a << tpb_log2) >= k_end) break;
+        uint32_t* HWb = h.HW + (a & 1) * 2 * nw * d;
+        sobol_build_hw(h.vt, h.sh, d, 0, tpb_log2, nw, Ab + (uint64_t)a, HWb, tid, tpb);
+        __syncthreads();
+        sob.HW = HWb;
+        const uint64_t k = K0 + tid + ((uint64_t)a << tpb_log2);
+        if (k >= k_end) continue;
+        int j = 0;
+        for (; j + 1 < d; j += 2) {
+            double xa, xb;
+            normal_from_u32_x2(sob.get(j), sob.get(j + 1), xa, xb);
+            out[(k - k_begin) * d + j] = xa;
+            out[(k - k_begin) * d + j + 1] = xb;
+        }
+        if (j < d) out[(k - k_begin) * d + j] = normal_from_u32(sob.get(j));
     }
 }
 
@@ -683,7 +877,7 @@ cudaError_t launch_sobol_hook(const uint32_t* d_vscr, const uint32_t* d_shift, i
                               cudaStream_t st) {
     const uint64_t nk = k_end - k_begin;
     const unsigned grid = (unsigned)((nk + kCellPoints - 1) / kCellPoints);
-    const size_t smem = (size_t)d * 128 * 4 + (size_t)d * 32 * 4;
+    const size_t smem = ((size_t)d * 64 + d + 2 * 2 * 4 * d) * 4;
     cudaError_t e = cudaFuncSetAttribute(sobol_hook_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     sobol_hook_kernel<<<grid, 128, smem, st>>>(d_vscr, d_shift, d, dim_begin, dim_end, k_begin, k_end, d_out);
@@ -696,7 +890,7 @@ cudaError_t launch_normals_hook(const uint32_t* d_vscr, const uint32_t* d_shift,
                                 cudaStream_t st) {
     const uint64_t nk = k_end - k_begin;
     const unsigned grid = (unsigned)((nk + kCellPoints - 1) / kCellPoints);
-    const size_t smem = method == kLr ? 0 : (size_t)d * 128 * 4 + (size_t)d * 32 * 4;
+    const size_t smem = method == kLr ? 0 : ((size_t)d * 64 + d + 2 * 2 * 4 * d) * 4;
     cudaError_t e =
         cudaFuncSetAttribute(normals_hook_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;

@@ -122,6 +122,89 @@ __device__ __forceinline__ double normal_from_u32(uint32_t y) {
 
 // phi(x); flushes to 0 below e^-700 (|x| > 37.4), where fast_exp's exponent
 // arithmetic would leave the normal range (the oracle's value there is < 1e-305)
+// ---- paired versions: two independent evaluations interleaved, so every
+// coefficient loaded into a uniform register feeds two DFMAs and the two Horner
+// chains hide each other's latency ------------------------------------------
+__device__ __forceinline__ void fast_exp_x2(double xa, double xb, double& ra, double& rb) {
+    const double ta = fma(xa, MC.log2e, MC.shift), tb = fma(xb, MC.log2e, MC.shift);
+    const int na = __double2loint(ta), nb = __double2loint(tb);
+    const double fa = ta - MC.shift, fb = tb - MC.shift;
+    double qa = fma(fa, -MC.ln2_hi, xa), qb = fma(fb, -MC.ln2_hi, xb);
+    qa = fma(fa, -MC.ln2_lo, qa);
+    qb = fma(fb, -MC.ln2_lo, qb);
+    double pa = EXP_POLY[12], pb = EXP_POLY[12];
+#pragma unroll
+    for (int j = 11; j >= 0; --j) {
+        pa = fma(pa, qa, EXP_POLY[j]);
+        pb = fma(pb, qb, EXP_POLY[j]);
+    }
+    ra = __hiloint2double(__double2hiint(pa) + (na << 20), __double2loint(pa));
+    rb = __hiloint2double(__double2hiint(pb) + (nb << 20), __double2loint(pb));
+}
+
+__device__ __forceinline__ void log_reduce(double t, double& m, double& kd) {
+    const int hi = __double2hiint(t), lo = __double2loint(t);
+    int k = (hi >> 20) - 1023;
+    int mhi = (hi & 0x000FFFFF) | 0x3FF00000;
+    const bool big = mhi > 0x3FF6A09E;
+    mhi -= big ? 0x00100000 : 0;
+    k += big ? 1 : 0;
+    m = __hiloint2double(mhi, lo);
+    kd = (double)k;
+}
+
+__device__ __forceinline__ void fast_log_x2(double ta, double tb, double& la, double& lb) {
+    double ma, mb, ka, kb;
+    log_reduce(ta, ma, ka);
+    log_reduce(tb, mb, kb);
+    const double fa = (ma - MC.one) * rcp_newton(ma + MC.one);
+    const double fb = (mb - MC.one) * rcp_newton(mb + MC.one);
+    const double ga = fa * fa, gb = fb * fb;
+    const double sa = ga - LOG_Q_CENTER, sb = gb - LOG_Q_CENTER;
+    double qa = LOG_Q[10], qb = LOG_Q[10];
+#pragma unroll
+    for (int j = 9; j >= 0; --j) {
+        qa = fma(qa, sa, LOG_Q[j]);
+        qb = fma(qb, sb, LOG_Q[j]);
+    }
+    const double lma = fma(fa * ga, qa, MC.two * fa), lmb = fma(fb * gb, qb, MC.two * fb);
+    la = fma(ka, MC.ln2_hi, fma(ka, MC.ln2_lo, lma));
+    lb = fma(kb, MC.ln2_hi, fma(kb, MC.ln2_lo, lmb));
+}
+
+__device__ __noinline__ double icdf_tail_poly(double w) {
+    const double v = sqrt(w) - ICDF_TAIL_CENTER;
+    double p = ICDF_TAIL[24];
+#pragma unroll
+    for (int j = 23; j >= 0; --j) p = fma(p, v, ICDF_TAIL[j]);
+    return p;
+}
+
+// two lattice points -> two standard normals (same arithmetic as normal_from_u32)
+__device__ __forceinline__ void normal_from_u32_x2(uint32_t ya, uint32_t yb, double& xa, double& xb) {
+    const bool upa = (ya >> 31) != 0u, upb = (yb >> 31) != 0u;
+    const uint32_t la = upa ? ~ya : ya, lb = upb ? ~yb : yb;
+    const double ua = fma((double)la, MC.p32, MC.p33), ub = fma((double)lb, MC.p32, MC.p33);
+    const double za = fma(MC.two, ua, -MC.one), zb = fma(MC.two, ub, -MC.one);
+    const double ta = (MC.four * ua) * (MC.one - ua), tb = (MC.four * ub) * (MC.one - ub);
+    double wa, wb;
+    fast_log_x2(ta, tb, wa, wb);
+    wa = -wa;
+    wb = -wb;
+    const double va = wa - ICDF_CENTRAL_CENTER, vb = wb - ICDF_CENTRAL_CENTER;
+    double pa = ICDF_CENTRAL[24], pb = ICDF_CENTRAL[24];
+#pragma unroll
+    for (int j = 23; j >= 0; --j) {
+        pa = fma(pa, va, ICDF_CENTRAL[j]);
+        pb = fma(pb, vb, ICDF_CENTRAL[j]);
+    }
+    if (wa >= MC.w_split) pa = icdf_tail_poly(wa);  // u < 4.8e-4: rare, divergent
+    if (wb >= MC.w_split) pb = icdf_tail_poly(wb);
+    const double ra = za * pa, rb = zb * pb;
+    xa = upa ? -ra : ra;
+    xb = upb ? -rb : rb;
+}
+
 __device__ __forceinline__ double normal_pdf(double x) {
     const double a = MC.minus_half * x * x;
     return a > MC.pdf_floor ? MC.inv_sqrt_2pi * fast_exp(a) : 0.0;
