@@ -362,12 +362,22 @@ PathArgs make_args(const Plan& pl, const Scratch& s) {
         }
         for (; n < kMaxDimGpu + 2; ++n) a.bb_seq[n] = a.bb_seq[n - 1];
     }
+    a.has_lookback = 0;
     for (int o = 0; o < pl.n_opt; ++o) {
+        a.has_lookback |= pl.types[o] == QMCCPW_LOOKBACK_CALL;
         a.type[o] = pl.types[o];
         a.K[o] = pl.p[o].K;
         a.lnK[o] = std::log(pl.p[o].K);
         a.lndK[o] = std::log((double)d * pl.p[o].K);
         bs_pivots(pl.types[o], pl.p[o], a.piv[o]);
+    }
+    for (int o = 0; o < pl.n_opt; ++o) {
+        a.tail_leader[o] = o;
+        for (int q = 0; q < o; ++q)
+            if (pl.p[q].K == pl.p[o].K && (pl.types[q] == QMCCPW_LOOKBACK_CALL) == (pl.types[o] == QMCCPW_LOOKBACK_CALL)) {
+                a.tail_leader[o] = q;
+                break;
+            }
     }
     a.mean_a = mean_first_column(pl.cfg.construction, d, p.T);
     a.vscr = s.vscr;

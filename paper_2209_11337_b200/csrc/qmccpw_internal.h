@@ -49,6 +49,8 @@ struct PathArgs {
     uint8_t bb_seq[kMaxDimGpu + 2];  // Sobol' dimension of the i-th normal consumed by the time-order
                                      // bridge (Alg. 4's consumption order), padded by repetition
     // options
+    int has_lookback;        // track S~_max / argmax (lookback present)
+    int tail_leader[kMaxOpt];  // first option with the same strike and statistic (shares psi etc.)
     int type[kMaxOpt];
     double K[kMaxOpt];
     double lnK[kMaxOpt];

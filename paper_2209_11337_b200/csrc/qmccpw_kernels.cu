@@ -199,44 +199,48 @@ __device__ __forceinline__ void sobol_build_hw(const uint32_t* vt, const uint32_
 // runner-up exponent.
 // ---------------------------------------------------------------------------
 struct W1Acc {
-    double sumS, sumI, Smax, Imax, emax, esec;
+    double sumS, sumI, emax, esec, ymax;
     __device__ __forceinline__ void reset() {
-        sumS = 0.0; sumI = 0.0; Smax = 0.0; Imax = 0.0; emax = -CUDART_INF; esec = -CUDART_INF;
+        sumS = 0.0; sumI = 0.0; emax = -CUDART_INF; esec = -CUDART_INF; ymax = 0.0;
+    }
+    // lookback: lowest argmax of e_j (= argmax of S~_j) and the runner-up exponent,
+    // with plain compare-selects (no NaN-aware fmax/fmin: e is always finite)
+    __device__ __forceinline__ void track(double e, double y) {
+        const bool gt = e > emax;
+        const double cand = gt ? emax : e;
+        esec = cand > esec ? cand : esec;
+        ymax = gt ? y : ymax;
+        emax = gt ? e : emax;
     }
     // date index j (0-based, t_{j+1} - t_1 = j dt), Wt = W~(t_{j+1} - t_1)
     __device__ __forceinline__ void push(const PathArgs& P, int j, double Wt) {
         const double tt = (double)j * P.t1;
         const double e = fma(P.sigma, Wt, P.omega * tt);
         const double St = P.S0 * fast_exp(e);
-        const double I = St * fma(-P.sigma, tt, Wt);
+        const double y = fma(-P.sigma, tt, Wt);
         sumS += St;
-        sumI += I;
-        // lowest argmax and runner-up exponent, branch-free
-        const bool gt = e > emax;
-        esec = fmax(esec, fmin(e, emax));
-        emax = gt ? e : emax;
-        Smax = gt ? St : Smax;
-        Imax = gt ? I : Imax;
-    }
-    __device__ __forceinline__ void take(double e, double St, double I) {
-        sumS += St;
-        sumI += I;
-        const bool gt = e > emax;
-        esec = fmax(esec, fmin(e, emax));
-        emax = gt ? e : emax;
-        Smax = gt ? St : Smax;
-        Imax = gt ? I : Imax;
+        sumI = fma(St, y, sumI);
+        if (P.has_lookback) track(e, y);
     }
     // dates j and j+1 together (paired exp)
     __device__ __forceinline__ void push2(const PathArgs& P, int j, double Wa, double Wb) {
-        const double ta = (double)j * P.t1, tb = (double)(j + 1) * P.t1;
+        const double ta = (double)j * P.t1, tb = ta + P.t1;
         const double ea = fma(P.sigma, Wa, P.omega * ta), eb = fma(P.sigma, Wb, P.omega * tb);
         double Xa, Xb;
         fast_exp_x2(ea, eb, Xa, Xb);
         const double Sa = P.S0 * Xa, Sb = P.S0 * Xb;
-        take(ea, Sa, Sa * fma(-P.sigma, ta, Wa));
-        take(eb, Sb, Sb * fma(-P.sigma, tb, Wb));
+        const double ya = fma(-P.sigma, ta, Wa), yb = fma(-P.sigma, tb, Wb);
+        sumS += Sa;
+        sumI = fma(Sa, ya, sumI);
+        sumS += Sb;
+        sumI = fma(Sb, yb, sumI);
+        if (P.has_lookback) {
+            track(ea, ya);
+            track(eb, yb);
+        }
     }
+    // S~_max and I_max = S~_{j*} (W~_{j*} - sigma (t_{j*} - t_1)), rebuilt once per path
+    __device__ __forceinline__ double smax(const PathArgs& P) const { return P.S0 * fast_exp(emax); }
 };
 
 // Two-slot FIFO of standard normals drawn in a fixed dimension order, two
@@ -259,27 +263,48 @@ struct NormalFifo {
 };
 
 // (a6)+(a7) W1 threshold psi_d and the closed-form smoothed
-// payoff and Greeks (readings 1-5).
-__device__ __forceinline__ void tail_w1(const PathArgs& P, int o, const W1Acc& acc, double f[4]) {
-    const int type = P.type[o];
+// payoff and Greeks (readings 1-5), all options of the
+// launch at once.  Options with the same strike and statistic (the arithmetic
+// and binary Asians of C4) share psi, phi(psi), Phibar(psi), Phibar(psi - s):
+// P.tail_leader[o] names the first such option.
+__device__ __forceinline__ void tail_w1_all(const PathArgs& P, const W1Acc& acc, double f[kMaxOpt][4]) {
     const double inv_d = 1.0 / (double)P.d;
-    const double stat = (type == kLookback) ? acc.Smax : acc.sumS * inv_d;
-    const double I = (type == kLookback) ? acc.Imax : acc.sumI * inv_d;
-    const double psi = (P.lnK[o] - fast_log(stat) - P.omega * P.t1) * P.inv_s;
-    const double ph = normal_pdf(psi);
-    const double P0 = normal_sf(psi);
-    const double K = P.K[o], D = P.Dfac, S0 = P.S0;
-    if (type == kBinary) {
-        f[0] = D * P0;
-        f[1] = D * ph * P.inv_s / S0;
-        f[2] = D * ph * (I * P.inv_s / stat + psi * P.inv_sigma - P.sqrt_t1);
-        f[3] = D * ph * P.inv_s / (S0 * S0) * (psi * P.inv_s - 1.0);
-    } else {
-        const double P1 = normal_sf(psi - P.s);
-        f[0] = P.Afac * stat * P1 - D * K * P0;
-        f[1] = P.Afac * (stat / S0) * P1;
-        f[2] = P.Afac * P1 * I + K * D * ph * P.sqrt_t1;
-        f[3] = K * D * ph * P.inv_s / (S0 * S0);
+    const double SA = acc.sumS * inv_d, IA = acc.sumI * inv_d;
+    const double Smax = P.has_lookback ? acc.smax(P) : SA;
+    const double Imax = Smax * acc.ymax;
+    double lnSA, lnSmax;
+    fast_log_x2(SA, Smax, lnSA, lnSmax);
+    double psi[kMaxOpt], Q0[kMaxOpt], Q1[kMaxOpt], ph[kMaxOpt];
+#pragma unroll
+    for (int o = 0; o < kMaxOpt; ++o) {
+        if (o >= P.n_opt) break;
+        const bool lb = P.type[o] == kLookback;
+        const int ld = P.tail_leader[o];
+        if (ld == o) {
+            psi[o] = (P.lnK[o] - (lb ? lnSmax : lnSA) - P.omega * P.t1) * P.inv_s;
+            double phs;
+            phibar_phi_x2(psi[o], psi[o] - P.s, Q0[o], Q1[o], ph[o], phs);
+        } else {
+            // leader index ld < o, resolved with selects (no dynamic register indexing)
+            psi[o] = ld == 0 ? psi[0] : psi[ld == 1 ? 1 : 0];
+            Q0[o] = ld == 0 ? Q0[0] : Q0[ld == 1 ? 1 : 0];
+            Q1[o] = ld == 0 ? Q1[0] : Q1[ld == 1 ? 1 : 0];
+            ph[o] = ld == 0 ? ph[0] : ph[ld == 1 ? 1 : 0];
+        }
+        const double stat = lb ? Smax : SA;
+        const double I = lb ? Imax : IA;
+        const double K = P.K[o], D = P.Dfac, S0 = P.S0;
+        if (P.type[o] == kBinary) {
+            f[o][0] = D * Q0[o];
+            f[o][1] = D * ph[o] * P.inv_s / S0;
+            f[o][2] = D * ph[o] * (I * P.inv_s / stat + psi[o] * P.inv_sigma - P.sqrt_t1);
+            f[o][3] = D * ph[o] * P.inv_s / (S0 * S0) * (psi[o] * P.inv_s - 1.0);
+        } else {
+            f[o][0] = P.Afac * stat * Q1[o] - D * K * Q0[o];
+            f[o][1] = P.Afac * (stat / S0) * Q1[o];
+            f[o][2] = P.Afac * Q1[o] * I + K * D * ph[o] * P.sqrt_t1;
+            f[o][3] = K * D * ph[o] * P.inv_s / (S0 * S0);
+        }
     }
 }
 
@@ -328,31 +353,44 @@ __device__ __forceinline__ void tail_x1(const PathArgs& P, int o, const double* 
     unconverged += conv ? 0u : 1u;
     double Dst = 0.0, Qst = 0.0, Vst = 0.0, sumW = 0.0, sumWv = 0.0;
     const bool arith = P.type[o] == kArith;
-    for (int j = 0; j < d; ++j) {
-        const double aj = P.a[j], cj = cb[j * stride];
-        const double tj = (double)(j + 1) * P.t1;
-        const double Rj = (cj - P.lnS0 - P.omega * tj) * P.inv_sigma;
-        const double E = fast_exp(fma(sg * aj, u, cj));
-        Dst = fma(aj, E, Dst);
-        Qst = fma(aj * aj, E, Qst);
-        Vst = fma(E, Rj - sg * tj + aj * u, Vst);
+#pragma unroll 1
+    for (int j = 0; j < d; j += 2) {
+        const int jb = (j + 1 < d) ? j + 1 : j;
+        const double wgt = (j + 1 < d) ? 1.0 : 0.0;  // odd d: the duplicate pair member counts 0
+        const double aa = P.a[j], ab = P.a[jb], ca = cb[j * stride], cbb = cb[jb * stride];
+        const double ta = (double)(j + 1) * P.t1, tb = (double)(jb + 1) * P.t1;
+        const double Ra = (ca - P.lnS0 - P.omega * ta) * P.inv_sigma, Rb = (cbb - P.lnS0 - P.omega * tb) * P.inv_sigma;
+        double Ea, Eb;
+        fast_exp_x2(fma(sg * aa, u, ca), fma(sg * ab, u, cbb), Ea, Eb);
+        Eb *= wgt;
+        Dst = fma(aa, Ea, Dst);
+        Qst = fma(aa * aa, Ea, Qst);
+        Vst = fma(Ea, Ra - sg * ta + aa * u, Vst);
+        Dst = fma(ab, Eb, Dst);
+        Qst = fma(ab * ab, Eb, Qst);
+        Vst = fma(Eb, Rb - sg * tb + ab * u, Vst);
         if (arith) {
-            const double w = fast_exp(fma(0.5 * sg * sg * aj, aj, cj));
-            const double Pj = normal_cdf(sg * aj - u);
-            sumW = fma(w, Pj, sumW);
-            sumWv = fma(w * (Rj - sg * tj + sg * aj * aj), Pj, sumWv);
+            double wa, wb, Pa, Pb, pa, pb;
+            fast_exp_x2(fma(0.5 * sg * sg * aa, aa, ca), fma(0.5 * sg * sg * ab, ab, cbb), wa, wb);
+            phibar_phi_x2(u - sg * aa, u - sg * ab, Pa, Pb, pa, pb);  // Phi(sigma a - u) = Phibar(u - sigma a)
+            wb *= wgt;
+            sumW = fma(wa, Pa, sumW);
+            sumWv = fma(wa * (Ra - sg * ta + sg * aa * aa), Pa, sumWv);
+            sumW = fma(wb, Pb, sumW);
+            sumWv = fma(wb * (Rb - sg * tb + sg * ab * ab), Pb, sumWv);
         }
     }
     const double D = P.Dfac, S0 = P.S0, K = P.K[o], dd = (double)d;
-    const double ph = normal_pdf(u);
+    double ph, Qu, Q2, ph2;
+    phibar_phi_x2(u, u, Qu, Q2, ph, ph2);
     if (arith) {
-        f[0] = D * (sumW / dd - K * normal_sf(u));
+        f[0] = D * (sumW / dd - K * Qu);
         f[1] = D * sumW / (dd * S0);
         f[2] = D * (sumWv / dd + ph * Dst / dd);
         f[3] = D * dd * K * K * ph / (S0 * S0 * sg * Dst);
     } else {
         const double up = -dd * K / (S0 * sg * Dst);
-        f[0] = D * normal_sf(u);
+        f[0] = D * Qu;
         f[1] = D * ph * dd * K / (S0 * sg * Dst);
         f[2] = D * ph * Vst / (sg * Dst);
         f[3] = D * (dd * K / sg) * ph / (S0 * Dst) * (-u * up - 2.0 / S0 - sg * up * Qst / Dst);
@@ -567,10 +605,8 @@ __global__ void __launch_bounds__(128) paths_kernel(const PathArgs P) {
                     w1.push(P, j, Wa - W1);
                 }
             }
-            if (w1.emax - w1.esec < 1e-12) ++ties;  // only meaningful for the lookback
-#pragma unroll
-            for (int o = 0; o < kMaxOpt; ++o)
-                if (o < P.n_opt) tail_w1(P, o, w1, f[o]);
+            if (P.has_lookback && w1.emax - w1.esec < 1e-12) ++ties;
+            tail_w1_all(P, w1, f);
         } else {
             // X1: c_j = ln S0 + omega t_j + sigma R_j, R = M x with x_1 := 0
             double* cb = (CONSTR == kPca ? buf1 : buf0) + tid;

@@ -15,7 +15,7 @@ namespace qmccpw {
 
 struct MathConst {
     double log2e, shift, ln2_hi, ln2_lo, one, two, half, minus_half, w_split, inv_sqrt_2pi, inv_sqrt2, p32, p33,
-        four, pdf_floor;
+        four, pdf_floor, mills_c, mills_2c, exp_floor;
 };
 __constant__ MathConst MC = {
     1.4426950408889634074,        // log2(e)
@@ -26,7 +26,7 @@ __constant__ MathConst MC = {
     6.25,                         // central / tail split of the inverse normal (w = -ln(1 - z^2))
     0.398942280401432677939946059934,  // 1/sqrt(2 pi)
     0.707106781186547524400844362105,  // 1/sqrt(2)
-    0x1p-32, 0x1p-33, 4.0, -700.0};
+    0x1p-32, 0x1p-33, 4.0, -700.0, 3.0, 6.0, 700.0};
 
 // Philox4x32-10 (Salmon et al., SC'11): 10 rounds of two 32x32->64 products,
 // Weyl key schedule.  c = counter in, output out (in place).
@@ -209,8 +209,37 @@ __device__ __forceinline__ double normal_pdf(double x) {
     const double a = MC.minus_half * x * x;
     return a > MC.pdf_floor ? MC.inv_sqrt_2pi * fast_exp(a) : 0.0;
 }
-// Phibar(x) = 1 - Phi(x) = erfc(x/sqrt2)/2, never formed as 1 - Phi (reading 22)
-__device__ __forceinline__ double normal_sf(double x) { return MC.half * erfc(x * MC.inv_sqrt2); }
-__device__ __forceinline__ double normal_cdf(double x) { return MC.half * erfc(-x * MC.inv_sqrt2); }
+// Phibar(x) = 1 - Phi(x) and phi(x) together, for two arguments.  Phibar(|x|) =
+// phi(|x|) R(|x|), R the Mills ratio: h(t) = (|x| + 3) R, t = (|x| - 3)/(|x| + 3),
+// polynomial fitted on |x| <= 40 (rel. 6e-17); x^2 is split exactly (hi + lo)
+// so phi keeps full relative accuracy in the tails.  For x < 0, 1 - Phibar(|x|)
+// with Phibar(|x|) <= 1/2: no cancellation (reading 22: never 1 - Phi(psi)).
+__device__ __forceinline__ void phibar_phi_x2(double xa, double xb, double& Qa, double& Qb, double& pha,
+                                              double& phb) {
+    const double aa = fabs(xa), ab = fabs(xb);
+    const double ra = rcp_newton(aa + MC.mills_c), rb = rcp_newton(ab + MC.mills_c);
+    const double ta = fma(-MC.mills_2c, ra, MC.one) - MILLS_H_CENTER, tb = fma(-MC.mills_2c, rb, MC.one) - MILLS_H_CENTER;
+    double ha = MILLS_H[27], hb = MILLS_H[27];
+#pragma unroll
+    for (int j = 26; j >= 0; --j) {
+        ha = fma(ha, ta, MILLS_H[j]);
+        hb = fma(hb, tb, MILLS_H[j]);
+    }
+    const double sa = aa * aa, sb = ab * ab;
+    const double la = fma(aa, aa, -sa), lb = fma(ab, ab, -sb);
+    double ea, eb;
+    fast_exp_x2(MC.minus_half * sa, MC.minus_half * sb, ea, eb);
+    pha = (sa < MC.exp_floor * MC.two) ? MC.inv_sqrt_2pi * ea * fma(MC.minus_half, la, MC.one) : 0.0;
+    phb = (sb < MC.exp_floor * MC.two) ? MC.inv_sqrt_2pi * eb * fma(MC.minus_half, lb, MC.one) : 0.0;
+    const double qa = pha * (ha * ra), qb = phb * (hb * rb);
+    Qa = xa >= 0.0 ? qa : MC.one - qa;
+    Qb = xb >= 0.0 ? qb : MC.one - qb;
+}
+__device__ __forceinline__ double normal_sf(double x) {
+    double Q, Q2, ph, ph2;
+    phibar_phi_x2(x, x, Q, Q2, ph, ph2);
+    return Q;
+}
+__device__ __forceinline__ double normal_cdf(double x) { return normal_sf(-x); }
 
 }  // namespace qmccpw
