@@ -133,8 +133,9 @@ int qmccpw_price_greeks_batch(const int32_t* options, const qmccpw_params* p, in
  * consecutive point indices), c = l * cells_per_replicate + b.  Each cell's
  * partial is partial_doubles_per_cell doubles:
  *   [o][q][0] = sum over its points of (f - pivot_{o,q}),
- *   [o][q][1] = sum of (f - pivot_{o,q})^2, then 2 counters
- *   (newton_unconverged, argmax_near_ties) stored as exact doubles.
+ *   [o][q][1] = sum of (f - pivot_{o,q})^2, then 3 counters
+ *   (newton_unconverged, argmax_near_ties, points evaluated) stored as exact
+ *   doubles.  partial_doubles_per_cell = 8 n_options + 3.
  * Pivots are the d = 1 Black-Scholes values of each output. */
 int qmccpw_cell_count(const qmccpw_params* p, int32_t n_options, uint64_t n_points, uint32_t n_replicates,
                       const qmccpw_config* cfg, uint64_t* n_cells, uint64_t* partial_doubles_per_cell);
@@ -159,7 +160,8 @@ int qmccpw_replicate_sums(const double* d_partials, const qmccpw_params* p, int3
 
 /* Host-only finalisation (no device work): replicate sums h_rep_sums
  * [n_replicates][partial_doubles_per_cell] (host memory) -> out[n_options]
- * (P:643-652). */
+ * (P:643-652).  EINVAL if any replicate's point counter differs from
+ * n_points (a rank's or a cell range's contribution is missing). */
 int qmccpw_finalize(const double* h_rep_sums, const int32_t* options, const qmccpw_params* p, int32_t n_options,
                     uint64_t n_points, uint32_t n_replicates, const qmccpw_config* cfg, qmccpw_result* out);
 

@@ -245,7 +245,7 @@ int make_plan(const int32_t* options, const qmccpw_params* p, int32_t n_options,
     pl->L = n_reps;
     pl->cells_per_rep = (uint32_t)((n_points + kCellPoints - 1) / kCellPoints);
     pl->n_cells = (uint64_t)n_reps * pl->cells_per_rep;
-    pl->stride = n_options * 8 + 2;
+    pl->stride = n_options * 8 + 3;
     for (int o = 0; o < n_options; ++o) {
         pl->types[o] = options[o];
         pl->p[o] = p[o];
@@ -392,10 +392,21 @@ PathArgs make_args(const Plan& pl, const Scratch& s) {
     return a;
 }
 
-// P:643-652 replicate summary from per-replicate sums [L][stride]
-void finalize_host(const Plan& pl, const double* rs, qmccpw_result* out) {
+// P:643-652 replicate summary from per-replicate sums [L][stride].  Every
+// replicate row must account for exactly n_points points (a missing rank or
+// cell range leaves a short count): EINVAL otherwise.
+int finalize_host(const Plan& pl, const double* rs, qmccpw_result* out) {
     const double N = (double)pl.N;
     const int L = (int)pl.L;
+    for (int l = 0; l < L; ++l) {
+        const double cnt = rs[(size_t)l * pl.stride + pl.n_opt * 8 + 2];
+        if (cnt != N) {
+            char buf[160];
+            snprintf(buf, sizeof buf, "incomplete partials: replicate %d covers %.0f of %llu points", l, cnt,
+                     (unsigned long long)pl.N);
+            return fail(QMCCPW_EINVAL, buf);
+        }
+    }
     double unconv = 0.0, ties = 0.0;
     for (int l = 0; l < L; ++l) {
         unconv += rs[(size_t)l * pl.stride + pl.n_opt * 8 + 0];
@@ -430,6 +441,7 @@ void finalize_host(const Plan& pl, const double* rs, qmccpw_result* out) {
         r.argmax_near_ties = (uint64_t)ties;
         out[o] = r;
     }
+    return QMCCPW_OK;
 }
 
 struct DeviceGuard {
@@ -467,8 +479,7 @@ int run_full(const Plan& pl, qmccpw_result* out) {
     if (rc) return rc;
     CUDA_TRY(cudaMemcpyAsync(c->h_pinned, s.rep_sums, rs_bytes, cudaMemcpyDeviceToHost, st));
     CUDA_TRY(cudaStreamSynchronize(st));
-    finalize_host(pl, c->h_pinned, out);
-    return QMCCPW_OK;
+    return finalize_host(pl, c->h_pinned, out);
 }
 
 }  // namespace
@@ -505,7 +516,7 @@ int qmccpw_cell_count(const qmccpw_params* p, int32_t n_options, uint64_t n_poin
     rc = validate_config(c, p->d, n_points, n_replicates);
     if (rc) return rc;
     *n_cells = (uint64_t)n_replicates * ((n_points + kCellPoints - 1) / kCellPoints);
-    *partial_doubles_per_cell = (uint64_t)n_options * 8 + 2;
+    *partial_doubles_per_cell = (uint64_t)n_options * 8 + 3;
     return QMCCPW_OK;
 }
 
@@ -548,7 +559,7 @@ int qmccpw_replicate_sums(const double* d_partials, const qmccpw_params* p, int3
     if (rep_begin > rep_end || rep_end > n_replicates) return fail(QMCCPW_EINVAL, "replicate range out of bounds");
     DeviceGuard g(c.device);
     const uint32_t cpr = (uint32_t)((n_points + kCellPoints - 1) / kCellPoints);
-    CUDA_TRY(launch_reduce_cells(d_partials, n_options * 8 + 2, rep_begin, rep_end, cpr, d_rep_sums,
+    CUDA_TRY(launch_reduce_cells(d_partials, n_options * 8 + 3, rep_begin, rep_end, cpr, d_rep_sums,
                                  static_cast<cudaStream_t>(c.stream)));
     return QMCCPW_OK;
 }
@@ -567,7 +578,8 @@ int qmccpw_finalize(const double* h_rep_sums, const int32_t* options, const qmcc
     int rc = make_plan(options, p, n_options, n_points, n_replicates, &c0, &pl);
     if (rc) return rc;
     std::vector<qmccpw_result> tmp(pl.n_opt);
-    finalize_host(pl, h_rep_sums, tmp.data());
+    rc = finalize_host(pl, h_rep_sums, tmp.data());
+    if (rc) return rc;
     for (int o = 0; o < pl.n_opt; ++o) out[o] = tmp[o];
     return QMCCPW_OK;
 }
@@ -594,7 +606,8 @@ int qmccpw_finalize_device(const double* d_partials, const int32_t* options, con
     CUDA_TRY(cudaMemcpyAsync(c->h_pinned, s.rep_sums, rs_bytes, cudaMemcpyDeviceToHost, st));
     CUDA_TRY(cudaStreamSynchronize(st));
     std::vector<qmccpw_result> tmp(pl.n_opt);
-    finalize_host(pl, c->h_pinned, tmp.data());
+    rc = finalize_host(pl, c->h_pinned, tmp.data());
+    if (rc) return rc;
     for (int o = 0; o < pl.n_opt; ++o) out[o] = tmp[o];
     return QMCCPW_OK;
 }

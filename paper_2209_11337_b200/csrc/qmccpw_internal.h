@@ -68,7 +68,7 @@ struct PathArgs {
     uint64_t seed;
     // outputs
     double* partials;        // [cell][partial_doubles_per_cell]
-    int partial_stride;      // doubles per cell = n_opt*8 + 2
+    int partial_stride;      // doubles per cell = n_opt*8 + 3
     // parity hook: per-path values out[(point index within range)][4] (NULL in production)
     double* path_out;
     int hook_option;         // option index whose values go to path_out

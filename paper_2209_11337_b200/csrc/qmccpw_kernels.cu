@@ -485,7 +485,7 @@ __global__ void __launch_bounds__(128) paths_kernel(const PathArgs P) {
         sobol_build_g(vt, d, G, tid, tpb);
     }
     for (int v = 0; v < n_acc; ++v) accs[v * tpb + tid] = 0.0;
-    unsigned unconverged = 0, ties = 0;
+    unsigned unconverged = 0, ties = 0, npts = 0;
 
     for (int a = 0; a < ppt; ++a) {
         if (i0 + ((uint64_t)a << tpb_log2) >= P.n_points) break;  // block-uniform: ragged last cell
@@ -497,6 +497,7 @@ __global__ void __launch_bounds__(128) paths_kernel(const PathArgs P) {
         }
         const uint64_t i = i0 + tid + ((uint64_t)a << tpb_log2);
         if (i >= P.n_points) continue;
+        ++npts;
         const uint64_t k = P.point_offset + i;
         double f[kMaxOpt][4];
 
@@ -731,15 +732,17 @@ __global__ void __launch_bounds__(128) paths_kernel(const PathArgs P) {
         for (int off = 16; off > 0; off >>= 1) s1 += __shfl_xor_sync(0xffffffffu, s1, off);
         if (lane == 0) red[warp * 32 + v] = s1;
     }
-    unsigned uc = unconverged, tc = ties;
+    unsigned uc = unconverged, tc = ties, nc = npts;
 #pragma unroll
     for (int off = 16; off > 0; off >>= 1) {
         uc += __shfl_xor_sync(0xffffffffu, uc, off);
         tc += __shfl_xor_sync(0xffffffffu, tc, off);
+        nc += __shfl_xor_sync(0xffffffffu, nc, off);
     }
     if (lane == 0) {
         red[warp * 32 + P.n_opt * 8 + 0] = (double)uc;
         red[warp * 32 + P.n_opt * 8 + 1] = (double)tc;
+        red[warp * 32 + P.n_opt * 8 + 2] = (double)nc;  // points this cell evaluated (completeness check)
     }
     __syncthreads();
     if (tid < n_out) {

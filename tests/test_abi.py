@@ -79,6 +79,6 @@ def test_no_cpu_fallback_without_gpu():
 def test_cell_count():
     import paper_2209_11337_b200 as q
     n, per = q.qmccpw_cell_count(q.params(d=64), 3, 1 << 20, 64, q.config())
-    assert (n, per) == (64 * 256, 26)
+    assert (n, per) == (64 * 256, 27)
     n, per = q.qmccpw_cell_count(q.params(d=4), 1, 4097, 3, q.config(construction=q.STD))
-    assert (n, per) == (6, 10)
+    assert (n, per) == (6, 11)

@@ -1,0 +1,133 @@
+"""CPU (gloo) tests of the multi-GPU host logic:
+
+  * replicate partition: contiguous, disjoint, complete, balanced for G = 1..8;
+  * world size 2 over gloo: each rank fills only its replicate rows of the
+    [L][stride] replicate-sum table, one all_reduce(SUM), host finalize ->
+    bit-identical to a single process finalising the full table (every row is
+    nonzero on exactly one rank, so the sum is exact);
+  * fault detection: a missing rank leaves short point counters and finalize
+    refuses the table (QMCCPW_EINVAL) instead of returning biased Greeks.
+
+No GPU is used: the per-replicate sums are synthetic, seeded tables with the
+layout the kernels write (8 n_opt sums + 3 counters per row).
+"""
+import os
+import socket
+import subprocess
+import sys
+import tempfile
+
+import numpy as np
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+N_POINTS, N_REPS, N_OPT = 1 << 12, 13, 3
+
+
+def _table(n_reps=N_REPS, n_opt=N_OPT, seed=7):
+    rng = np.random.default_rng(seed)
+    per = 8 * n_opt + 3
+    t = np.zeros((n_reps, per))
+    for l in range(n_reps):
+        for o in range(n_opt):
+            for q in range(4):
+                s1 = rng.normal() * 50.0
+                t[l, o * 8 + q * 2] = s1
+                t[l, o * 8 + q * 2 + 1] = s1 * s1 / N_POINTS + abs(rng.normal()) * N_POINTS
+        t[l, n_opt * 8 + 2] = N_POINTS
+    return t
+
+
+def _plist(q):
+    return [q.params(d=64) for _ in range(N_OPT)]
+
+
+def test_replicate_partition():
+    from paper_2209_11337_b200.distributed import replicate_range
+    for L in (1, 5, 64, 512, 1000):
+        for G in range(1, 9):
+            rs = [replicate_range(L, G, g) for g in range(G)]
+            assert rs[0][0] == 0 and rs[-1][1] == L
+            assert all(rs[g][1] == rs[g + 1][0] for g in range(G - 1))
+            sizes = [e - b for b, e in rs]
+            assert max(sizes) - min(sizes) <= 1
+
+
+def _worker(rank, world, port, outdir):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    import torch
+    import torch.distributed as dist
+    sys.path.insert(0, ROOT)
+    import paper_2209_11337_b200 as q
+    from paper_2209_11337_b200.distributed import replicate_range
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    full = _table()
+    b, e = replicate_range(N_REPS, world, rank)
+    mine = np.zeros_like(full)
+    mine[b:e] = full[b:e]                     # this rank's replicate rows only
+    t = torch.from_numpy(mine)
+    dist.all_reduce(t)                        # the one exchange step
+    res = q.qmccpw_finalize(t.numpy(), [0, 1, 2], _plist(q), N_POINTS, N_REPS, q.config())
+    np.save(os.path.join(outdir, f"rank{rank}.npy"),
+            np.array([[r.mean[:], r.se[:], r.sigma_run[:], r.within_var[:]] for r in res]))
+    np.save(os.path.join(outdir, f"table{rank}.npy"), t.numpy())
+    dist.destroy_process_group()
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def test_gloo_world2_allreduce_is_exact_and_matches_single_process():
+    import torch.multiprocessing as mp
+    import paper_2209_11337_b200 as q
+    with tempfile.TemporaryDirectory() as d:
+        mp.spawn(_worker, args=(2, _free_port(), d), nprocs=2, join=True)
+        full = _table()
+        ref = q.qmccpw_finalize(full, [0, 1, 2], _plist(q), N_POINTS, N_REPS, q.config())
+        ref = np.array([[r.mean[:], r.se[:], r.sigma_run[:], r.within_var[:]] for r in ref])
+        for rank in (0, 1):
+            assert np.array_equal(np.load(os.path.join(d, f"table{rank}.npy")), full)
+            assert np.array_equal(np.load(os.path.join(d, f"rank{rank}.npy")), ref)
+
+
+def test_finalize_refuses_a_missing_rank():
+    import paper_2209_11337_b200 as q
+    from paper_2209_11337_b200.distributed import replicate_range
+    full = _table()
+    b, e = replicate_range(N_REPS, 4, 2)
+    partial = full.copy()
+    partial[b:e] = 0.0                        # rank 2 of 4 never contributed
+    with pytest.raises(q.QmcCpwError) as err:
+        q.qmccpw_finalize(partial, [0, 1, 2], _plist(q), N_POINTS, N_REPS, q.config())
+    assert err.value.code == q.EINVAL and "incomplete" in str(err.value)
+
+
+def test_finalize_matches_the_paper_statistics():
+    # C_l = p + S1_l/N, C = mean_l C_l, sigma = sqrt(mean (C_l - C)^2):
+    # shift-invariance in the pivot means C - mean_l(S1_l/N) is the same for every replicate split
+    import paper_2209_11337_b200 as q
+    full = _table()
+    r = q.qmccpw_finalize(full, [0, 1, 2], _plist(q), N_POINTS, N_REPS, q.config())
+    for o in range(N_OPT):
+        for qq in range(4):
+            Cl = full[:, o * 8 + qq * 2] / N_POINTS
+            sig = np.sqrt(np.mean((Cl - Cl.mean()) ** 2))
+            assert abs(r[o].sigma_run[qq] - sig) <= 1e-12 * sig
+            assert abs(r[o].se[qq] - sig * np.sqrt(N_REPS / (N_REPS - 1)) / np.sqrt(N_REPS)) <= 1e-12 * sig
+
+
+def test_bench_reference_arm_runs_on_cpu():
+    out = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--impl", "reference", "--steps", "1",
+                          "--warmup", "0"], capture_output=True, text=True, timeout=600)
+    assert out.returncode == 0, out.stderr
+    import json
+    lines = [l for l in out.stdout.splitlines() if l.startswith("{")]
+    assert len(lines) == 1
+    d = json.loads(lines[0])
+    assert d["impl"] == "reference" and d["value"] > 0 and d["cpu_baseline"]["kind"] == "oracle"
+    assert d["e2e"]["h2d_bytes_per_step"] == 0
