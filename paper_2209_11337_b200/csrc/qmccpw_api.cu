@@ -183,7 +183,9 @@ int tpb_log2_for(const qmccpw_config& c, int d, int n_opt) {
     for (int lg = 7; lg >= 5; --lg) {
         size_t tpb = (size_t)1 << lg, nw = tpb / 32;
         size_t b = (size_t)n_opt * 8 * tpb * 8;
-        if (need_buf) b += (size_t)d * tpb * 8;
+        const bool mma = c.method == QMCCPW_QMC_CPW && c.construction == QMCCPW_PCA && c.conditioning == QMCCPW_COND_W1;
+        if (mma) b += (size_t)((d + 7) & ~7) * (tpb + 8) * 8;
+        else if (need_buf) b += (size_t)d * tpb * 8;
         if (two_buf) b += (size_t)d * tpb * 8;
         const size_t hw = 4 * nw * d * 4;
         b += ((size_t)d * 64 + d) * 4 + 4 + (hw > 1024 ? hw : 1024);
@@ -271,7 +273,8 @@ int carve(DeviceCache* c, const Plan& pl, bool own_partials, uint32_t table_reps
     size_t off = 0;
     size_t o_vscr = off; off = align_up(off + (size_t)table_reps * d * 32 * 4);
     size_t o_shift = off; off = align_up(off + (size_t)table_reps * d * 4);
-    size_t o_M = off; off = align_up(off + (size_t)d * d * 8);
+    const int ld = (d + 7) & ~7;
+    size_t o_M = off; off = align_up(off + (size_t)ld * ld * 8);
     size_t o_a = off; off = align_up(off + (size_t)d * 8);
     size_t o_isa = off; off = align_up(off + (size_t)d * 8);
     size_t o_part = off; off = align_up(off + (own_partials ? (size_t)pl.n_cells * pl.stride * 8 : 0));
@@ -307,7 +310,7 @@ int build_tables(DeviceCache* c, const Plan& pl, uint32_t rep_base, uint32_t tab
                                       s.shift, st));
     }
     if (cfg.method == QMCCPW_QMC_CPW && (cfg.construction == QMCCPW_PCA || cfg.conditioning == QMCCPW_COND_X1))
-        CUDA_TRY(launch_path_matrix(cfg.construction, pl.d, pl.p[0].T, pl.p[0].sigma,
+        CUDA_TRY(launch_path_matrix(cfg.construction, pl.d, (pl.d + 7) & ~7, pl.p[0].T, pl.p[0].sigma,
                                     cfg.construction == QMCCPW_PCA ? s.M : nullptr, s.a, s.inv_sa, st));
     return QMCCPW_OK;
 }
@@ -383,6 +386,7 @@ PathArgs make_args(const Plan& pl, const Scratch& s) {
     a.vscr = s.vscr;
     a.shift = s.shift;
     a.M = s.M;
+    a.M_ld = (d + 7) & ~7;
     a.a = s.a;
     a.inv_sa = s.inv_sa;
     a.seed = pl.cfg.seed;

@@ -61,7 +61,8 @@ struct PathArgs {
     // tables (device pointers)
     const uint32_t* vscr;    // [n_reps][d][32] scrambled direction numbers
     const uint32_t* shift;   // [n_reps][d]
-    const double* M;         // [d][d] path matrix (PCA, and X1 for PCA)
+    const double* M;         // [M_ld][M_ld] path matrix (PCA), zero-padded to a multiple of 8
+    int M_ld;
     const double* a;         // [d] first column a_j of the path matrix (X1)
     const double* inv_sa;    // [d] 1/(sigma a_j)   (X1)
     // LR
@@ -78,7 +79,7 @@ struct PathArgs {
 cudaError_t launch_randomization(const uint32_t* d_base_v, const uint32_t* d_base_shift, int d, uint32_t n_reps,
                                  uint32_t rep_base, uint64_t seed, int mode, uint32_t* d_vscr, uint32_t* d_shift,
                                  cudaStream_t st);
-cudaError_t launch_path_matrix(int construction, int d, double T, double sigma, double* d_M, double* d_a,
+cudaError_t launch_path_matrix(int construction, int d, int ld, double T, double sigma, double* d_M, double* d_a,
                                double* d_inv_sa, cudaStream_t st);
 cudaError_t launch_paths(const PathArgs& args, int construction, int conditioning, int method, cudaStream_t st,
                          int* smem_bytes_out);

@@ -95,13 +95,15 @@ cudaError_t launch_randomization(const uint32_t* d_base_v, const uint32_t* d_bas
 // with sinpi on exactly reduced rational arguments.  a_j = M_j1 for every
 // construction (STD: sqrt(dt); BB: t_j/sqrt(T)).
 // ---------------------------------------------------------------------------
-__global__ void path_matrix_kernel(int construction, int d, double T, double sigma, double* __restrict__ M,
+__global__ void path_matrix_kernel(int construction, int d, int ld, double T, double sigma, double* __restrict__ M,
                                    double* __restrict__ a, double* __restrict__ inv_sa) {
     const int idx = blockIdx.x * blockDim.x + threadIdx.x;
     const double dt = T / d;
     const long long den = 2LL * d + 1;
-    if (construction == kPca && M != nullptr && idx < d * d) {
-        const int j = idx / d + 1, k = idx % d + 1;
+    if (construction == kPca && M != nullptr && idx < ld * ld && (idx / ld >= d || idx % ld >= d)) {
+        M[idx] = 0.0;  // zero padding to the mma tile multiple
+    } else if (construction == kPca && M != nullptr && idx < ld * ld) {
+        const int j = idx / ld + 1, k = idx % ld + 1;
         const double sh = sinpi((double)(2 * k - 1) / (double)(2 * den));        // sin(theta_k / 2)
         const long long num = ((long long)j * (2 * k - 1)) % (2 * den);           // j theta_k / pi mod 2
         const double s = sinpi((double)num / (double)den);
@@ -124,11 +126,11 @@ __global__ void path_matrix_kernel(int construction, int d, double T, double sig
     }
 }
 
-cudaError_t launch_path_matrix(int construction, int d, double T, double sigma, double* d_M, double* d_a,
+cudaError_t launch_path_matrix(int construction, int d, int ld, double T, double sigma, double* d_M, double* d_a,
                                double* d_inv_sa, cudaStream_t st) {
-    const int n = (construction == kPca && d_M) ? d * d : d;
+    const int n = (construction == kPca && d_M) ? (ld * ld > d ? ld * ld : d) : d;
     const int tpb = 256;
-    path_matrix_kernel<<<(n + tpb - 1) / tpb, tpb, 0, st>>>(construction, d, T, sigma, d_M, d_a, d_inv_sa);
+    path_matrix_kernel<<<(n + tpb - 1) / tpb, tpb, 0, st>>>(construction, d, ld, T, sigma, d_M, d_a, d_inv_sa);
     ++launch_counter();
     return cudaGetLastError();
 }
@@ -456,6 +458,7 @@ __global__ void __launch_bounds__(128) paths_kernel(const PathArgs P) {
     const int ppt = kCellPoints >> tpb_log2;
     constexpr bool kNeedBuf = (METHOD == kQmc) && (CONSTR == kPca || COND == kX1);
     constexpr bool kTwoBuf = (METHOD == kQmc) && (CONSTR == kPca && COND == kX1);
+    constexpr bool kWarpMma = (METHOD == kQmc) && (CONSTR == kPca && COND == kW1);
 
     // shared memory carve-up (8-byte aligned first):
     //   acc [n_opt*8][tpb] | buf0, buf1 [d][tpb] | vt [d][32] | sh [d] | G [d][32] | pad | HW [2][2][nw][d] (>= 1 KB)
@@ -464,7 +467,7 @@ __global__ void __launch_bounds__(128) paths_kernel(const PathArgs P) {
     const int n_acc = P.n_opt * 8;
     double* accs = reinterpret_cast<double*>(smem_raw);
     double* buf0 = accs + (size_t)n_acc * tpb;
-    double* buf1 = buf0 + (kNeedBuf ? (size_t)d * tpb : 0);
+    double* buf1 = buf0 + (kWarpMma ? (size_t)P.M_ld * (tpb + 8) : (kNeedBuf ? (size_t)d * tpb : 0));
     uint32_t* vt = reinterpret_cast<uint32_t*>(buf1 + (kTwoBuf ? (size_t)d * tpb : 0));
     uint32_t* sh = vt + (METHOD == kQmc ? (size_t)d * 32 : 0);
     uint32_t* G = sh + (METHOD == kQmc ? d : 0);
@@ -485,6 +488,8 @@ __global__ void __launch_bounds__(128) paths_kernel(const PathArgs P) {
         sobol_build_g(vt, d, G, tid, tpb);
     }
     for (int v = 0; v < n_acc; ++v) accs[v * tpb + tid] = 0.0;
+    if (kWarpMma)  // zero X rows d..dp-1 (the padded K of the mma tiles)
+        for (int r = d; r < P.M_ld; ++r) buf0[(size_t)r * (tpb + 8) + tid] = 0.0;
     unsigned unconverged = 0, ties = 0, npts = 0;
 
     for (int a = 0; a < ppt; ++a) {
@@ -496,8 +501,9 @@ __global__ void __launch_bounds__(128) paths_kernel(const PathArgs P) {
             sob.HW = HWb;
         }
         const uint64_t i = i0 + tid + ((uint64_t)a << tpb_log2);
-        if (i >= P.n_points) continue;
-        ++npts;
+        const bool valid = i < P.n_points;
+        if (!valid && !kWarpMma) continue;  // the mma.sync path needs every lane of the warp
+        npts += valid ? 1u : 0u;
         const uint64_t k = P.point_offset + i;
         double f[kMaxOpt][4];
 
@@ -570,42 +576,131 @@ __global__ void __launch_bounds__(128) paths_kernel(const PathArgs P) {
                 }
                 if (d & 1) w1.push(P, d - 1, Wpend);
             } else {
-                // PCA: W = M x (the dense contraction), x staged per thread in shared memory,
-                // two rows of M per pass so every x load feeds two DFMAs
-                double* xb = buf0 + tid;
+                // PCA: W = X M^T, the one dense contraction, on the FP64 tensor
+                // cores.  Each thread writes its path's normals as a column of X (shared
+                // memory, row stride tpb + 8 doubles: the 4 k-rows of an A fragment fall on
+                // disjoint bank halves); each warp then runs mma.sync.m8n8k4.f64 (SASS DMMA)
+                // over its 32 paths x dp times: A = X[k][path] (8 paths x 4 k), B = M[j][k]
+                // (4 k x 8 j, from L1), D = 8 paths x 8 j.  Lane (q = lane/4, r = lane%4) ends
+                // up holding W for paths 8 rt + q (rt = 0..3) at times jt + 2r + {0,1}; it
+                // accumulates those paths' S~ statistics, the quad reduces them, and the
+                // owning lane takes them over for the tail.
+                const int XS = tpb + 8;
+                const int dp = P.M_ld;
+                double* xc = buf0 + tid;
                 int kk = 0;
 #pragma unroll 1
                 for (; kk + 1 < d; kk += 2) {
-                    double xa, xc;
-                    normal_from_u32_x2(sob.get(kk), sob.get(kk + 1), xa, xc);
-                    xb[kk * tpb] = xa;
-                    xb[(kk + 1) * tpb] = xc;
+                    double xa, xc2;
+                    normal_from_u32_x2(sob.get(kk), sob.get(kk + 1), xa, xc2);
+                    xc[kk * XS] = xa;
+                    xc[(kk + 1) * XS] = xc2;
                 }
-                if (kk < d) xb[kk * tpb] = normal_from_u32(sob.get(kk));
-                double W1 = 0.0;
-                int j = 0;
+                if (kk < d) xc[kk * XS] = normal_from_u32(sob.get(kk));
+                __syncwarp();
+                const int lane = tid & 31, q = lane >> 2, r4 = lane & 3;
+                const double* Xw = buf0 + (tid & ~31);
+                double sS[4], sI[4], em[4], es[4], ym[4], W1r[4];
+                int jm[4];
+#pragma unroll
+                for (int rt = 0; rt < 4; ++rt) {
+                    sS[rt] = 0.0; sI[rt] = 0.0; em[rt] = -CUDART_INF; es[rt] = -CUDART_INF; ym[rt] = 0.0;
+                    jm[rt] = 0x7fffffff; W1r[rt] = 0.0;
+                }
 #pragma unroll 1
-                for (; j + 1 < d; j += 2) {
-                    const double* Ma = P.M + (size_t)j * d;
-                    const double* Mb = Ma + d;
-                    double Wa = 0.0, Wb = 0.0;
-#pragma unroll 4
-                    for (int q = 0; q < d; ++q) {
-                        const double xq = xb[q * tpb];
-                        Wa = fma(__ldg(Ma + q), xq, Wa);
-                        Wb = fma(__ldg(Mb + q), xq, Wb);
+                for (int jt = 0; jt < dp; jt += 8) {
+                    double acc[4][2];
+#pragma unroll
+                    for (int rt = 0; rt < 4; ++rt) acc[rt][0] = acc[rt][1] = 0.0;
+                    const double* Mrow = P.M + (size_t)(jt + q) * dp + r4;
+                    const double* Xk = Xw + (size_t)r4 * XS + q;
+#pragma unroll 2
+                    for (int kt = 0; kt < dp; kt += 4) {
+                        const double bfrag = __ldg(Mrow + kt);
+                        const double* Xr = Xk + (size_t)kt * XS;
+#pragma unroll
+                        for (int rt = 0; rt < 4; ++rt) {
+                            const double afrag = Xr[8 * rt];
+                            asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+                                         : "+d"(acc[rt][0]), "+d"(acc[rt][1])
+                                         : "d"(afrag), "d"(bfrag));
+                        }
                     }
-                    if (j == 0) W1 = Wa;
-                    w1.push2(P, j, Wa - W1, Wb - W1);
+                    if (jt == 0) {
+#pragma unroll
+                        for (int rt = 0; rt < 4; ++rt) W1r[rt] = __shfl_sync(0xffffffffu, acc[rt][0], lane & ~3);
+                    }
+                    const int j0 = jt + 2 * r4;
+#pragma unroll
+                    for (int rt = 0; rt < 4; ++rt) {
+                        const double Wa = acc[rt][0] - W1r[rt], Wb = acc[rt][1] - W1r[rt];
+                        const double ta = (double)j0 * P.t1, tb = ta + P.t1;
+                        const double ea = fma(P.sigma, Wa, P.omega * ta), eb = fma(P.sigma, Wb, P.omega * tb);
+                        double Xa, Xb;
+                        fast_exp_x2(ea, eb, Xa, Xb);
+                        const double va = (j0 < d) ? 1.0 : 0.0, vb = (j0 + 1 < d) ? 1.0 : 0.0;
+                        const double Sa = P.S0 * Xa * va, Sb = P.S0 * Xb * vb;
+                        const double ya = fma(-P.sigma, ta, Wa), yb = fma(-P.sigma, tb, Wb);
+                        sS[rt] += Sa;
+                        sI[rt] = fma(Sa, ya, sI[rt]);
+                        sS[rt] += Sb;
+                        sI[rt] = fma(Sb, yb, sI[rt]);
+                        if (P.has_lookback) {
+                            const double eav = (j0 < d) ? ea : -CUDART_INF, ebv = (j0 + 1 < d) ? eb : -CUDART_INF;
+                            // lowest index wins ties (j0 < j0 + 1 < later tiles)
+                            bool gt = eav > em[rt];
+                            es[rt] = fmax(es[rt], gt ? em[rt] : eav);
+                            ym[rt] = gt ? ya : ym[rt];
+                            jm[rt] = gt ? j0 : jm[rt];
+                            em[rt] = gt ? eav : em[rt];
+                            gt = ebv > em[rt];
+                            es[rt] = fmax(es[rt], gt ? em[rt] : ebv);
+                            ym[rt] = gt ? yb : ym[rt];
+                            jm[rt] = gt ? j0 + 1 : jm[rt];
+                            em[rt] = gt ? ebv : em[rt];
+                        }
+                    }
                 }
-                if (j < d) {
-                    const double* Ma = P.M + (size_t)j * d;
-                    double Wa = 0.0;
-                    for (int q = 0; q < d; ++q) Wa = fma(__ldg(Ma + q), xb[q * tpb], Wa);
-                    if (j == 0) W1 = Wa;
-                    w1.push(P, j, Wa - W1);
+                __syncwarp();  // X may be overwritten by the next point only after every lane's mma
+                // quad reduction (lanes 4q..4q+3 hold disjoint j's of the same paths)
+#pragma unroll
+                for (int rt = 0; rt < 4; ++rt) {
+#pragma unroll
+                    for (int off = 1; off <= 2; off <<= 1) {
+                        sS[rt] += __shfl_xor_sync(0xffffffffu, sS[rt], off);
+                        sI[rt] += __shfl_xor_sync(0xffffffffu, sI[rt], off);
+                        if (P.has_lookback) {
+                            const double pe = __shfl_xor_sync(0xffffffffu, em[rt], off);
+                            const double pes = __shfl_xor_sync(0xffffffffu, es[rt], off);
+                            const double py = __shfl_xor_sync(0xffffffffu, ym[rt], off);
+                            const int pj = __shfl_xor_sync(0xffffffffu, jm[rt], off);
+                            const bool take = pe > em[rt] || (pe == em[rt] && pj < jm[rt]);
+                            es[rt] = fmax(fmax(es[rt], pes), fmin(em[rt], pe));
+                            em[rt] = take ? pe : em[rt];
+                            ym[rt] = take ? py : ym[rt];
+                            jm[rt] = take ? pj : jm[rt];
+                        }
+                    }
+                }
+                // hand path 8 rt + q's statistics to its owner lane (lane = 8 rt + q)
+                const int src = 4 * (lane & 7), mine = lane >> 3;
+#pragma unroll
+                for (int rt = 0; rt < 4; ++rt) {
+                    const double a0 = __shfl_sync(0xffffffffu, sS[rt], src);
+                    const double a1 = __shfl_sync(0xffffffffu, sI[rt], src);
+                    const double a2 = __shfl_sync(0xffffffffu, em[rt], src);
+                    const double a3 = __shfl_sync(0xffffffffu, es[rt], src);
+                    const double a4 = __shfl_sync(0xffffffffu, ym[rt], src);
+                    if (rt == mine) {
+                        w1.sumS = a0;
+                        w1.sumI = a1;
+                        w1.emax = a2;
+                        w1.esec = a3;
+                        w1.ymax = a4;
+                    }
                 }
             }
+            if (!valid) continue;
             if (P.has_lookback && w1.emax - w1.esec < 1e-12) ++ties;
             tail_w1_all(P, w1, f);
         } else {
@@ -677,8 +772,8 @@ __global__ void __launch_bounds__(128) paths_kernel(const PathArgs P) {
                 int j = 0;
 #pragma unroll 1
                 for (; j + 1 < d; j += 2) {
-                    const double* Ma = P.M + (size_t)j * d;
-                    const double* Mb = Ma + d;
+                    const double* Ma = P.M + (size_t)j * P.M_ld;
+                    const double* Mb = Ma + P.M_ld;
                     double Ra = 0.0, Rb = 0.0;
 #pragma unroll 4
                     for (int q = 1; q < d; ++q) {
@@ -690,7 +785,7 @@ __global__ void __launch_bounds__(128) paths_kernel(const PathArgs P) {
                     cb[(j + 1) * tpb] = P.lnS0 + P.omega * (double)(j + 2) * P.t1 + P.sigma * Rb;
                 }
                 if (j < d) {
-                    const double* Ma = P.M + (size_t)j * d;
+                    const double* Ma = P.M + (size_t)j * P.M_ld;
                     double Ra = 0.0;
                     for (int q = 1; q < d; ++q) Ra = fma(__ldg(Ma + q), xb[q * tpb], Ra);
                     cb[j * tpb] = P.lnS0 + P.omega * (double)(j + 1) * P.t1 + P.sigma * Ra;
@@ -757,7 +852,8 @@ static size_t path_smem_bytes(const PathArgs& a, int constr, int cond, int metho
     const bool need_buf = method == kQmc && (constr == kPca || cond == kX1);
     const bool two_buf = method == kQmc && constr == kPca && cond == kX1;
     size_t b = (size_t)a.n_opt * 8 * tpb * sizeof(double);
-    if (need_buf) b += (size_t)a.d * tpb * sizeof(double);
+    if (method == kQmc && constr == kPca && cond == kW1) b += (size_t)a.M_ld * (tpb + 8) * sizeof(double);
+    else if (need_buf) b += (size_t)a.d * tpb * sizeof(double);
     if (two_buf) b += (size_t)a.d * tpb * sizeof(double);
     size_t hw = 0;
     if (method == kQmc) {
@@ -769,19 +865,39 @@ static size_t path_smem_bytes(const PathArgs& a, int constr, int cond, int metho
 }
 
 template <int C, int K, int M>
-static cudaError_t launch_paths_t(const PathArgs& args, cudaStream_t st, int* smem_out) {
-    const size_t smem = path_smem_bytes(args, C, K, M);
-    if (smem_out) *smem_out = (int)smem;
+static cudaError_t launch_paths_t(const PathArgs& args_in, cudaStream_t st, int* smem_out) {
     // raise the dynamic-smem limit once per device (not on every call: it is a driver round trip)
     static thread_local int set_for[64] = {0};
     int dev = 0;
     cudaGetDevice(&dev);
-    if (set_for[dev & 63] < (int)smem) {
+    if (set_for[dev & 63] == 0) {
         cudaError_t e = cudaFuncSetAttribute(paths_kernel<C, K, M>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                              200 * 1024);
         if (e != cudaSuccess) return e;
-        set_for[dev & 63] = 200 * 1024;
+        set_for[dev & 63] = 1;
     }
+    // block size: the candidate (128, 64, 32 threads) with the most resident warps per SM
+    // (registers and shared memory both counted by the occupancy calculator); a deterministic
+    // function of (mode, d, n_opt), so results stay independent of the GPU count.
+    PathArgs args = args_in;
+    int best_lg = -1, best_warps = -1;
+    for (int lg = 7; lg >= 5; --lg) {
+        args.tpb_log2 = lg;
+        const size_t smem = path_smem_bytes(args, C, K, M);
+        if (smem > 200 * 1024) continue;
+        int nb = 0;
+        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, paths_kernel<C, K, M>, 1 << lg, smem) != cudaSuccess)
+            continue;
+        const int warps = nb * (1 << lg) / 32;
+        if (warps > best_warps) {
+            best_warps = warps;
+            best_lg = lg;
+        }
+    }
+    if (best_lg < 0) return cudaErrorInvalidConfiguration;
+    args.tpb_log2 = best_lg;
+    const size_t smem = path_smem_bytes(args, C, K, M);
+    if (smem_out) *smem_out = (int)smem;
     const uint64_t nblocks = args.cell_end - args.cell_begin;
     if (nblocks == 0) return cudaSuccess;
     paths_kernel<C, K, M><<<(unsigned)nblocks, 1 << args.tpb_log2, smem, st>>>(args);
