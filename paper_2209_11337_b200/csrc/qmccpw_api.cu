@@ -382,6 +382,11 @@ PathArgs make_args(const Plan& pl, const Scratch& s) {
                 break;
             }
     }
+    for (int o = 0; o < pl.n_opt; ++o) {
+        a.x1_need_arith[o] = 0;
+        for (int q = 0; q < pl.n_opt; ++q)
+            if (a.tail_leader[q] == o && pl.types[q] == QMCCPW_ARITH_ASIAN_CALL) a.x1_need_arith[o] = 1;
+    }
     a.mean_a = mean_first_column(pl.cfg.construction, d, p.T);
     a.vscr = s.vscr;
     a.shift = s.shift;

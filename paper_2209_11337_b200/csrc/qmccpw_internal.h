@@ -51,6 +51,7 @@ struct PathArgs {
     // options
     int has_lookback;        // track S~_max / argmax (lookback present)
     int tail_leader[kMaxOpt];  // first option with the same strike and statistic (shares psi etc.)
+    int x1_need_arith[kMaxOpt];  // X1: some option of this leader's strike group is arithmetic
     int type[kMaxOpt];
     double K[kMaxOpt];
     double lnK[kMaxOpt];

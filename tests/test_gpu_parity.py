@@ -111,6 +111,15 @@ def test_path_values_lr(q, O, otype):
         _pv_check(q, O, otype, 100.0, d, 0, 0, 1, 2, 5, 1500)
 
 
+@pytest.mark.parametrize("cond", [0, 1])
+@pytest.mark.parametrize("d", [2, 8, 24, 40, 72, 96, 128, 200])
+def test_path_values_pca_tile_edges(q, O, cond, d):
+    # the tensor-core PCA kernel (d <= 128 in 8-wide tiles) and its fallback (other d);
+    # ragged point ranges so some lanes of the last warp carry no point
+    for otype in ((0, 1) if cond else (0, 1, 2)):
+        _pv_check(q, O, otype, 100.0, d, 2, cond, 0, 1, 17, 17 + 301)
+
+
 @pytest.mark.parametrize("constr,cond", [(1, 0), (2, 0), (2, 1)])
 def test_path_values_d256_and_other_markets(q, O, constr, cond):
     _pv_check(q, O, 0, 100.0, 256, constr, cond, 0, 1, 0, 200)
