@@ -65,8 +65,12 @@ typedef enum {
 } qmccpw_conditioning;
 
 typedef enum {
-    QMCCPW_QMC_CPW = 0, /* randomised Sobol' + conditional pathwise estimators */
-    QMCCPW_LR_MC = 1    /* Monte Carlo likelihood-ratio baseline, P:604-629 (STD path only) */
+    QMCCPW_QMC_CPW = 0,  /* randomised Sobol' + conditional pathwise estimators;
+                            STD = the paper's QMC-CPW, BB = QMC+BB-CPW */
+    QMCCPW_LR_MC = 1,    /* Monte Carlo likelihood-ratio baseline, P:604-629 (STD path only) */
+    QMCCPW_MC_CPW = 2,   /* pseudo-random (Philox) normals + CPW estimators; STD/BB, W1 */
+    QMCCPW_MC_AV_CPW = 3 /* MC-CPW with antithetic pairs x, -x averaged; STD/BB, W1;
+                            n_points counts pairs */
 } qmccpw_method;
 
 typedef enum {
@@ -116,6 +120,7 @@ typedef struct {
  *   NULL p or out.
  * EUNSUPPORTED: BB with d != 2^m (Alg. 4 is defined for 2^m steps);
  *   X1 with the lookback; LR_MC with a construction other than STD;
+ *   MC_CPW / MC_AV_CPW with PCA or X1;
  *   d > 256 on the GPU. */
 int qmccpw_price_greeks(int32_t option, const qmccpw_params* p, uint64_t n_points, uint32_t n_replicates,
                         const qmccpw_config* cfg, qmccpw_result* out);

@@ -19,7 +19,7 @@ JOE_KUO = os.path.join(HERE, "data", "new-joe-kuo-6.1024.txt")
 ARITH, BINARY, LOOKBACK, GEOM_CALL, GEOM_DIGITAL = 0, 1, 2, 100, 101
 STD, BB, PCA = 0, 1, 2
 W1, X1 = 0, 1
-QMC_CPW, LR_MC = 0, 1
+QMC_CPW, LR_MC, MC_CPW, MC_AV_CPW = 0, 1, 2, 3
 RAND_LMS_SHIFT, RAND_SHIFT, RAND_NONE = 0, 1, 3
 DEFAULT_SEED = 2209113370
 

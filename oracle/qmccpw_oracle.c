@@ -578,6 +578,19 @@ static int estimate_impl(const or_option* opt, const or_market* mk, int method, 
     mkt_fill(&m, mk, opt->K);
     if (near_tie) *near_tie = 0;
     if (method == OR_LR_MC) return estimate_lr(opt->type, &m, x, out);
+    if (method == OR_MC_AV_CPW) {
+        /* the estimate from the path of x and from its antithetic path -x, combined */
+        double* xm = malloc(sizeof(double) * mk->d);
+        double o1[4], o2[4];
+        int t1 = 0, t2 = 0;
+        for (int j = 0; j < mk->d; j++) xm[j] = -x[j];
+        int rc = estimate_impl(opt, mk, OR_QMC_CPW, construction, conditioning, M, x, o1, near_tie ? &t1 : NULL);
+        if (rc == 0) rc = estimate_impl(opt, mk, OR_QMC_CPW, construction, conditioning, M, xm, o2, near_tie ? &t2 : NULL);
+        for (int q = 0; q < 4; q++) out[q] = 0.5 * (o1[q] + o2[q]);
+        if (near_tie) *near_tie = t1 + t2;
+        free(xm);
+        return rc;
+    }
     if (conditioning == OR_COND_X1) return estimate_x1(opt->type, &m, M, x, out);
     double* W = malloc(sizeof(double) * mk->d);
     int rc = or_construct(construction, mk->d, mk->T, x, W);
@@ -594,6 +607,9 @@ static int validate(const or_option* opt, const or_market* mk, int method, int c
     if (mk->d < 1 || mk->d > OR_MAX_DIM) return set_err(-1, "d out of range");
     if (construction == OR_BB && !is_pow2(mk->d)) return set_err(-2, "BB needs d = 2^m");
     if (method == OR_LR_MC && construction != OR_STD) return set_err(-2, "LR+MC uses the STD path");
+    if ((method == OR_MC_CPW || method == OR_MC_AV_CPW) && (construction == OR_PCA || conditioning != OR_COND_W1))
+        return set_err(-2, "MC-CPW / MC+AV-CPW: STD or BB construction, W1 conditioning");
+    if (method < 0 || method > 3) return set_err(-1, "unknown method");
     if (method == OR_QMC_CPW && conditioning == OR_COND_X1 && opt->type != OR_ARITH && opt->type != OR_BINARY)
         return set_err(-2, "X1 conditioning supports arithmetic and binary Asian options only");
     return 0;
@@ -626,7 +642,7 @@ int or_path_values(const or_option* opt, const or_market* mk, const or_config* c
         or_path_matrix(cfg->construction, d, mk->T, M);
     }
     for (uint64_t k = k_begin; k < k_end && rc == 0; k++) {
-        if (cfg->method == OR_LR_MC) rc = or_lr_normals(rep, d, k, k + 1, cfg->seed, x);
+        if (cfg->method != OR_QMC_CPW) rc = or_lr_normals(rep, d, k, k + 1, cfg->seed, x);
         else rc = or_normals(rep, d, k, k + 1, cfg, x);
         if (rc == 0) rc = estimate_impl(opt, mk, cfg->method, cfg->construction, cfg->conditioning, M, x,
                                         out + 4 * (k - k_begin), NULL);
@@ -717,7 +733,7 @@ static void* worker(void* arg) {
         uint64_t ties = 0;
         for (uint64_t i = 0; i < jb->N && rc == 0; i++) {
             uint64_t k = jb->cfg->point_offset + i;
-            if (jb->cfg->method == OR_LR_MC) {
+            if (jb->cfg->method != OR_QMC_CPW) {
                 for (int j = 0; j < d; j++) x[j] = lr_normal(jb->cfg->seed, (uint32_t)rep, k, j);
             } else {
                 for (int j = 0; j < d; j++) x[j] = or_normal_from_u32(sobol_direct(v + 32 * j, c[j], k));

@@ -25,7 +25,10 @@ extern "C" {
 enum { OR_ARITH = 0, OR_BINARY = 1, OR_LOOKBACK = 2, OR_GEOM_CALL = 100, OR_GEOM_DIGITAL = 101 };
 enum { OR_STD = 0, OR_BB = 1, OR_PCA = 2 };
 enum { OR_COND_W1 = 0, OR_COND_X1 = 1 };
-enum { OR_QMC_CPW = 0, OR_LR_MC = 1 };
+/* methods compared in the paper: QMC-CPW (with the construction of the
+ * config: STD = the paper's QMC-CPW, BB = QMC+BB-CPW), LR+MC, MC-CPW and
+ * MC+AV-CPW (pseudo-random normals, antithetic pairs averaged) */
+enum { OR_QMC_CPW = 0, OR_LR_MC = 1, OR_MC_CPW = 2, OR_MC_AV_CPW = 3 };
 /* randomisation of the Sobol' points: per-replicate left-matrix scramble +
  * digital shift, shift only, none (plain Sobol'), or caller-supplied vectors */
 enum { OR_RAND_LMS_SHIFT = 0, OR_RAND_SHIFT = 1, OR_RAND_NONE = 3 };

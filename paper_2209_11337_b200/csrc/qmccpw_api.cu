@@ -143,7 +143,7 @@ int validate_params(const qmccpw_params* p) {
 }
 
 int validate_config(const qmccpw_config& c, int d, uint64_t n_points, uint32_t n_reps) {
-    if (c.method != QMCCPW_QMC_CPW && c.method != QMCCPW_LR_MC) return fail(QMCCPW_EINVAL, "unknown method");
+    if (c.method < QMCCPW_QMC_CPW || c.method > QMCCPW_MC_AV_CPW) return fail(QMCCPW_EINVAL, "unknown method");
     if (c.construction < 0 || c.construction > 2) return fail(QMCCPW_EINVAL, "unknown construction");
     if (c.conditioning < 0 || c.conditioning > 1) return fail(QMCCPW_EINVAL, "unknown conditioning");
     if (c.randomization < 0 || c.randomization > 3) return fail(QMCCPW_EINVAL, "unknown randomization");
@@ -154,6 +154,9 @@ int validate_config(const qmccpw_config& c, int d, uint64_t n_points, uint32_t n
         return fail(QMCCPW_EUNSUPPORTED, "Brownian bridge needs d = 2^m (Alg. 4, P:504)");
     if (c.method == QMCCPW_LR_MC && c.construction != QMCCPW_STD)
         return fail(QMCCPW_EUNSUPPORTED, "LR+MC uses the standard construction");
+    if ((c.method == QMCCPW_MC_CPW || c.method == QMCCPW_MC_AV_CPW) &&
+        (c.construction == QMCCPW_PCA || c.conditioning != QMCCPW_COND_W1))
+        return fail(QMCCPW_EUNSUPPORTED, "MC-CPW / MC+AV-CPW: STD or BB construction with W1 conditioning");
     if (d > kMaxDimGpu) return fail(QMCCPW_EUNSUPPORTED, "d > 256 is not supported by the sm_100a kernels");
     return QMCCPW_OK;
 }

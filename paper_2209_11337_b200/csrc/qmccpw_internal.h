@@ -14,7 +14,7 @@ constexpr int kNewtonMax = 8;
 
 enum Construction { kStd = 0, kBB = 1, kPca = 2 };
 enum Conditioning { kW1 = 0, kX1 = 1 };
-enum Method { kQmc = 0, kLr = 1 };
+enum Method { kQmc = 0, kLr = 1, kMc = 2, kMcAv = 3 };
 enum OptType { kArith = 0, kBinary = 1, kLookback = 2 };
 
 // Everything one launch of the path kernel needs, passed BY VALUE as the

@@ -200,6 +200,27 @@ __device__ __forceinline__ void sobol_build_hw(const uint32_t* vt, const uint32_
 // (P:599 with the 1/d removed, reading 3).  Near-ties are tracked with the
 // runner-up exponent.
 // ---------------------------------------------------------------------------
+// MC-CPW / MC+AV-CPW / LR+MC normals: Philox4x32-10, counter (k_lo, k_hi, j/4,
+// (rep<<8)|0x02), word j%4 (the paper's PSEUDO generator).
+__device__ __forceinline__ uint32_t pick4(const uint32_t c[4], int w) {
+    return w == 0 ? c[0] : (w == 1 ? c[1] : (w == 2 ? c[2] : c[3]));
+}
+__device__ __forceinline__ void mc_normal_pair(const PathArgs& P, uint32_t rep, uint64_t k, int ja, int jb, double& xa,
+                                               double& xb) {
+    uint32_t ca[4] = {(uint32_t)k, (uint32_t)(k >> 32), (uint32_t)(ja >> 2), (rep << 8) | 0x02u};
+    philox4x32_10(ca, (uint32_t)P.seed, (uint32_t)(P.seed >> 32));
+    const uint32_t ya = pick4(ca, ja & 3);
+    uint32_t yb;
+    if ((jb >> 2) == (ja >> 2)) {
+        yb = pick4(ca, jb & 3);
+    } else {
+        uint32_t cb[4] = {(uint32_t)k, (uint32_t)(k >> 32), (uint32_t)(jb >> 2), (rep << 8) | 0x02u};
+        philox4x32_10(cb, (uint32_t)P.seed, (uint32_t)(P.seed >> 32));
+        yb = pick4(cb, jb & 3);
+    }
+    normal_from_u32_x2(ya, yb, xa, xb);
+}
+
 struct W1Acc {
     double sumS, sumI, emax, esec, ymax;
     __device__ __forceinline__ void reset() {
@@ -256,6 +277,17 @@ struct NormalFifo {
     __device__ __forceinline__ double next(const SobolBlock& sob, DimAt dim_at) {
         if (have == 0) {
             normal_from_u32_x2(sob.get(dim_at(0)), sob.get(dim_at(1)), x0, x1);
+            have = 2;
+        }
+        const double r = (have == 2) ? x0 : x1;
+        --have;
+        return r;
+    }
+    // same, with an arbitrary pair drawer draw(dim_a, dim_b, x_a, x_b)
+    template <class Draw, class DimAt>
+    __device__ __forceinline__ double next_from(Draw draw, DimAt dim_at) {
+        if (have == 0) {
+            draw(dim_at(0), dim_at(1), x0, x1);
             have = 2;
         }
         const double r = (have == 2) ? x0 : x1;
@@ -570,6 +602,92 @@ __global__ void __launch_bounds__(128) paths_kernel(const PathArgs P) {
 
         if (METHOD == kLr) {
             lr_path(P, P.rep_base + rep_local, k, f);
+        } else if (METHOD == kMc || METHOD == kMcAv) {
+            // MC-CPW and MC+AV-CPW: pseudo-random normals through the
+            // same W1 estimator; the antithetic path of -x has W~ -> -W~ (the constructions
+            // are linear), so one traversal feeds both accumulators.
+            const uint32_t rep = P.rep_base + rep_local;
+            W1Acc w1, w1m;
+            w1.reset();
+            w1m.reset();
+            if (CONSTR == kStd) {
+                double Wt = 0.0;
+                w1.push(P, 0, 0.0);
+                if (METHOD == kMcAv) w1m.push(P, 0, 0.0);
+#pragma unroll 1
+                for (int jq = 0; jq < d; jq += 4) {
+                    uint32_t c[4] = {(uint32_t)k, (uint32_t)(k >> 32), (uint32_t)(jq >> 2), (rep << 8) | 0x02u};
+                    philox4x32_10(c, (uint32_t)P.seed, (uint32_t)(P.seed >> 32));
+                    double xs[4];
+                    normal_from_u32_x2(c[0], c[1], xs[0], xs[1]);
+                    normal_from_u32_x2(c[2], c[3], xs[2], xs[3]);
+#pragma unroll
+                    for (int w = 0; w < 4; ++w) {
+                        const int j = jq + w;
+                        if (j >= 1 && j < d) {
+                            Wt = fma(P.sqrt_t1, xs[w], Wt);
+                            w1.push(P, j, Wt);
+                            if (METHOD == kMcAv) w1m.push(P, j, -Wt);
+                        }
+                    }
+                }
+            } else {
+                NormalFifo fifo;
+                fifo.reset();
+                int pos = 0;
+                auto dim_at = [&](int o) { return (int)P.bb_seq[pos + o]; };
+                auto draw = [&](int da, int db, double& xa, double& xb) { mc_normal_pair(P, rep, k, da, db, xa, xb); };
+                double stW[12];
+                int sp = 0;
+                stW[0] = P.sqrtT * fifo.next_from(draw, dim_at);
+                pos += 2;
+                double Wl = 0.0, W1 = 0.0, Wpend = 0.0;
+                const int m = P.bb_m;
+#pragma unroll 1
+                for (int j = 1; j <= d; ++j) {
+                    const int e = (j == 1) ? m : (__ffs(j - 1) - 1);
+                    double Wj;
+                    if (e == 0) {
+                        Wj = stW[sp];
+                        --sp;
+                    } else {
+                        double Wr = stW[sp];
+#pragma unroll 1
+                        for (int c = e - 1; c >= 0; --c) {
+                            const bool refill = fifo.have == 0;
+                            const double x = fifo.next_from(draw, dim_at);
+                            pos += refill ? 2 : 0;
+                            const double Wm = fma(P.bb_b[m - c], x, 0.5 * (Wl + Wr));
+                            if (c > 0) stW[++sp] = Wm;
+                            Wr = Wm;
+                        }
+                        Wj = Wr;
+                    }
+                    if (j == 1) W1 = Wj;
+                    if (j & 1) {
+                        Wpend = Wj - W1;
+                    } else {
+                        w1.push2(P, j - 2, Wpend, Wj - W1);
+                        if (METHOD == kMcAv) w1m.push2(P, j - 2, -Wpend, -(Wj - W1));
+                    }
+                    Wl = Wj;
+                }
+                if (d & 1) {
+                    w1.push(P, d - 1, Wpend);
+                    if (METHOD == kMcAv) w1m.push(P, d - 1, -Wpend);
+                }
+            }
+            if (P.has_lookback && w1.emax - w1.esec < 1e-12) ++ties;
+            tail_w1_all(P, w1, f);
+            if (METHOD == kMcAv) {
+                if (P.has_lookback && w1m.emax - w1m.esec < 1e-12) ++ties;
+                double fm[kMaxOpt][4];
+                tail_w1_all(P, w1m, fm);
+#pragma unroll
+                for (int o = 0; o < kMaxOpt; ++o)
+#pragma unroll
+                    for (int qq = 0; qq < 4; ++qq) f[o][qq] = 0.5 * (f[o][qq] + fm[o][qq]);
+            }
         } else if (COND == kW1) {
             W1Acc w1;
             w1.reset();
@@ -1308,6 +1426,10 @@ static cudaError_t launch_paths_t(const PathArgs& args_in, cudaStream_t st, int*
 cudaError_t launch_paths(const PathArgs& args, int construction, int conditioning, int method, cudaStream_t st,
                          int* smem_out) {
     if (method == kLr) return launch_paths_t<kStd, kW1, kLr>(args, st, smem_out);
+    if (method == kMc) return construction == kBB ? launch_paths_t<kBB, kW1, kMc>(args, st, smem_out)
+                                                  : launch_paths_t<kStd, kW1, kMc>(args, st, smem_out);
+    if (method == kMcAv) return construction == kBB ? launch_paths_t<kBB, kW1, kMcAv>(args, st, smem_out)
+                                                    : launch_paths_t<kStd, kW1, kMcAv>(args, st, smem_out);
     if (construction == kPca && method == kQmc) {  // fragment-native tensor-core path for d <= 128
         bool handled = false;
         cudaError_t e = conditioning == kW1 ? launch_pca<kW1>(args, st, &handled) : launch_pca<kX1>(args, st, &handled);
@@ -1395,7 +1517,7 @@ __global__ void normals_hook_kernel(const uint32_t* __restrict__ vscr, const uin
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const int tpb_log2 = 7, tpb = 128, tid = threadIdx.x, nw = 4;
     const uint64_t K0 = k_begin + (uint64_t)blockIdx.x * kCellPoints;
-    if (method == kLr) {
+    if (method != kQmc) {  // LR+MC, MC-CPW, MC+AV-CPW: the Philox stream
         for (int a = 0; a < kCellPoints / tpb; ++a) {
             const uint64_t k = K0 + tid + ((uint64_t)a << tpb_log2);
             if (k >= k_end) break;
@@ -1450,7 +1572,7 @@ cudaError_t launch_normals_hook(const uint32_t* d_vscr, const uint32_t* d_shift,
                                 cudaStream_t st) {
     const uint64_t nk = k_end - k_begin;
     const unsigned grid = (unsigned)((nk + kCellPoints - 1) / kCellPoints);
-    const size_t smem = method == kLr ? 0 : ((size_t)d * 64 + d + 2 * 2 * 4 * d) * 4;
+    const size_t smem = method != kQmc ? 0 : ((size_t)d * 64 + d + 2 * 2 * 4 * d) * 4;
     cudaError_t e =
         cudaFuncSetAttribute(normals_hook_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;

@@ -111,6 +111,24 @@ def test_path_values_lr(q, O, otype):
         _pv_check(q, O, otype, 100.0, d, 0, 0, 1, 2, 5, 1500)
 
 
+@pytest.mark.parametrize("method", [2, 3])
+@pytest.mark.parametrize("constr", [0, 1])
+def test_path_values_mc_cpw_and_antithetic(q, O, method, constr):
+    # MC-CPW and MC+AV-CPW: Philox normals through the CPW estimators
+    for d in (1, 4, 64):
+        for otype in (0, 1, 2):
+            _pv_check(q, O, otype, 100.0, d, constr, 0, method, 2, 5, 5 + 700)
+
+
+def test_mc_methods_full_runs(q, O):
+    N, L = 2 * 4096 + 99, 5
+    for method in (2, 3):
+        for constr in (0, 1):
+            g = q.qmccpw_price_greeks_batch([0, 1, 2], [q.params(d=64)] * 3, N, L, qcfg(q, constr, 0, method))
+            o, _ = O.price_greeks([(t, 100.0) for t in (0, 1, 2)], O.market(d=64), N, L, ocfg(O, constr, 0, method))
+            _means_check(g, o)
+
+
 @pytest.mark.parametrize("cond", [0, 1])
 @pytest.mark.parametrize("d", [2, 8, 24, 40, 72, 96, 128, 200])
 def test_path_values_pca_tile_edges(q, O, cond, d):

@@ -70,6 +70,9 @@ PAPER_VRF_K100_D64 = {
     (0, "QMC-CPW"): (903, 7770, 5427), (0, "QMC+BB-CPW"): (52689, 376285, 75020),
     (1, "QMC-CPW"): (58, 1176, 126), (1, "QMC+BB-CPW"): (830, 12571, 784),
     (2, "QMC-CPW"): (21857, 6580, 89333), (2, "QMC+BB-CPW"): (40682, 35370, 212928),
+    (0, "MC-CPW"): (106, 294, 3814), (0, "MC+AV-CPW"): (963, 759, 9433),
+    (1, "MC-CPW"): (43, 771, 136), (1, "MC+AV-CPW"): (123, 2078, 201),
+    (2, "MC-CPW"): (1635, 311, 27235), (2, "MC+AV-CPW"): (12183, 1420, 72792),
 }
 
 
@@ -81,8 +84,10 @@ def test_vrf_magnitudes_match_paper_tables(O):
     lr, _ = O.price_greeks(opts, mk, P, L, O.config(method=1, construction=0))
     qmc, _ = O.price_greeks(opts, mk, P, L, O.config(construction=0))
     bb, _ = O.price_greeks(opts, mk, P, L, O.config(construction=1))
+    mc, _ = O.price_greeks(opts, mk, P, L, O.config(method=2, construction=0))
+    av, _ = O.price_greeks(opts, mk, P, L, O.config(method=3, construction=0))
     for o in range(3):
-        for name, res in (("QMC-CPW", qmc), ("QMC+BB-CPW", bb)):
+        for name, res in (("QMC-CPW", qmc), ("QMC+BB-CPW", bb), ("MC-CPW", mc), ("MC+AV-CPW", av)):
             for i, q in enumerate((1, 2, 3)):
                 vrf = (lr[o]["sigma_run"][q] / res[o]["sigma_run"][q]) ** 2
                 paper = PAPER_VRF_K100_D64[(o, name)][i]
