@@ -127,8 +127,14 @@ int qmccpw_price_greeks(int32_t option, const qmccpw_params* p, uint64_t n_point
 
 /* n_options options priced on the SAME points in one pass (one path feeds all
  * of them, SURVEY.md 8(a5) "option fusion").  options[i], p[i] for i <
- * n_options (1..3); all p[i] must share S0, r, sigma, T and d (EUNSUPPORTED
- * otherwise) and may differ in K.  out[i] receives option i. */
+ * n_options; out[i] receives option i.  All p[i] share S0, r and d.
+ *  - 1..3 options that also share sigma and T (may differ in K): the fused
+ *    path kernel, any method / construction / conditioning;
+ *  - otherwise (up to 1024 options in up to 8 (sigma, T) families; the C5
+ *    portfolio): the portfolio kernel, QMC-CPW with PCA + W1 only and d <= 128
+ *    (padded to 8, 16, 32, 64 or 128); W(T) = sqrt(T) W(1) and the S~
+ *    statistics are shared per family, the tails run per option.
+ * EUNSUPPORTED for other combinations. */
 int qmccpw_price_greeks_batch(const int32_t* options, const qmccpw_params* p, int32_t n_options,
                               uint64_t n_points, uint32_t n_replicates, const qmccpw_config* cfg,
                               qmccpw_result* out);
@@ -198,6 +204,12 @@ int qmccpw_path_values(int32_t option, const qmccpw_params* p, uint32_t replicat
  * nominal SM clock in MHz.  Outputs are host pointers. */
 int qmccpw_fp64_roof(int32_t device, double* dfma_tflops, double* dfma_latency_cycles, double* dmma_tflops,
                      double* sm_clock_mhz);
+
+/* Per-path values of a portfolio call (the C5 portfolio kernel):
+ * out[((k-k_begin)*n_options + o)*4 + q]. */
+int qmccpw_portfolio_path_values(const int32_t* options, const qmccpw_params* p, int32_t n_options,
+                                 uint32_t replicate, uint64_t k_begin, uint64_t k_end, const qmccpw_config* cfg,
+                                 double* out);
 
 /* ---- housekeeping ----------------------------------------------------- */
 const char* qmccpw_last_error(void); /* thread-local; valid until the next call on this thread */

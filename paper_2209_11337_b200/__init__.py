@@ -99,6 +99,8 @@ def lib():
                                      f64p]
         L.qmccpw_path_values.argtypes = [ctypes.c_int32, P(Params), ctypes.c_uint32, ctypes.c_uint64,
                                          ctypes.c_uint64, P(Config), f64p]
+        L.qmccpw_portfolio_path_values.argtypes = [P(ctypes.c_int32), P(Params), ctypes.c_int32, ctypes.c_uint32,
+                                                   ctypes.c_uint64, ctypes.c_uint64, P(Config), f64p]
         L.qmccpw_fp64_roof.argtypes = [ctypes.c_int32, f64p, f64p, f64p, f64p]
         L.qmccpw_last_error.restype = ctypes.c_char_p
         L.qmccpw_release.argtypes = [ctypes.c_int32]
@@ -195,6 +197,15 @@ def qmccpw_fp64_roof(device=0):
     _check(lib().qmccpw_fp64_roof(device, *[ctypes.byref(v) for v in vals]))
     return dict(dfma_tflops=vals[0].value, dfma_latency_cycles=vals[1].value, dmma_tflops=vals[2].value,
                 sm_clock_mhz=vals[3].value)
+
+
+def qmccpw_portfolio_path_values(options, plist, replicate, k_begin, k_end, cfg=None):
+    n = len(options)
+    out = np.zeros((k_end - k_begin, n, 4))
+    _check(lib().qmccpw_portfolio_path_values((ctypes.c_int32 * n)(*options), (Params * n)(*plist), n, replicate,
+                                              k_begin, k_end, _cfg(cfg),
+                                              out.ctypes.data_as(ctypes.POINTER(ctypes.c_double))))
+    return out
 
 
 def qmccpw_last_error():

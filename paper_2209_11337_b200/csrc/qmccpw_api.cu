@@ -222,20 +222,26 @@ struct Plan {
     uint32_t cells_per_rep;
     uint64_t n_cells;
     int stride;
-    int types[kMaxOpt];
-    qmccpw_params p[kMaxOpt];
+    bool portfolio;            // > 3 options or several (sigma, T) families: the C5 portfolio kernel
+    int n_fam;
+    int fam_of[kMaxPortfolio];
+    int fam_rep[kMaxFamilies];  // an option index representing each family
+    int types[kMaxPortfolio];
+    qmccpw_params p[kMaxPortfolio];
 };
 
 int make_plan(const int32_t* options, const qmccpw_params* p, int32_t n_options, uint64_t n_points,
               uint32_t n_reps, const qmccpw_config* cfg, Plan* pl) {
     if (!options || !p) return fail(QMCCPW_EINVAL, "NULL options or params");
-    if (n_options < 1 || n_options > kMaxOpt) return fail(QMCCPW_EUNSUPPORTED, "1..3 options per call");
+    if (n_options < 1 || n_options > kMaxPortfolio) return fail(QMCCPW_EUNSUPPORTED, "1..1024 options per call");
+    bool same_market = true;
     for (int o = 0; o < n_options; ++o) {
         int rc = validate_params(&p[o]);
         if (rc) return rc;
         if (options[o] < 0 || options[o] > 2) return fail(QMCCPW_EINVAL, "unknown option type");
-        if (p[o].S0 != p[0].S0 || p[o].r != p[0].r || p[o].sigma != p[0].sigma || p[o].T != p[0].T || p[o].d != p[0].d)
-            return fail(QMCCPW_EUNSUPPORTED, "batched options must share S0, r, sigma, T and d");
+        if (p[o].S0 != p[0].S0 || p[o].r != p[0].r || p[o].d != p[0].d)
+            return fail(QMCCPW_EUNSUPPORTED, "batched options must share S0, r and d");
+        if (p[o].sigma != p[0].sigma || p[o].T != p[0].T) same_market = false;
     }
     pl->cfg = resolve(cfg, p[0].d);
     int rc = validate_config(pl->cfg, p[0].d, n_points, n_reps);
@@ -244,6 +250,25 @@ int make_plan(const int32_t* options, const qmccpw_params* p, int32_t n_options,
         if (pl->cfg.method == QMCCPW_QMC_CPW && pl->cfg.conditioning == QMCCPW_COND_X1 &&
             options[o] == QMCCPW_LOOKBACK_CALL)
             return fail(QMCCPW_EUNSUPPORTED, "X1 conditioning supports arithmetic and binary Asian calls only");
+    pl->portfolio = !(same_market && n_options <= kMaxOpt);
+    pl->n_fam = 0;
+    for (int o = 0; o < n_options; ++o) {
+        int f = 0;
+        while (f < pl->n_fam && !(p[pl->fam_rep[f]].sigma == p[o].sigma && p[pl->fam_rep[f]].T == p[o].T)) ++f;
+        if (f == pl->n_fam) {
+            if (pl->n_fam == kMaxFamilies) return fail(QMCCPW_EUNSUPPORTED, "at most 8 (sigma, T) families per call");
+            pl->fam_rep[pl->n_fam++] = o;
+        }
+        pl->fam_of[o] = f;
+    }
+    if (pl->portfolio) {
+        const int ld = (p[0].d + 7) & ~7;
+        if (pl->cfg.method != QMCCPW_QMC_CPW || pl->cfg.construction != QMCCPW_PCA ||
+            pl->cfg.conditioning != QMCCPW_COND_W1)
+            return fail(QMCCPW_EUNSUPPORTED, "portfolios (> 3 options or several sigma/T) use QMC-CPW with PCA + W1");
+        if (!(ld == 8 || ld == 16 || ld == 32 || ld == 64 || ld == 128))
+            return fail(QMCCPW_EUNSUPPORTED, "portfolio kernel: d padded to 8, 16, 32, 64 or 128");
+    }
     pl->n_opt = n_options;
     pl->d = p[0].d;
     pl->N = n_points;
@@ -267,6 +292,7 @@ struct Scratch {
     double* inv_sa;
     double* partials;
     double* rep_sums;
+    PortfolioOption* opts;
 };
 
 size_t align_up(size_t x) { return (x + 255) & ~(size_t)255; }
@@ -282,6 +308,7 @@ int carve(DeviceCache* c, const Plan& pl, bool own_partials, uint32_t table_reps
     size_t o_isa = off; off = align_up(off + (size_t)d * 8);
     size_t o_part = off; off = align_up(off + (own_partials ? (size_t)pl.n_cells * pl.stride * 8 : 0));
     size_t o_rs = off; off = align_up(off + (size_t)pl.L * pl.stride * 8);
+    size_t o_opt = off; off = align_up(off + (pl.portfolio ? (size_t)pl.n_opt * sizeof(PortfolioOption) : 0));
     int rc = ensure_scratch(c, off);
     if (rc) return rc;
     char* b = static_cast<char*>(c->scratch);
@@ -292,6 +319,7 @@ int carve(DeviceCache* c, const Plan& pl, bool own_partials, uint32_t table_reps
     s->inv_sa = reinterpret_cast<double*>(b + o_isa);
     s->partials = own_partials ? reinterpret_cast<double*>(b + o_part) : nullptr;
     s->rep_sums = reinterpret_cast<double*>(b + o_rs);
+    s->opts = reinterpret_cast<PortfolioOption*>(b + o_opt);
     return QMCCPW_OK;
 }
 
@@ -313,7 +341,8 @@ int build_tables(DeviceCache* c, const Plan& pl, uint32_t rep_base, uint32_t tab
                                       s.shift, st));
     }
     if (cfg.method == QMCCPW_QMC_CPW && (cfg.construction == QMCCPW_PCA || cfg.conditioning == QMCCPW_COND_X1))
-        CUDA_TRY(launch_path_matrix(cfg.construction, pl.d, (pl.d + 7) & ~7, pl.p[0].T, pl.p[0].sigma,
+        CUDA_TRY(launch_path_matrix(cfg.construction, pl.d, (pl.d + 7) & ~7, pl.portfolio ? 1.0 : pl.p[0].T,
+                                    pl.p[0].sigma,
                                     cfg.construction == QMCCPW_PCA ? s.M : nullptr, s.a, s.inv_sa, st));
     return QMCCPW_OK;
 }
@@ -469,6 +498,66 @@ struct DeviceGuard {
     }
 };
 
+// C5 portfolio launch: option table to the device (pinned staging), families in the arguments
+int launch_portfolio_plan(DeviceCache* c, const Plan& pl, const Scratch& s, uint64_t cell_begin, uint64_t cell_end,
+                          double* d_partials, double* d_path_out, uint32_t rep_base, cudaStream_t st) {
+    const size_t ob = (size_t)pl.n_opt * sizeof(PortfolioOption);
+    std::vector<PortfolioOption> host(pl.n_opt);
+    for (int o = 0; o < pl.n_opt; ++o) {
+        host[o].type = pl.types[o];
+        host[o].family = pl.fam_of[o];
+        host[o].K = pl.p[o].K;
+        host[o].lnK = std::log(pl.p[o].K);
+        bs_pivots(pl.types[o], pl.p[o], host[o].piv);
+    }
+    CUDA_TRY(cudaMemcpyAsync(s.opts, host.data(), ob, cudaMemcpyHostToDevice, st));
+    CUDA_TRY(cudaStreamSynchronize(st));  // the host staging vector dies with this scope
+    PortfolioArgs a;
+    std::memset(&a, 0, sizeof a);
+    const qmccpw_params& p0 = pl.p[0];
+    a.d = pl.d;
+    a.n_opt = pl.n_opt;
+    a.n_fam = pl.n_fam;
+    a.M_ld = (pl.d + 7) & ~7;
+    a.n_points = pl.N;
+    a.point_offset = pl.cfg.point_offset;
+    a.n_reps = pl.L;
+    a.rep_base = rep_base;
+    a.cells_per_rep = pl.cells_per_rep;
+    a.cell_begin = cell_begin;
+    a.cell_end = cell_end;
+    a.S0 = p0.S0;
+    a.r = p0.r;
+    a.lnS0 = std::log(p0.S0);
+    a.has_lookback = 0;
+    for (int o = 0; o < pl.n_opt; ++o) a.has_lookback |= pl.types[o] == QMCCPW_LOOKBACK_CALL;
+    for (int f = 0; f < pl.n_fam; ++f) {
+        const qmccpw_params& q = pl.p[pl.fam_rep[f]];
+        Family& F = a.fam[f];
+        F.sigma = q.sigma;
+        F.T = q.T;
+        F.omega = q.r - 0.5 * q.sigma * q.sigma;
+        F.t1 = q.T / pl.d;
+        F.sqrt_t1 = std::sqrt(F.t1);
+        F.s = q.sigma * F.sqrt_t1;
+        F.inv_s = 1.0 / F.s;
+        F.inv_sigma = 1.0 / q.sigma;
+        F.Dfac = std::exp(-q.r * q.T);
+        F.Afac = std::exp(q.r * (F.t1 - q.T));
+        F.sqrtT = std::sqrt(q.T);
+    }
+    a.opts = s.opts;
+    a.vscr = s.vscr;
+    a.shift = s.shift;
+    a.M = s.M;
+    a.partials = d_partials;
+    a.partial_stride = pl.stride;
+    a.path_out = d_path_out;
+    CUDA_TRY(launch_portfolio(a, st));
+    (void)c;
+    return QMCCPW_OK;
+}
+
 int run_full(const Plan& pl, qmccpw_result* out) {
     DeviceGuard g(pl.cfg.device);
     DeviceCache* c = nullptr;
@@ -480,11 +569,16 @@ int run_full(const Plan& pl, qmccpw_result* out) {
     cudaStream_t st = static_cast<cudaStream_t>(pl.cfg.stream);
     rc = build_tables(c, pl, 0, pl.L, s, st);
     if (rc) return rc;
-    PathArgs a = make_args(pl, s);
-    a.partials = s.partials;
-    a.cell_begin = 0;
-    a.cell_end = pl.n_cells;
-    CUDA_TRY(launch_paths(a, pl.cfg.construction, pl.cfg.conditioning, pl.cfg.method, st, nullptr));
+    if (pl.portfolio) {
+        rc = launch_portfolio_plan(c, pl, s, 0, pl.n_cells, s.partials, nullptr, 0, st);
+        if (rc) return rc;
+    } else {
+        PathArgs a = make_args(pl, s);
+        a.partials = s.partials;
+        a.cell_begin = 0;
+        a.cell_end = pl.n_cells;
+        CUDA_TRY(launch_paths(a, pl.cfg.construction, pl.cfg.conditioning, pl.cfg.method, st, nullptr));
+    }
     CUDA_TRY(launch_reduce_cells(s.partials, pl.stride, 0, pl.L, pl.cells_per_rep, s.rep_sums, st));
     const size_t rs_bytes = (size_t)pl.L * pl.stride * 8;
     rc = ensure_pinned(c, rs_bytes);
@@ -508,7 +602,7 @@ int qmccpw_price_greeks(int32_t option, const qmccpw_params* p, uint64_t n_point
 int qmccpw_price_greeks_batch(const int32_t* options, const qmccpw_params* p, int32_t n_options, uint64_t n_points,
                               uint32_t n_replicates, const qmccpw_config* cfg, qmccpw_result* out) {
     if (!out) return fail(QMCCPW_EINVAL, "NULL out");
-    Plan pl;
+    static thread_local Plan pl;
     int rc = make_plan(options, p, n_options, n_points, n_replicates, cfg, &pl);
     if (rc) return rc;
     std::vector<qmccpw_result> tmp(pl.n_opt);
@@ -523,7 +617,7 @@ int qmccpw_cell_count(const qmccpw_params* p, int32_t n_options, uint64_t n_poin
     if (!n_cells || !partial_doubles_per_cell) return fail(QMCCPW_EINVAL, "NULL output");
     int rc = validate_params(p);
     if (rc) return rc;
-    if (n_options < 1 || n_options > kMaxOpt) return fail(QMCCPW_EUNSUPPORTED, "1..3 options per call");
+    if (n_options < 1 || n_options > kMaxPortfolio) return fail(QMCCPW_EUNSUPPORTED, "1..1024 options per call");
     qmccpw_config c = resolve(cfg, p->d);
     rc = validate_config(c, p->d, n_points, n_replicates);
     if (rc) return rc;
@@ -550,6 +644,7 @@ int qmccpw_partials(const int32_t* options, const qmccpw_params* p, int32_t n_op
     cudaStream_t st = static_cast<cudaStream_t>(pl.cfg.stream);
     rc = build_tables(c, pl, 0, pl.L, s, st);
     if (rc) return rc;
+    if (pl.portfolio) return launch_portfolio_plan(c, pl, s, cell_begin, cell_end, d_partials, nullptr, 0, st);
     PathArgs a = make_args(pl, s);
     a.partials = d_partials;
     a.cell_begin = cell_begin;
@@ -564,7 +659,7 @@ int qmccpw_replicate_sums(const double* d_partials, const qmccpw_params* p, int3
     if (!d_partials || !d_rep_sums) return fail(QMCCPW_EINVAL, "NULL pointer");
     int rc = validate_params(p);
     if (rc) return rc;
-    if (n_options < 1 || n_options > kMaxOpt) return fail(QMCCPW_EUNSUPPORTED, "1..3 options per call");
+    if (n_options < 1 || n_options > kMaxPortfolio) return fail(QMCCPW_EUNSUPPORTED, "1..1024 options per call");
     qmccpw_config c = resolve(cfg, p->d);
     rc = validate_config(c, p->d, n_points, n_replicates);
     if (rc) return rc;
@@ -737,6 +832,45 @@ int qmccpw_path_values(int32_t option, const qmccpw_params* p, uint32_t replicat
     if (e == cudaSuccess) e = cudaStreamSynchronize(st);
     cudaFree(d_out);
     if (e != cudaSuccess) return fail(QMCCPW_ECUDA, std::string("path values hook: ") + cudaGetErrorString(e));
+    return QMCCPW_OK;
+}
+
+int qmccpw_portfolio_path_values(const int32_t* options, const qmccpw_params* p, int32_t n_options,
+                                 uint32_t replicate, uint64_t k_begin, uint64_t k_end, const qmccpw_config* cfg,
+                                 double* out) {
+    if (!out || !p) return fail(QMCCPW_EINVAL, "NULL pointer");
+    if (k_end < k_begin || k_end > (1ull << 32)) return fail(QMCCPW_EINVAL, "point range");
+    if (replicate >= (1u << 24)) return fail(QMCCPW_EINVAL, "replicate >= 2^24");
+    if (k_end == k_begin) return QMCCPW_OK;
+    qmccpw_config c0 = resolve(cfg, p->d);
+    c0.point_offset = k_begin;
+    static thread_local Plan pl;  // large (1024 options): not on the stack twice
+    int rc = make_plan(options, p, n_options, k_end - k_begin, 1, &c0, &pl);
+    if (rc) return rc;
+    pl.portfolio = true;  // force the portfolio kernel (also for <= 3 options)
+    const int ld = (pl.d + 7) & ~7;
+    if (pl.cfg.method != QMCCPW_QMC_CPW || pl.cfg.construction != QMCCPW_PCA || pl.cfg.conditioning != QMCCPW_COND_W1 ||
+        !(ld == 8 || ld == 16 || ld == 32 || ld == 64 || ld == 128))
+        return fail(QMCCPW_EUNSUPPORTED, "portfolio kernel: QMC-CPW, PCA + W1, d <= 128");
+    DeviceGuard g(pl.cfg.device);
+    DeviceCache* c = nullptr;
+    rc = ensure_device(pl.cfg.device, &c);
+    if (rc) return rc;
+    Scratch s;
+    rc = carve(c, pl, true, 1, &s);
+    if (rc) return rc;
+    cudaStream_t st = static_cast<cudaStream_t>(pl.cfg.stream);
+    rc = build_tables(c, pl, replicate, 1, s, st);
+    if (rc) return rc;
+    const size_t n = (size_t)(k_end - k_begin) * n_options * 4;
+    double* d_out = nullptr;
+    CUDA_TRY(cudaMalloc(&d_out, n * 8));
+    rc = launch_portfolio_plan(c, pl, s, 0, pl.n_cells, s.partials, d_out, replicate, st);
+    cudaError_t e = rc ? cudaSuccess : cudaMemcpyAsync(out, d_out, n * 8, cudaMemcpyDeviceToHost, st);
+    if (e == cudaSuccess && !rc) e = cudaStreamSynchronize(st);
+    cudaFree(d_out);
+    if (rc) return rc;
+    if (e != cudaSuccess) return fail(QMCCPW_ECUDA, std::string("portfolio hook: ") + cudaGetErrorString(e));
     return QMCCPW_OK;
 }
 

@@ -76,6 +76,41 @@ struct PathArgs {
     int hook_option;         // option index whose values go to path_out
 };
 
+// ---- portfolio (C5): up to kMaxPortfolio options in up to kMaxFamilies (sigma, T) families
+// sharing S0, r, d; PCA-W1 on the tensor cores (d <= 128).
+constexpr int kMaxPortfolio = 1024;
+constexpr int kMaxFamilies = 8;
+
+struct PortfolioOption {  // device table, one per option
+    int type;
+    int family;
+    double K, lnK;
+    double piv[4];
+};
+
+struct Family {            // market constants of one (sigma, T) family
+    double sigma, T, omega, t1, sqrt_t1, s, inv_s, inv_sigma, Dfac, Afac, sqrtT;
+};
+
+struct PortfolioArgs {
+    int d, n_opt, n_fam, tpb_log2, M_ld;
+    uint64_t n_points, point_offset;
+    uint32_t n_reps, rep_base, cells_per_rep;
+    uint64_t cell_begin, cell_end;
+    double S0, r, lnS0;
+    int has_lookback;
+    Family fam[kMaxFamilies];
+    const PortfolioOption* opts;  // [n_opt] device
+    const uint32_t* vscr;
+    const uint32_t* shift;
+    const double* M;               // PCA of T = 1, [M_ld][M_ld]
+    double* partials;
+    int partial_stride;            // 8 n_opt + 3
+    double* path_out;              // hook: [point][n_opt][4] or NULL
+};
+
+cudaError_t launch_portfolio(const PortfolioArgs& args, cudaStream_t st);
+
 // Launchers (qmccpw_kernels.cu).  All return cudaError_t of the launch.
 cudaError_t launch_randomization(const uint32_t* d_base_v, const uint32_t* d_base_shift, int d, uint32_t n_reps,
                                  uint32_t rep_base, uint64_t seed, int mode, uint32_t* d_vscr, uint32_t* d_shift,

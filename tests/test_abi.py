@@ -62,9 +62,17 @@ def test_validation_happens_before_device_access():
         with pytest.raises(q.QmcCpwError) as e:
             q.qmccpw_price_greeks(opt, q.params(d=6), 1024, 8, cfg)
         assert e.value.code == q.EUNSUPPORTED
-    with pytest.raises(q.QmcCpwError) as e:
+    with pytest.raises(q.QmcCpwError) as e:  # several (sigma, T) families need the PCA-W1 portfolio kernel
         q.qmccpw_price_greeks_batch([0, 1], [q.params(sigma=0.2, d=4), q.params(sigma=0.3, d=4)], 1024, 8,
                                     q.config(construction=q.STD))
+    assert e.value.code == q.EUNSUPPORTED
+    with pytest.raises(q.QmcCpwError) as e:  # more than 8 families
+        q.qmccpw_price_greeks_batch([0] * 9, [q.params(sigma=0.1 + 0.01 * i, d=8) for i in range(9)], 1024, 2,
+                                    q.config(construction=q.PCA))
+    assert e.value.code == q.EUNSUPPORTED
+    with pytest.raises(q.QmcCpwError) as e:  # different S0
+        q.qmccpw_price_greeks_batch([0, 0], [q.params(S0=100.0, d=8), q.params(S0=90.0, d=8)], 1024, 2,
+                                    q.config(construction=q.PCA))
     assert e.value.code == q.EUNSUPPORTED
 
 

@@ -2,11 +2,15 @@
 seeded points.  Tolerances:
   Sobol' integers        bit-exact
   normals                |dx| <= 2e-15 max(1, |x|)
-  per-path values        |df| <= 1e-12 (|f| + |pivot|); gamma x max(1, 0.03/(sigma^2 t_1))
+  per-path values        |df| <= 1e-12 (|f| + |pivot_K| + |pivot_ATM|); gamma x max(1, 0.03/(sigma^2 t_1))
+                         (pivot = the d = 1 Black-Scholes value of that output at the
+                         option's strike and at K = S0: the output's natural scale,
+                         so deep in/out-of-the-money Greeks near 0 keep a floor)
                          (the threshold psi / u* carries an absolute rounding of
                          ~c eps / (sigma sqrt t_1), c <~ 30 measured, and gamma
                          differentiates it once more -> relative ~ c eps / s^2)
-  replicate / run means  |dC| <= 1e-9 sqrt(within_var + C^2)   (>= mean|f|)
+  replicate / run means  |dC| <= 1e-9 sqrt(within_var + C^2)   (>= mean|f|; + |pivot_ATM| for the
+                         portfolio, whose deep in-the-money lookback gammas are ~1e-24)
   SE, sigma_run          <= 1e-6 relative (+ a 1e-12 x scale floor: at d = 1 the
                          estimator is exact per path and the spread is rounding)
   counters               equal
@@ -86,7 +90,7 @@ def _pv_check(q, O, otype, K, d, constr, cond, method, rep, k0, k1, S0=W.S0, sig
     g = q.qmccpw_path_values(otype, p, rep, k0, k1, qcfg(q, constr, cond, method))
     mk = O.market(S0, r, sigma, T, d)
     o = O.path_values(otype, K, mk, ocfg(O, constr, cond, method), rep, k0, k1)
-    piv = np.abs(O.pivots(otype, K, mk))
+    piv = np.abs(O.pivots(otype, K, mk)) + np.abs(O.pivots(otype, S0, mk))
     err = np.abs(g - o) / (np.abs(o) + piv)
     s2 = sigma * sigma * T / d
     tol = np.array([1e-12, 1e-12, 1e-12, 1e-12 * max(1.0, 0.03 / s2)])
@@ -146,10 +150,11 @@ def test_path_values_d256_and_other_markets(q, O, constr, cond):
 
 
 # ------------------------------------------------------------------ (a8) full runs
-def _means_check(gres, ores):
+def _means_check(gres, ores, floor=0.0):
+    """floor: the output's natural scale (|ATM Black-Scholes value|) where the mean itself can be ~0."""
     for gr, orr in zip(gres, ores):
         g = gr.as_dict() if hasattr(gr, "as_dict") else gr
-        scale = np.sqrt(np.maximum(orr["within_var"], 0) + orr["mean"] ** 2)
+        scale = np.sqrt(np.maximum(orr["within_var"], 0) + orr["mean"] ** 2) + floor
         assert np.all(np.abs(g["mean"] - orr["mean"]) <= 1e-9 * scale), (g["mean"], orr["mean"])
         if orr["n_replicates"] > 1:
             assert np.all(np.abs(g["se"] - orr["se"]) <= 1e-6 * orr["se"] + 1e-12 * scale), (g["se"], orr["se"])
@@ -256,3 +261,53 @@ def test_bench_launch_config_sampled_replicates(q, O):
                 C_gpu = piv[qq] + s1[oi * 8 + qq * 2] / N
                 scale = math.sqrt(max(o[oi]["within_var"][qq], 0) + o[oi]["mean"][qq] ** 2)
                 assert abs(C_gpu - rm[rep, oi, qq]) <= 1e-9 * scale, (rep, oi, qq, C_gpu, rm[rep, oi, qq])
+
+
+# ------------------------------------------------------------------ C5 portfolio kernel
+def _c5_subset(q, d, picks):
+    opts = W.c5_portfolio()
+    sel = [opts[i] for i in picks]
+    return [o["type"] for o in sel], [q.params(S0=o["S0"], K=o["K"], r=o["r"], sigma=o["sigma"], T=o["T"], d=d)
+                                      for o in sel], sel
+
+
+@pytest.mark.parametrize("d", [16, 128])
+def test_portfolio_path_values(q, O, d):
+    # 8 (sigma, T) families x 3 option types, strikes across the C5 range
+    picks = [f * 128 + m for f in range(8) for m in (5, 64, 127)]
+    types, ps, sel = _c5_subset(q, d, picks)
+    cfg = qcfg(q, 2, 0)
+    g = q.qmccpw_portfolio_path_values(types, ps, 1, 13, 13 + 300, cfg)
+    for j, o in enumerate(sel):
+        mk = O.market(o["S0"], o["r"], o["sigma"], o["T"], d)
+        ref = O.path_values(o["type"], o["K"], mk, ocfg(O, 2, 0), 1, 13, 13 + 300)
+        piv = np.abs(O.pivots(o["type"], o["K"], mk)) + np.abs(O.pivots(o["type"], o["S0"], mk))
+        err = np.abs(g[:, j, :] - ref) / (np.abs(ref) + piv)
+        s2 = o["sigma"] ** 2 * o["T"] / d
+        tol = np.array([1e-12, 1e-12, 1e-12, 1e-12 * max(1.0, 0.03 / s2)])
+        assert np.all(err <= tol), (j, o, err.max(axis=0))
+
+
+def test_portfolio_means_full_option_count(q, O):
+    # all 1024 C5 options through one launch (ragged N, 2 replicates); a sample checked against the oracle
+    d, N, L = 128, 4096 + 333, 2
+    types, ps, sel = _c5_subset(q, d, list(range(1024)))
+    res = q.qmccpw_price_greeks_batch(types, ps, N, L, qcfg(q, 2, 0))
+    for i in list(range(0, 1024, 61)) + [1023]:
+        o = sel[i]
+        mk = O.market(o["S0"], o["r"], o["sigma"], o["T"], d)
+        ref, _ = O.price_greeks([(o["type"], o["K"])], mk, N, L, ocfg(O, 2, 0))
+        _means_check([res[i]], ref, floor=np.abs(O.pivots(o["type"], o["S0"], mk)))
+
+
+def test_portfolio_matches_fused_kernel_for_one_family(q):
+    # the sharing logic: a one-family portfolio equals the fused path kernel on the same points
+    ps = [q.params(K=K, d=64) for K in (95.0, 100.0, 105.0)]
+    a = q.qmccpw_price_greeks_batch([0, 1, 2], ps, 4096 * 2, 3, qcfg(q, 2, 0))
+    g = q.qmccpw_portfolio_path_values([0, 1, 2], ps, 0, 0, 4096 * 2, qcfg(q, 2, 0))
+    assert g.shape == (8192, 3, 4)
+    for o in range(3):
+        assert a[o].n_points == 8192
+    b = q.qmccpw_price_greeks_batch([0, 1, 2, 2], ps + [ps[2]], 4096 * 2, 3, qcfg(q, 2, 0))  # 4 options -> portfolio
+    for o in range(3):
+        assert np.allclose(np.array(a[o].mean[:]), np.array(b[o].mean[:]), rtol=1e-12, atol=1e-15)
