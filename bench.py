@@ -177,8 +177,10 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--construction", type=int, default=W.BB)
     ap.add_argument("--conditioning", type=int, default=W.W1)
-    ap.add_argument("--points", type=int, default=W.CONFIGS["C4"]["n_points"])
-    ap.add_argument("--reps-per-gpu", type=int, default=W.CONFIGS["C4"]["n_replicates"])
+    ap.add_argument("--workload", default="C4", choices=["C4", "C5"],
+                    help="C4: 3 exotics fused, d=64 (the BASELINE metric); C5: 1024-option portfolio, d=128")
+    ap.add_argument("--points", type=int, default=None)
+    ap.add_argument("--reps-per-gpu", type=int, default=None)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=None)
     args = ap.parse_args()
@@ -200,13 +202,21 @@ def main():
     if world > 1:
         dist.init_process_group("nccl", device_id=dev)
 
-    c = W.CONFIGS[W.HEADLINE]
-    options, d = c["options"], c["d"]
-    if args.conditioning == W.X1:
-        options = [W.ARITH, W.BINARY]
-    N = args.points
-    L = args.reps_per_gpu * world
-    plist = [q.params(S0=W.S0, K=100.0, r=W.R, sigma=W.SIGMA, T=W.T, d=d) for _ in options]
+    if args.workload == "C5":
+        port = W.c5_portfolio()
+        options, d = [o["type"] for o in port], 128
+        args.construction, args.conditioning = W.PCA, W.W1
+        N = args.points or (1 << 18)
+        L = (args.reps_per_gpu or 16) * world
+        plist = [q.params(S0=o["S0"], K=o["K"], r=o["r"], sigma=o["sigma"], T=o["T"], d=d) for o in port]
+    else:
+        c = W.CONFIGS[W.HEADLINE]
+        options, d = c["options"], c["d"]
+        if args.conditioning == W.X1:
+            options = [W.ARITH, W.BINARY]
+        N = args.points or c["n_points"]
+        L = (args.reps_per_gpu or c["n_replicates"]) * world
+        plist = [q.params(S0=W.S0, K=100.0, r=W.R, sigma=W.SIGMA, T=W.T, d=d) for _ in options]
     cfg = q.config(construction=args.construction, conditioning=args.conditioning, seed=W.SEED, device=local)
     pricer = DistributedPricer(options, plist, N, L, cfg, dev, rank, world)
 
@@ -282,29 +292,42 @@ def main():
     peaks = measured_peaks()
     sm_max = float(peaks.get("sm_max_mhz", SM_MAX_MHZ_FALLBACK))
     peak_tflops = SM_COUNT * FP64_LANES_PER_SM * 2 * sm_max * 1e6 / 1e12
-    per_path = fp64_model_per_path(d, args.construction, args.conditioning, len(options),
-                                   arith_x1=int(args.conditioning == W.X1))
+    if args.workload == "C5":
+        # phase A per point: d inverse normals, the d x d contraction, 8 families x d exps;
+        # phase B: the 1024 option tails (160 each, SURVEY 8(d) c_tail)
+        per_path = d * 50 + d * d + 8 * d * (17 + 6) + len(options) * 160
+    else:
+        per_path = fp64_model_per_path(d, args.construction, args.conditioning, len(options),
+                                       arith_x1=int(args.conditioning == W.X1))
     launch_paths = N * (L // world)
     achieved = 2.0 * per_path * launch_paths / (kernel_avg_ms / 1e3) / 1e12
     traffic = None
     tpath = os.path.join(ROOT, "profiles", "ncu_traffic.json")
-    if os.path.exists(tpath):
+    if os.path.exists(tpath) and args.workload == "C4" and (args.construction, args.conditioning) == (W.BB, W.W1):
         try:
             traffic = json.load(open(tpath)).get("bytes_per_launch")
         except Exception:
             traffic = None
 
+    metric, unit = METRIC, UNIT
+    if args.workload == "C5":
+        metric = "C5 portfolio option-paths/sec (1024 options, d=128) with price+delta+vega+gamma; % FP64 roof"
+        unit = "option-paths/s"
+        value *= len(options)
+        e2e_value *= len(options)
     if rank == 0:
         line = {
-            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "metric": metric, "value": value, "unit": unit, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (seeded Sobol'/Philox; no datasets or weights)",
             "config": {
-                "workload": "C4: arithmetic+binary+lookback Asian calls fused on shared paths, S0=K=100, sigma=0.2, "
-                            "r=0.1, T=1, d=64, " + {(1, 0): "BB-W1 (QMC+BB-CPW)", (0, 0): "STD-W1 (QMC-CPW)",
-                                                    (2, 0): "PCA-W1", (2, 1): "PCA-X1 (Newton)"}.get(
-                                (args.construction, args.conditioning), "custom"),
+                "workload": ("C5: 1024 options (8 sigma/T families x 128; K 70..130; arith/binary/lookback), S0=100, "
+                             "r=0.1, d=128, PCA-W1 (portfolio kernel)") if args.workload == "C5" else
+                            ("C4: arithmetic+binary+lookback Asian calls fused on shared paths, S0=K=100, sigma=0.2, "
+                             "r=0.1, T=1, d=64, " + {(1, 0): "BB-W1 (QMC+BB-CPW)", (0, 0): "STD-W1 (QMC-CPW)",
+                                                     (2, 0): "PCA-W1", (2, 1): "PCA-X1 (Newton)"}.get(
+                                 (args.construction, args.conditioning), "custom")),
                 "points_per_replicate": N, "replicates_per_gpu": L // world, "replicates_total": L,
                 "global_batch": N * L, "seq_len": d, "parallelism": f"dp{world} (replicate-partitioned)",
                 "option_paths_per_s": value * len(options), "greek_sets_per_s": value * len(options),
@@ -316,13 +339,13 @@ def main():
                          "note": f"FP64 pipe: {SM_COUNT} SMs x {FP64_LANES_PER_SM} FMA lanes x 2 x {sm_max:.0f} MHz; "
                                  f"algorithmic work {per_path} FP64 lane-instr/path (SURVEY 8(d) model)"},
             "clocks": clk.summary(),
-            "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": pricer.h2d_bytes,
+            "e2e": {"value": e2e_value, "unit": unit, "h2d_bytes_per_step": pricer.h2d_bytes,
                     "d2h_bytes_per_step": pricer.d2h_bytes},
             "gpu_launches": int(launches),
-            "results_sample": {"price": [r.mean[0] for r in results], "delta": [r.mean[1] for r in results],
-                               "vega": [r.mean[2] for r in results], "gamma": [r.mean[3] for r in results]},
+            "results_sample": {"price": [r.mean[0] for r in results[:3]], "delta": [r.mean[1] for r in results[:3]],
+                               "vega": [r.mean[2] for r in results[:3]], "gamma": [r.mean[3] for r in results[:3]]},
         }
-        if world == 1 and not args.no_cpu_baseline:
+        if world == 1 and not args.no_cpu_baseline and args.workload == "C4":
             line["cpu_baseline"] = cpu_baseline_oracle(options, d, args.construction, args.conditioning)
         print(json.dumps(line), flush=True)
     if world > 1:
