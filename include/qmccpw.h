@@ -60,8 +60,9 @@ typedef enum {
 
 typedef enum {
     QMCCPW_COND_W1 = 0, /* condition on W(t_1): the paper's variable separation */
-    QMCCPW_COND_X1 = 1  /* condition on the first coordinate x_1 of the path matrix;
-                           threshold by Newton's method (north star; arithmetic and binary only) */
+    QMCCPW_COND_X1 = 1  /* condition on the first coordinate x_1 of the path matrix (north star):
+                           arithmetic / binary threshold by Newton's method; lookback by the
+                           closed-form threshold and its upper envelope */
 } qmccpw_conditioning;
 
 typedef enum {
@@ -119,7 +120,7 @@ typedef struct {
  *   [1, 1024]; n_points = 0 or beyond the Sobol32 period; n_replicates = 0;
  *   NULL p or out.
  * EUNSUPPORTED: BB with d != 2^m (Alg. 4 is defined for 2^m steps);
- *   X1 with the lookback; LR_MC with a construction other than STD;
+ *   LR_MC with a construction other than STD;
  *   MC_CPW / MC_AV_CPW with PCA or X1;
  *   d > 256 on the GPU. */
 int qmccpw_price_greeks(int32_t option, const qmccpw_params* p, uint64_t n_points, uint32_t n_replicates,

@@ -539,9 +539,65 @@ static int estimate_x1(int type, const mkt_t* m, const double* M, const double* 
         out[3] = D * (d * K / sg) * phi(u) / (S0 * Dst) * (-u * up - 2.0 / S0 - sg * up * Qst / Dst);
     } else {
         free(a); free(R); free(c);
-        return set_err(-2, "X1 conditioning supports arithmetic and binary Asian options only");
+        return set_err(-2, "X1 conditioning: unsupported option type");
     }
     free(a); free(R); free(c);
+    return 0;
+}
+
+/* Lookback under X1.  With lines
+ * l_j(u) = c_j + b_j u, b_j = sigma a_j, max_j S(t_j) = exp(L(u)), L = max_j l_j:
+ * {L > ln K} = {u > u*}, u* = min_j (ln K - c_j)/b_j.  Line j is the maximum on
+ * [lo_j, hi_j]: lo_j = max over lines i of smaller slope of their crossing
+ * x_ij = (c_i - c_j)/(b_j - b_i), hi_j = min over lines of larger slope; an
+ * equal-slope line with a larger intercept (or the same one and a lower index)
+ * hides j.  Then, on [max(lo_j, u*), hi_j]:
+ *   G     = D [ sum_j w_j (Phibar(lo - b_j) - Phibar(hi - b_j)) - K Phibar(u*) ],
+ *           w_j = exp(c_j + b_j^2/2)
+ *   delta = (G + D K Phibar(u*)) / S0                      (all c_j shift by ln S0)
+ *   gamma = D K phi(u*) / (S0^2 b_{j0}),  j0 the line that crosses ln K at u*
+ *   vega  = D sum_j w_j [ (R_j - sigma t_j + sigma a_j^2)(Phibar(lo - b_j) - Phibar(hi - b_j))
+ *                         + a_j (phi(lo - b_j) - phi(hi - b_j)) ]
+ * (the envelope is continuous, so breakpoint motion contributes nothing). */
+static int estimate_x1_lookback(const mkt_t* m, const double* M, const double* x, double* out) {
+    int d = m->d;
+    double *b = malloc(sizeof(double) * d), *c = malloc(sizeof(double) * d), *R = malloc(sizeof(double) * d);
+    double lnK = log(m->K), u_star = INFINITY;
+    int j0 = 0;
+    for (int j = 0; j < d; j++) {
+        double tj = (double)(j + 1) * m->T / d, Rj = 0.0;
+        for (int k = 1; k < d; k++) Rj += M[j * d + k] * x[k];
+        R[j] = Rj;
+        c[j] = log(m->S0) + m->omega * tj + m->sigma * Rj;
+        b[j] = m->sigma * M[j * d + 0];
+        if (!(b[j] > 0.0)) { free(b); free(c); free(R); return set_err(-2, "X1 needs a_j > 0"); }
+        double uj = (lnK - c[j]) / b[j];
+        if (uj < u_star) { u_star = uj; j0 = j; }
+    }
+    double J = 0.0, V = 0.0;
+    for (int j = 0; j < d; j++) {
+        double lo = u_star, hi = INFINITY;
+        int hidden = 0;
+        for (int i = 0; i < d && !hidden; i++) {
+            if (i == j) continue;
+            if (b[i] < b[j]) lo = fmax(lo, (c[i] - c[j]) / (b[j] - b[i]));
+            else if (b[i] > b[j]) hi = fmin(hi, (c[i] - c[j]) / (b[j] - b[i]));
+            else if (c[i] > c[j] || (c[i] == c[j] && i < j)) hidden = 1;
+        }
+        if (hidden || !(lo < hi)) continue;
+        double tj = (double)(j + 1) * m->T / d, aj = b[j] / m->sigma;
+        double w = exp(c[j] + 0.5 * b[j] * b[j]);
+        double dP = Phibar(lo - b[j]) - (isinf(hi) ? 0.0 : Phibar(hi - b[j]));
+        double dphi = phi(lo - b[j]) - (isinf(hi) ? 0.0 : phi(hi - b[j]));
+        J += w * dP;
+        V += w * ((R[j] - m->sigma * tj + m->sigma * aj * aj) * dP + aj * dphi);
+    }
+    double D = m->D, K = m->K, S0 = m->S0;
+    out[0] = D * (J - K * Phibar(u_star));
+    out[1] = D * J / S0;
+    out[2] = D * V;
+    out[3] = D * K * phi(u_star) / (S0 * S0 * b[j0]);
+    free(b); free(c); free(R);
     return 0;
 }
 
@@ -591,7 +647,8 @@ static int estimate_impl(const or_option* opt, const or_market* mk, int method, 
         free(xm);
         return rc;
     }
-    if (conditioning == OR_COND_X1) return estimate_x1(opt->type, &m, M, x, out);
+    if (conditioning == OR_COND_X1)
+        return opt->type == OR_LOOKBACK ? estimate_x1_lookback(&m, M, x, out) : estimate_x1(opt->type, &m, M, x, out);
     double* W = malloc(sizeof(double) * mk->d);
     int rc = or_construct(construction, mk->d, mk->T, x, W);
     if (rc == 0) rc = estimate_w1(opt->type, &m, W, out, opt->type == OR_LOOKBACK ? near_tie : NULL);
@@ -610,8 +667,9 @@ static int validate(const or_option* opt, const or_market* mk, int method, int c
     if ((method == OR_MC_CPW || method == OR_MC_AV_CPW) && (construction == OR_PCA || conditioning != OR_COND_W1))
         return set_err(-2, "MC-CPW / MC+AV-CPW: STD or BB construction, W1 conditioning");
     if (method < 0 || method > 3) return set_err(-1, "unknown method");
-    if (method == OR_QMC_CPW && conditioning == OR_COND_X1 && opt->type != OR_ARITH && opt->type != OR_BINARY)
-        return set_err(-2, "X1 conditioning supports arithmetic and binary Asian options only");
+    if (method == OR_QMC_CPW && conditioning == OR_COND_X1 && opt->type != OR_ARITH && opt->type != OR_BINARY &&
+        opt->type != OR_LOOKBACK)
+        return set_err(-2, "X1 conditioning supports the three paper options only");
     return 0;
 }
 

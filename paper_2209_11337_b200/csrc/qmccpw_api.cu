@@ -246,10 +246,6 @@ int make_plan(const int32_t* options, const qmccpw_params* p, int32_t n_options,
     pl->cfg = resolve(cfg, p[0].d);
     int rc = validate_config(pl->cfg, p[0].d, n_points, n_reps);
     if (rc) return rc;
-    for (int o = 0; o < n_options; ++o)
-        if (pl->cfg.method == QMCCPW_QMC_CPW && pl->cfg.conditioning == QMCCPW_COND_X1 &&
-            options[o] == QMCCPW_LOOKBACK_CALL)
-            return fail(QMCCPW_EUNSUPPORTED, "X1 conditioning supports arithmetic and binary Asian calls only");
     pl->portfolio = !(same_market && n_options <= kMaxOpt);
     pl->n_fam = 0;
     for (int o = 0; o < n_options; ++o) {

@@ -441,6 +441,77 @@ __device__ __forceinline__ void x1_outputs(const PathArgs& P, int o, const X1Sum
     }
 }
 
+// Lookback under X1 (next-row f1).  Lines l_j(u) = c_j + b_j u,
+// b_j = sigma a_j; u* = min_j (ln K - c_j)/b_j in closed form; G integrates
+// exp(max_j l_j(u)) phi(u) over [u*, inf), walking the upper envelope from u*:
+// on each segment the next breakpoint is the first steeper line to overtake.
+__device__ __forceinline__ void x1_lookback(const PathArgs& P, int o, const double* cb, int stride, double f[4]) {
+    const int d = P.d;
+    const double sg = P.sigma, lnK = P.lnK[o];
+    double ustar = CUDART_INF;
+    int j0 = 0;
+    for (int j = 0; j < d; ++j) {
+        const double uj = (lnK - cb[j * stride]) * P.inv_sa[j];
+        if (uj < ustar) {
+            ustar = uj;
+            j0 = j;
+        }
+    }
+    // active line at u*: the maximum there; on ties the steeper one (it dominates just after)
+    int act = 0;
+    double best = -CUDART_INF, bact = 0.0;
+    for (int j = 0; j < d; ++j) {
+        const double bj = sg * __ldg(P.a + j);
+        const double v = fma(bj, ustar, cb[j * stride]);
+        if (v > best || (v == best && bj > bact)) {
+            best = v;
+            act = j;
+            bact = bj;
+        }
+    }
+    double J = 0.0, V = 0.0, lo = ustar;
+    for (int seg = 0; seg < d; ++seg) {
+        const double cact = cb[act * stride];
+        double hi = CUDART_INF, bn = 0.0;
+        int nxt = -1;
+        for (int i = 0; i < d; ++i) {
+            const double bi = sg * __ldg(P.a + i);
+            if (bi > bact) {
+                const double x = (cact - cb[i * stride]) / (bi - bact);
+                if (x < hi || (x == hi && bi > bn)) {
+                    hi = x;
+                    nxt = i;
+                    bn = bi;
+                }
+            }
+        }
+        hi = fmax(hi, lo);
+        const double aa = bact / sg;
+        const double tj = (double)(act + 1) * P.t1;
+        const double Rj = (cact - P.lnS0 - P.omega * tj) * P.inv_sigma;
+        const double w = fast_exp(fma(0.5 * bact, bact, cact));
+        double Qlo, Qhi, plo, phi_hi;
+        phibar_phi_x2(lo - bact, (nxt < 0) ? 0.0 : hi - bact, Qlo, Qhi, plo, phi_hi);
+        if (nxt < 0) {
+            Qhi = 0.0;
+            phi_hi = 0.0;
+        }
+        J = fma(w, Qlo - Qhi, J);
+        V = fma(w, (Rj - sg * tj + sg * aa * aa) * (Qlo - Qhi) + aa * (plo - phi_hi), V);
+        if (nxt < 0) break;
+        lo = hi;
+        act = nxt;
+        bact = bn;
+    }
+    const double D = P.Dfac, S0 = P.S0, K = P.K[o];
+    double Qu, Q2, ph, ph2;
+    phibar_phi_x2(ustar, ustar, Qu, Q2, ph, ph2);
+    f[0] = D * (J - K * Qu);
+    f[1] = D * J / S0;
+    f[2] = D * V;
+    f[3] = D * K * ph / (S0 * S0 * sg * __ldg(P.a + j0));
+}
+
 // all options of the launch: one Newton solve (and one set of E*-sums) per distinct strike
 __device__ __forceinline__ void tail_x1_all(const PathArgs& P, const double* cb, int stride, double f[kMaxOpt][4],
                                             unsigned& unconverged) {
@@ -448,6 +519,11 @@ __device__ __forceinline__ void tail_x1_all(const PathArgs& P, const double* cb,
 #pragma unroll
     for (int o = 0; o < kMaxOpt; ++o) {
         if (o >= P.n_opt) break;
+        if (P.type[o] == kLookback) {
+            x1_lookback(P, o, cb, stride, f[o]);
+            xs[o] = X1Sums{0, 0, 0, 0, 0, 0};
+            continue;
+        }
         const int ld = P.tail_leader[o];
         if (ld == o) {
             xs[o] = x1_solve(P, o, P.x1_need_arith[o] != 0, cb, stride, unconverged);
@@ -1698,7 +1774,8 @@ cudaError_t launch_paths(const PathArgs& args, int construction, int conditionin
                                                   : launch_paths_t<kStd, kW1, kMc>(args, st, smem_out);
     if (method == kMcAv) return construction == kBB ? launch_paths_t<kBB, kW1, kMcAv>(args, st, smem_out)
                                                     : launch_paths_t<kStd, kW1, kMcAv>(args, st, smem_out);
-    if (construction == kPca && method == kQmc) {  // fragment-native tensor-core path for d <= 128
+    if (construction == kPca && method == kQmc && !(conditioning == kX1 && args.has_lookback)) {
+        // fragment-native tensor-core path for d <= 128 (the X1 lookback walks its envelope per thread)
         bool handled = false;
         cudaError_t e = conditioning == kW1 ? launch_pca<kW1>(args, st, &handled) : launch_pca<kX1>(args, st, &handled);
         if (handled) return e;

@@ -102,8 +102,6 @@ def _pv_check(q, O, otype, K, d, constr, cond, method, rep, k0, k1, S0=W.S0, sig
 @pytest.mark.parametrize("otype", [0, 1, 2])
 @pytest.mark.parametrize("d", [1, 4, 16, 64])
 def test_path_values(q, O, constr, cond, otype, d):
-    if cond == 1 and otype == 2:
-        pytest.skip("X1 lookback is out of scope (EUNSUPPORTED)")
     for K in W.STRIKES:
         _pv_check(q, O, otype, K, d, constr, cond, 0, 3, 1000, 1000 + 700)
     _pv_check(q, O, otype, 100.0, d, constr, cond, 0, 0, 0, 300)
@@ -138,7 +136,7 @@ def test_mc_methods_full_runs(q, O):
 def test_path_values_pca_tile_edges(q, O, cond, d):
     # the tensor-core PCA kernel (d <= 128 in 8-wide tiles) and its fallback (other d);
     # ragged point ranges so some lanes of the last warp carry no point
-    for otype in ((0, 1) if cond else (0, 1, 2)):
+    for otype in (0, 1, 2):
         _pv_check(q, O, otype, 100.0, d, 2, cond, 0, 1, 17, 17 + 301)
 
 
@@ -196,9 +194,9 @@ def test_c4_fused_three_options_and_lr(q, O):
         g = q.qmccpw_price_greeks_batch(opts, [q.params(d=64)] * 3, N, L, qcfg(q, constr, 0, method))
         o, _ = O.price_greeks([(t, 100.0) for t in opts], O.market(d=64), N, L, ocfg(O, constr, 0, method))
         _means_check(g, o)
-    # X1 on the PCA construction for the two Asians (the north star's Newton path)
-    g = q.qmccpw_price_greeks_batch([0, 1], [q.params(K=95.0, d=64)] * 2, N, L, qcfg(q, 2, 1))
-    o, _ = O.price_greeks([(0, 95.0), (1, 95.0)], O.market(d=64), N, L, ocfg(O, 2, 1))
+    # X1 on the PCA construction (the north star's Newton path) incl. the lookback's envelope (row f1)
+    g = q.qmccpw_price_greeks_batch([0, 1, 2], [q.params(K=95.0, d=64)] * 3, N, L, qcfg(q, 2, 1))
+    o, _ = O.price_greeks([(0, 95.0), (1, 95.0), (2, 95.0)], O.market(d=64), N, L, ocfg(O, 2, 1))
     _means_check(g, o)
 
 

@@ -63,13 +63,14 @@ def raw_payoff(otype, K, S):
     return D * max(S.max() - K, 0.0)
 
 
-def conditional_quadrature(otype, K, S_of):
-    """E[raw payoff | everything but xi] = int raw(S(xi)) phi(xi) dxi, threshold as a breakpoint."""
+def conditional_quadrature(otype, K, S_of, kinks=()):
+    """E[raw payoff | everything but xi] = int raw(S(xi)) phi(xi) dxi, with the threshold and the
+    kinks of the payoff (crossings of the dates' log-price lines, lookback under X1) as breakpoints."""
     stat = (lambda S: S.max()) if otype == 2 else (lambda S: S.mean())
     thr = optimize.brentq(lambda u: stat(S_of(u)) - K, -60, 60, xtol=1e-15, rtol=1e-15)
     f = lambda u: raw_payoff(otype, K, S_of(u)) * phi(u)
-    val, err = integrate.quad(f, thr, thr + 40, epsabs=1e-15, epsrel=1e-13, limit=400)
-    return val
+    pts = [thr] + sorted(k for k in kinks if thr < k < thr + 40) + [thr + 40]
+    return sum(integrate.quad(f, a, b, epsabs=1e-15, epsrel=1e-13, limit=400)[0] for a, b in zip(pts[:-1], pts[1:]))
 
 
 def paths_w1(O, constr, d, x, S0=S0, sg=SIG):
@@ -90,9 +91,17 @@ def paths_x1(O, constr, d, x, S0=S0, sg=SIG):
     return lambda u: S0 * np.exp(om * t + sg * (Rj + M[:, 0] * u))
 
 
+def x1_kinks(O, constr, d, x, sg=SIG):
+    M = O.path_matrix(constr, d, T)
+    t = np.arange(1, d + 1) * T / d
+    c = (R - 0.5 * sg * sg) * t + sg * (M[:, 1:] @ x[1:])
+    b = sg * M[:, 0]
+    return [(c[i] - c[j]) / (b[j] - b[i]) for i in range(d) for j in range(i + 1, d) if b[i] != b[j]]
+
+
 @pytest.mark.parametrize("otype,constr,cond", [(0, 0, 0), (1, 0, 0), (2, 0, 0), (0, 1, 0), (1, 1, 0), (2, 1, 0),
                                                (0, 2, 0), (1, 2, 0), (2, 2, 0), (0, 2, 1), (1, 2, 1), (0, 1, 1),
-                                               (1, 1, 1)])
+                                               (1, 1, 1), (2, 2, 1), (2, 1, 1), (2, 0, 1)])
 def test_smoothed_payoff_equals_quadrature_of_raw_payoff(O, otype, constr, cond):
     rng = np.random.default_rng(100 + 10 * otype + constr)
     for d in (4, 16):
@@ -101,7 +110,8 @@ def test_smoothed_payoff_equals_quadrature_of_raw_payoff(O, otype, constr, cond)
             x = rng.standard_normal(d)
             for K in (90.0, 100.0, 110.0):
                 S_of = paths_x1(O, constr, d, x) if cond else paths_w1(O, constr, d, x)
-                ref = conditional_quadrature(otype, K, S_of)
+                kinks = x1_kinks(O, constr, d, x) if (cond and otype == 2) else ()
+                ref = conditional_quadrature(otype, K, S_of, kinks)
                 got = O.estimate(otype, K, mk, x, construction=constr, conditioning=cond)[0]
                 assert abs(got - ref) <= 1e-12 * max(1.0, abs(ref)), (d, K, got, ref)
 
@@ -114,7 +124,7 @@ def richardson(f, x0, h):
 
 @pytest.mark.parametrize("otype,constr,cond", [(0, 0, 0), (1, 0, 0), (2, 0, 0), (0, 1, 0), (1, 1, 0), (2, 1, 0),
                                                (0, 2, 0), (1, 2, 0), (2, 2, 0), (0, 2, 1), (1, 2, 1), (0, 1, 1),
-                                               (1, 1, 1)])
+                                               (1, 1, 1), (2, 2, 1), (2, 1, 1)])
 def test_greeks_equal_finite_differences_of_G(O, otype, constr, cond):
     rng = np.random.default_rng(7 + 10 * otype + constr + 100 * cond)
     tol = 5e-8 if cond else 1e-8
@@ -144,7 +154,7 @@ def test_std_x1_equals_w1(O):
         mk = O.market(S0, R, SIG, T, d)
         for _ in range(10):
             x = rng.standard_normal(d)
-            for otype in (0, 1):
+            for otype in (0, 1, 2):
                 for K in (90.0, 110.0):
                     a = O.estimate(otype, K, mk, x, construction=0, conditioning=0)
                     b = O.estimate(otype, K, mk, x, construction=0, conditioning=1)

@@ -57,7 +57,8 @@ def test_all_modes_estimate_the_same_greeks(O):
     runs = {}
     for constr in (0, 1, 2):
         runs[(constr, 0)] = O.price_greeks(opts, mk, N, L, O.config(construction=constr))[0]
-    runs[(2, 1)] = O.price_greeks(opts[:2], mk, N, L, O.config(construction=2, conditioning=1))[0]
+    runs[(2, 1)] = O.price_greeks(opts, mk, N, L, O.config(construction=2, conditioning=1))[0]
+    runs[(1, 1)] = O.price_greeks(opts, mk, N, L, O.config(construction=1, conditioning=1))[0]
     for key, res in runs.items():
         for o in range(len(res)):
             _agree(res[o], lr[o])
