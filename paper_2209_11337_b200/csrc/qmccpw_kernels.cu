@@ -786,11 +786,12 @@ __global__ void __launch_bounds__(128) paths_kernel(const PathArgs P) {
                     w1.push(P, j, Wt);
                 }
             } else if (CONSTR == kBB) {
-                // Alg. 4 generated in time order.  Before emitting W(t_j) the
-                // bridge descends e = ctz(j-1) levels (e = m at j = 1) from the interval
-                // (t_{j-1}, t_{j-1+2^e}]; midpoint mid = j-1+2^c (c = e-1..0) sits at level
-                // m-c and consumes the next Sobol' dimension of Alg. 4's order (bb_seq, built
-                // on the host); W(mid) = (W(l) + W(r))/2 + b_{m-c} x.
+                // Alg. 4 generated in time order, two dates per step.  At odd
+                // j = 2p+1 the bridge descends e = 1 + ctz(p) levels (e = m at p = 0) from the
+                // interval (t_{j-1}, t_{j-1+2^e}]: midpoint mid = j-1+2^c (c = e-1..0) sits at
+                // level m-c, consumes the next Sobol' dimension of Alg. 4's order (bb_seq, built
+                // on the host), W(mid) = (W(l) + W(r))/2 + b_{m-c} x, and is pushed for c > 0.
+                // W(t_j) is the c = 0 midpoint; W(t_{j+1}) is then exactly the stack top.
                 NormalFifo fifo;
                 fifo.reset();
                 int pos = 0;
@@ -799,16 +800,14 @@ __global__ void __launch_bounds__(128) paths_kernel(const PathArgs P) {
                 int sp = 0;
                 stW[0] = P.sqrtT * fifo.next(sob, dim_at);
                 pos += 2;
-                double Wl = 0.0, W1 = 0.0, Wpend = 0.0;
                 const int m = P.bb_m;
+                if (d == 1) {
+                    w1.push(P, 0, 0.0);
+                } else {
+                    double Wl = 0.0, W1 = 0.0;
 #pragma unroll 1
-                for (int j = 1; j <= d; ++j) {
-                    const int e = (j == 1) ? m : (__ffs(j - 1) - 1);
-                    double Wj;
-                    if (e == 0) {
-                        Wj = stW[sp];
-                        --sp;
-                    } else {
+                    for (int pp = 0; pp < (d >> 1); ++pp) {
+                        const int e = (pp == 0) ? m : __ffs(pp);  // 1 + ctz(pp)
                         double Wr = stW[sp];
 #pragma unroll 1
                         for (int c = e - 1; c >= 0; --c) {
@@ -819,17 +818,13 @@ __global__ void __launch_bounds__(128) paths_kernel(const PathArgs P) {
                             if (c > 0) stW[++sp] = Wm;
                             Wr = Wm;
                         }
-                        Wj = Wr;
+                        const double Wodd = Wr, Weven = stW[sp];
+                        --sp;
+                        if (pp == 0) W1 = Wodd;
+                        w1.push2(P, 2 * pp, Wodd - W1, Weven - W1);
+                        Wl = Weven;
                     }
-                    if (j == 1) W1 = Wj;
-                    if (j & 1) {
-                        Wpend = Wj - W1;
-                    } else {
-                        w1.push2(P, j - 2, Wpend, Wj - W1);
-                    }
-                    Wl = Wj;
                 }
-                if (d & 1) w1.push(P, d - 1, Wpend);
             } else {
                 // PCA: W = X M^T, the one dense contraction, on the FP64 tensor
                 // cores.  Each thread writes its path's normals as a column of X (shared
