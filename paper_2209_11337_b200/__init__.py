@@ -12,7 +12,7 @@ import os
 import numpy as np
 
 _PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_PKG, "libqmccpw.so")
+LIB_PATH = os.environ.get("QMCCPW_LIB") or os.path.join(_PKG, "libqmccpw.so")  # QMCCPW_LIB: A/B variants
 
 OK, EINVAL, EUNSUPPORTED, ECUDA, ENOMEM = 0, -1, -2, -3, -4
 ARITH_ASIAN_CALL, BINARY_ASIAN_CALL, LOOKBACK_CALL = 0, 1, 2

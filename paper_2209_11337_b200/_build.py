@@ -21,18 +21,20 @@ def stale():
     return any(os.path.getmtime(f) > t for f in SOURCES + HEADERS)
 
 
-def build(force=False, verbose=False):
-    if not force and not stale():
+def build(force=False, verbose=False, defines=(), out=None):
+    """defines/out: build an experimental variant (e.g. -DQMCCPW_ACC_SMEM=1) to another
+    file, selected at load time with QMCCPW_LIB=<path> (A/B timing in one GPU session)."""
+    if out is None and not force and not stale():
         return LIB
-    cmd = [NVCC] + FLAGS + ["-o", LIB] + SOURCES + ["-lcurand"]
+    cmd = [NVCC] + FLAGS + [f"-D{d}" for d in defines] + ["-o", out or LIB] + SOURCES + ["-lcurand"]
     res = subprocess.run(cmd, capture_output=True, text=True)
     if res.returncode != 0:
         raise RuntimeError("nvcc failed:\n" + res.stdout + res.stderr)
-    with open(os.path.join(PKG, "ptxas_info.txt"), "w") as f:
+    with open(os.path.join(PKG, "ptxas_info.txt" if out is None else os.path.basename(out) + ".ptxas.txt"), "w") as f:
         f.write(res.stderr)
     if verbose:
         print(res.stderr)
-    return LIB
+    return out or LIB
 
 
 if __name__ == "__main__":

@@ -579,19 +579,88 @@ __device__ __forceinline__ void lr_path(const PathArgs& P, uint32_t rep, uint64_
 // ---------------------------------------------------------------------------
 // The fused path kernel: one block = one cell (replicate, 4096 points).
 // ---------------------------------------------------------------------------
+// (a8) per-iteration warp reduction of the centred sums of option o (8 slots: S1, S2
+// per Greek, slot 2q + {0,1}, the partials layout): a reduce-scatter that halves
+// the slot set at xor 16, 8, 4 (each lane sends the half it drops), then a butterfly
+// over xor 2, 1; lanes 4s..4s+3 end with the warp total of slot s = lane >> 2, and
+// lane 4s adds it to the warp's running sums wacc[o*8 + s] in shared memory (no
+// per-thread accumulators, nothing live in registers across paths).
+__device__ __forceinline__ void warp_slot_sums(const double (&f)[kMaxOpt][4], const PathArgs& P, bool valid,
+                                               int lane, double* wacc) {
+#pragma unroll
+    for (int o = 0; o < kMaxOpt; ++o) {
+        if (o >= P.n_opt) break;  // warp-uniform
+        double v[8];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            const double y = valid ? f[o][q] - P.piv[o][q] : 0.0;
+            v[2 * q] = y;
+            v[2 * q + 1] = y * y;
+        }
+#pragma unroll
+        for (int half = 4; half > 0; half >>= 1) {
+            const bool up = (lane & (half * 4)) != 0;
+#pragma unroll
+            for (int j = 0; j < half; ++j) {
+                const double send = up ? v[j] : v[j + half];
+                const double keep = up ? v[j + half] : v[j];
+                v[j] = keep + __shfl_xor_sync(0xffffffffu, send, half * 4);
+            }
+        }
+        v[0] += __shfl_xor_sync(0xffffffffu, v[0], 2);
+        v[0] += __shfl_xor_sync(0xffffffffu, v[0], 1);
+        if ((lane & 3) == 0) wacc[o * 8 + (lane >> 2)] += v[0];
+    }
+}
+
+// per-thread (S1, S2) double2 accumulators in smem: cheaper in issue slots than the warp
+// reduction, so kernels with smem to spare (pca_kernel, register-limited) use it; the
+// path kernel, at its smem limit, uses warp_slot_sums (measured: BB-W1 -8%, PCA-W1 +4%)
+__device__ __forceinline__ void thread_acc2(const double (&f)[kMaxOpt][4], const PathArgs& P, bool valid,
+                                            double2* acc2, int tpb, int tid) {
+    if (!valid) return;
+#pragma unroll
+    for (int o = 0; o < kMaxOpt; ++o) {
+        if (o >= P.n_opt) break;
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            const double y = f[o][q] - P.piv[o][q];
+            double2* a = acc2 + (size_t)(o * 4 + q) * tpb + tid;
+            double2 t = *a;
+            t.x += y;
+            t.y = fma(y, y, t.y);
+            *a = t;
+        }
+    }
+}
+__device__ __forceinline__ void acc2_to_wacc(const PathArgs& P, const double2* acc2, double* wacc, int tpb, int tid) {
+    const int lane = tid & 31;
+    for (int v = 0; v < P.n_opt * 8; ++v) {
+        const double2 t = acc2[(size_t)(v >> 1) * tpb + tid];
+        double s1 = (v & 1) ? t.y : t.x;
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) s1 += __shfl_xor_sync(0xffffffffu, s1, off);
+        if (lane == 0) wacc[(tid >> 5) * 32 + v] = s1;
+    }
+}
+
 // (a8) fixed-shape reduction of a block's accumulators into its cell's partials:
 // warp butterfly, then the warps in order (deterministic for a given block size).
-__device__ __forceinline__ void block_epilogue(const PathArgs& P, const double* accs, double* red, int n_acc, int tpb,
-                                               int tid, uint64_t cell, unsigned unconverged, unsigned ties,
-                                               unsigned npts) {
+__device__ __forceinline__ void block_epilogue(const PathArgs& P, const double* accs, const double* wacc, double* red,
+                                               int n_acc, int tpb, int tid, uint64_t cell, unsigned unconverged,
+                                               unsigned ties, unsigned npts) {
     const int lane = tid & 31, warp = tid >> 5, nwarps = tpb >> 5;
     const int n_out = P.partial_stride;
     __syncthreads();  // red aliases the Sobol' tables
-    for (int v = 0; v < n_acc; ++v) {
-        double s1 = accs[v * tpb + tid];
+    if (accs == nullptr) {  // per-warp sums (warp_slot_sums)
+        if (lane < n_acc) red[warp * 32 + lane] = wacc[warp * 32 + lane];
+    } else {
+        for (int v = 0; v < n_acc; ++v) {
+            double s1 = accs[v * tpb + tid];
 #pragma unroll
-        for (int off = 16; off > 0; off >>= 1) s1 += __shfl_xor_sync(0xffffffffu, s1, off);
-        if (lane == 0) red[warp * 32 + v] = s1;
+            for (int off = 16; off > 0; off >>= 1) s1 += __shfl_xor_sync(0xffffffffu, s1, off);
+            if (lane == 0) red[warp * 32 + v] = s1;
+        }
     }
     unsigned uc = unconverged, tc = ties, nc = npts;
 #pragma unroll
@@ -613,8 +682,22 @@ __device__ __forceinline__ void block_epilogue(const PathArgs& P, const double* 
     }
 }
 
+#ifndef QMCCPW_BB_MINB
+#define QMCCPW_BB_MINB 8
+#endif
+#ifndef QMCCPW_STD_MINB
+#define QMCCPW_STD_MINB 6
+#endif
+// resident blocks per SM the register allocator must allow (128 threads each); 0 = ptxas'
+// own choice.  Measured on C4 (ms/step): BB-W1 34.3 (ptxas, 96 regs) / 33.8 (7) / 33.4
+// (8: 64 regs, a few spills to L1); STD-W1 33.1 (4) / 31.9 (5) / 31.2 (6)
 template <int CONSTR, int COND, int METHOD>
-__global__ void __launch_bounds__(128) paths_kernel(const PathArgs P) {
+constexpr int paths_min_blocks() {
+    return (COND == kW1 && METHOD == kQmc) ? (CONSTR == kBB ? QMCCPW_BB_MINB : CONSTR == kStd ? QMCCPW_STD_MINB : 0) : 0;
+}
+template <int CONSTR, int COND, int METHOD>
+__global__ void __launch_bounds__(128, paths_min_blocks<CONSTR, COND, METHOD>())
+    paths_kernel(const PathArgs P) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const int tpb_log2 = P.tpb_log2;
     const int tpb = 1 << tpb_log2;
@@ -630,12 +713,13 @@ __global__ void __launch_bounds__(128) paths_kernel(const PathArgs P) {
     constexpr bool kWarpMma = (METHOD == kQmc) && (CONSTR == kPca && COND == kW1);
 
     // shared memory carve-up (8-byte aligned first):
-    //   acc [n_opt*8][tpb] | buf0, buf1 [d][tpb] | vt [d][32] | sh [d] | G [d][32] | pad | HW [2][2][nw][d] (>= 1 KB)
-    // the reduction scratch red [4 warps][32] aliases HW after the point loop.
+    //   buf0, buf1 [d][tpb] | vt [d][32] | sh [d] | G [d][32] | pad | HW [2][2][nw][d] (>= 1 KB)
+    // the reduction scratch red [4 warps][32] aliases HW after the point loop; the
+    // centred sums live in one register per lane (warp_slot_sums).
     const int nw = tpb >> 5;
     const int n_acc = P.n_opt * 8;
-    double* accs = reinterpret_cast<double*>(smem_raw);
-    double* buf0 = accs + (size_t)n_acc * tpb;
+    const int lane = tid & 31;
+    double* buf0 = reinterpret_cast<double*>(smem_raw);
     double* buf1 = buf0 + (kWarpMma ? (size_t)P.M_ld * (tpb + 8) : (kNeedBuf ? (size_t)d * tpb : 0));
     uint32_t* vt = reinterpret_cast<uint32_t*>(buf1 + (kTwoBuf ? (size_t)d * tpb : 0));
     uint32_t* sh = vt + (METHOD == kQmc ? (size_t)d * 32 : 0);
@@ -656,7 +740,9 @@ __global__ void __launch_bounds__(128) paths_kernel(const PathArgs P) {
         __syncthreads();
         sobol_build_g(vt, d, G, tid, tpb);
     }
-    for (int v = 0; v < n_acc; ++v) accs[v * tpb + tid] = 0.0;
+    __shared__ double wacc[4 * 32];  // per-warp centred sums (tpb <= 128)
+    wacc[tid] = 0.0;
+    __syncwarp();
     if (kWarpMma)  // zero X rows d..dp-1 (the padded K of the mma tiles)
         for (int r = d; r < P.M_ld; ++r) buf0[(size_t)r * (tpb + 8) + tid] = 0.0;
     unsigned unconverged = 0, ties = 0, npts = 0;
@@ -670,8 +756,11 @@ __global__ void __launch_bounds__(128) paths_kernel(const PathArgs P) {
             sob.HW = HWb;
         }
         const uint64_t i = i0 + tid + ((uint64_t)a << tpb_log2);
+        // every lane runs (the warp reduction and the mma.sync tiles need the whole warp);
+        // lanes past N in a ragged last iteration evaluate a real lattice point whose
+        // result and counters are dropped
         const bool valid = i < P.n_points;
-        if (!valid && !kWarpMma) continue;  // the mma.sync path needs every lane of the warp
+        const unsigned unconverged0 = unconverged, ties0 = ties;
         npts += valid ? 1u : 0u;
         const uint64_t k = P.point_offset + i;
         double f[kMaxOpt][4];
@@ -950,7 +1039,6 @@ __global__ void __launch_bounds__(128) paths_kernel(const PathArgs P) {
                     }
                 }
             }
-            if (!valid) continue;
             if (P.has_lookback && w1.emax - w1.esec < 1e-12) ++ties;
             tail_w1_all(P, w1, f);
         } else {
@@ -1044,28 +1132,21 @@ __global__ void __launch_bounds__(128) paths_kernel(const PathArgs P) {
             tail_x1_all(P, cb, tpb, f, unconverged);
         }
 
-        if (P.path_out != nullptr) {
+        if (!valid) {
+            unconverged = unconverged0;
+            ties = ties0;
+        }
+        if (P.path_out != nullptr && valid) {
 #pragma unroll
             for (int o = 0; o < kMaxOpt; ++o)
                 if (o == P.hook_option)
                     for (int q = 0; q < 4; ++q) P.path_out[i * 4 + q] = f[o][q];
         }
-#pragma unroll
-        for (int o = 0; o < kMaxOpt; ++o) {
-            if (o < P.n_opt) {
-#pragma unroll
-                for (int q = 0; q < 4; ++q) {
-                    const double y = f[o][q] - P.piv[o][q];
-                    double* a1 = accs + (size_t)(o * 8 + q * 2) * tpb + tid;
-                    a1[0] += y;
-                    a1[tpb] = fma(y, y, a1[tpb]);
-                }
-            }
-        }
+        warp_slot_sums(f, P, valid, lane, wacc + (tid >> 5) * 32);
         (void)k;
     }
 
-    block_epilogue(P, accs, red, n_acc, tpb, tid, cell, unconverged, ties, npts);
+    block_epilogue(P, nullptr, wacc, red, n_acc, tpb, tid, cell, unconverged, ties, npts);
 }
 
 
@@ -1093,8 +1174,20 @@ __device__ __forceinline__ double quad_min(double v) {
     return fmin(v, __shfl_xor_sync(0xffffffffu, v, 2));
 }
 
+#ifndef QMCCPW_PCA_W1_MINB
+#define QMCCPW_PCA_W1_MINB 4
+#endif
+#ifndef QMCCPW_PCA_X1_MINB
+#define QMCCPW_PCA_X1_MINB 5
+#endif
+// d <= 64: shared memory allows 5 blocks/SM, so cap registers to match (measured on C4:
+// PCA-W1 72.4 -> 69.4 ms, PCA-X1 175 -> 165 ms); larger d is smem-limited anyway
 template <int COND, int KF>
-__global__ void __launch_bounds__(128) pca_kernel(const PathArgs P) {
+constexpr int pca_min_blocks() {
+    return KF > 16 ? 0 : (COND == kW1 ? QMCCPW_PCA_W1_MINB : QMCCPW_PCA_X1_MINB);
+}
+template <int COND, int KF>
+__global__ void __launch_bounds__(128, pca_min_blocks<COND, KF>()) pca_kernel(const PathArgs P) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     constexpr int DP = 4 * KF;  // padded dimension (multiple of 8)
     constexpr int JT = DP / 8;  // column tiles of 8 dates
@@ -1107,7 +1200,9 @@ __global__ void __launch_bounds__(128) pca_kernel(const PathArgs P) {
     const int ppt = kCellPoints >> tpb_log2;
     const int nw = tpb >> 5;
     const int n_acc = P.n_opt * 8;
+    // per-path accumulators in smem: X1 as scalars (one quad lane per path), W1 as (S1, S2) pairs
     double* accs = reinterpret_cast<double*>(smem_raw);
+    double2* acc2 = reinterpret_cast<double2*>(smem_raw);
     uint32_t* vt = reinterpret_cast<uint32_t*>(accs + (size_t)n_acc * tpb);
     uint32_t* sh = vt + (size_t)d * 32;
     uint32_t* G = sh + d;
@@ -1125,6 +1220,9 @@ __global__ void __launch_bounds__(128) pca_kernel(const PathArgs P) {
         sobol_build_g(vt, d, G, tid, tpb);
     }
     for (int v = 0; v < n_acc; ++v) accs[v * tpb + tid] = 0.0;
+    __shared__ double wacc[4 * 32];  // per-warp centred sums (tpb <= 128)
+    wacc[tid] = 0.0;
+    __syncwarp();
     unsigned unconverged = 0, ties = 0, npts = 0;
     const double sg = P.sigma;
 
@@ -1349,33 +1447,22 @@ __global__ void __launch_bounds__(128) pca_kernel(const PathArgs P) {
         if (COND == kW1) {
             const W1Acc& w1 = w1own;
             const uint64_t i = i0 + tid + ((uint64_t)a << tpb_log2);
-            if (i < P.n_points) {
-                ++npts;
-                if (P.has_lookback && w1.emax - w1.esec < 1e-12) ++ties;
-                double f[kMaxOpt][4];
-                tail_w1_all(P, w1, f);
-                if (P.path_out != nullptr) {
+            const bool valid = i < P.n_points;  // all lanes run: the warp reduction needs them
+            npts += valid ? 1u : 0u;
+            if (valid && P.has_lookback && w1.emax - w1.esec < 1e-12) ++ties;
+            double f[kMaxOpt][4];
+            tail_w1_all(P, w1, f);
+            if (P.path_out != nullptr && valid) {
 #pragma unroll
-                    for (int o = 0; o < kMaxOpt; ++o)
-                        if (o == P.hook_option)
-                            for (int qq = 0; qq < 4; ++qq) P.path_out[i * 4 + qq] = f[o][qq];
-                }
-#pragma unroll
-                for (int o = 0; o < kMaxOpt; ++o) {
-                    if (o < P.n_opt) {
-#pragma unroll
-                        for (int qq = 0; qq < 4; ++qq) {
-                            const double y = f[o][qq] - P.piv[o][qq];
-                            double* a1 = accs + (size_t)(o * 8 + qq * 2) * tpb + tid;
-                            a1[0] += y;
-                            a1[tpb] = fma(y, y, a1[tpb]);
-                        }
-                    }
-                }
+                for (int o = 0; o < kMaxOpt; ++o)
+                    if (o == P.hook_option)
+                        for (int qq = 0; qq < 4; ++qq) P.path_out[i * 4 + qq] = f[o][qq];
             }
+            thread_acc2(f, P, valid, acc2, tpb, tid);
         }
     }
-    block_epilogue(P, accs, red, n_acc, tpb, tid, cell, unconverged, ties, npts);
+    if (COND == kW1) acc2_to_wacc(P, acc2, wacc, tpb, tid);
+    block_epilogue(P, COND == kX1 ? accs : nullptr, wacc, red, n_acc, tpb, tid, cell, unconverged, ties, npts);
 }
 
 static size_t pca_smem_bytes(const PathArgs& a) {
@@ -1708,7 +1795,7 @@ static size_t path_smem_bytes(const PathArgs& a, int constr, int cond, int metho
     const size_t tpb = (size_t)1 << a.tpb_log2, nw = tpb / 32;
     const bool need_buf = method == kQmc && (constr == kPca || cond == kX1);
     const bool two_buf = method == kQmc && constr == kPca && cond == kX1;
-    size_t b = (size_t)a.n_opt * 8 * tpb * sizeof(double);
+    size_t b = 0;
     if (method == kQmc && constr == kPca && cond == kW1) b += (size_t)a.M_ld * (tpb + 8) * sizeof(double);
     else if (need_buf) b += (size_t)a.d * tpb * sizeof(double);
     if (two_buf) b += (size_t)a.d * tpb * sizeof(double);

@@ -70,26 +70,39 @@ __device__ __forceinline__ double rcp_newton(double y) {
     return fma(r, e, r);
 }
 
-// ln(t) for normal t > 0: t = 2^k m, m in [sqrt(1/2), sqrt(2)),
-// ln m = 2 atanh(f) = 2f + f^3 Q(f^2), f = (m-1)/(m+1).
-__device__ __forceinline__ double fast_log(double t) {
-    int hi = __double2hiint(t);
-    const int lo = __double2loint(t);
-    int k = (hi >> 20) - 1023;
-    int mhi = (hi & 0x000FFFFF) | 0x3FF00000;
-    const bool big = mhi > 0x3FF6A09E;  // m > sqrt(2)
-    mhi -= big ? 0x00100000 : 0;
-    k += big ? 1 : 0;
-    const double m = __hiloint2double(mhi, lo);
-    const double f = (m - MC.one) * rcp_newton(m + MC.one);
-    const double g = f * f;
-    const double gt = g - LOG_Q_CENTER;
-    double q = LOG_Q[10];
+// ln(t) for normal t > 0 by table lookup: t = 2^k m, m in [1, 2), i = top 6 mantissa
+// bits, ln t = k ln2 + ln c_i + log1p(r), r = fma(m, 1/c_i, -1) (|r| <= 2^-7, one
+// rounding), log1p(r) = r + r^2 L(r).  ~10 FP64 ops and no MUFU against ~22 + a MUFU
+// for the atanh form; the 1 KB table stays L1-resident (__ldg).
+__device__ __forceinline__ void fast_log_x2(double ta, double tb, double& la, double& lb) {
+    const int ha = __double2hiint(ta), hb = __double2hiint(tb);
+    const double ma = __hiloint2double((ha & 0x000FFFFF) | 0x3FF00000, __double2loint(ta));
+    const double mb = __hiloint2double((hb & 0x000FFFFF) | 0x3FF00000, __double2loint(tb));
+    const double ka = (double)((ha >> 20) - 1023), kb = (double)((hb >> 20) - 1023);
+    const double2 ca = __ldg(reinterpret_cast<const double2*>(LOG_TAB) + ((ha >> 14) & 63));
+    const double2 cb = __ldg(reinterpret_cast<const double2*>(LOG_TAB) + ((hb >> 14) & 63));
+    const double ra = fma(ma, ca.x, -MC.one), rb = fma(mb, cb.x, -MC.one);
+    double pa = LOG1P_L[5], pb = LOG1P_L[5];
 #pragma unroll
-    for (int j = 9; j >= 0; --j) q = fma(q, gt, LOG_Q[j]);
-    const double lnm = fma(f * g, q, MC.two * f);
-    const double kd = (double)k;
-    return fma(kd, MC.ln2_hi, fma(kd, MC.ln2_lo, lnm));
+    for (int j = 4; j >= 0; --j) {
+        pa = fma(pa, ra, LOG1P_L[j]);
+        pb = fma(pb, rb, LOG1P_L[j]);
+    }
+    const double sa = fma(ra * ra, pa, ra) + ca.y, sb = fma(rb * rb, pb, rb) + cb.y;
+    la = fma(ka, MC.ln2_hi, fma(ka, MC.ln2_lo, sa));
+    lb = fma(kb, MC.ln2_hi, fma(kb, MC.ln2_lo, sb));
+}
+
+__device__ __forceinline__ double fast_log(double t) {
+    const int h = __double2hiint(t);
+    const double m = __hiloint2double((h & 0x000FFFFF) | 0x3FF00000, __double2loint(t));
+    const double k = (double)((h >> 20) - 1023);
+    const double2 c = __ldg(reinterpret_cast<const double2*>(LOG_TAB) + ((h >> 14) & 63));
+    const double r = fma(m, c.x, -MC.one);
+    double p = LOG1P_L[5];
+#pragma unroll
+    for (int j = 4; j >= 0; --j) p = fma(p, r, LOG1P_L[j]);
+    return fma(k, MC.ln2_hi, fma(k, MC.ln2_lo, fma(r * r, p, r) + c.y));
 }
 
 // (a3) lattice point -> standard normal, Phi^{-1}((y + 1/2) 2^-32).
@@ -142,59 +155,6 @@ __device__ __forceinline__ void fast_exp_x2(double xa, double xb, double& ra, do
     rb = __hiloint2double(__double2hiint(pb) + (nb << 20), __double2loint(pb));
 }
 
-__device__ __forceinline__ void log_reduce(double t, double& m, double& kd) {
-    const int hi = __double2hiint(t), lo = __double2loint(t);
-    int k = (hi >> 20) - 1023;
-    int mhi = (hi & 0x000FFFFF) | 0x3FF00000;
-    const bool big = mhi > 0x3FF6A09E;
-    mhi -= big ? 0x00100000 : 0;
-    k += big ? 1 : 0;
-    m = __hiloint2double(mhi, lo);
-    kd = (double)k;
-}
-
-__device__ __forceinline__ void fast_log_x2(double ta, double tb, double& la, double& lb) {
-    double ma, mb, ka, kb;
-    log_reduce(ta, ma, ka);
-    log_reduce(tb, mb, kb);
-    const double fa = (ma - MC.one) * rcp_newton(ma + MC.one);
-    const double fb = (mb - MC.one) * rcp_newton(mb + MC.one);
-    const double ga = fa * fa, gb = fb * fb;
-    const double sa = ga - LOG_Q_CENTER, sb = gb - LOG_Q_CENTER;
-    double qa = LOG_Q[10], qb = LOG_Q[10];
-#pragma unroll
-    for (int j = 9; j >= 0; --j) {
-        qa = fma(qa, sa, LOG_Q[j]);
-        qb = fma(qb, sb, LOG_Q[j]);
-    }
-    const double lma = fma(fa * ga, qa, MC.two * fa), lmb = fma(fb * gb, qb, MC.two * fb);
-    la = fma(ka, MC.ln2_hi, fma(ka, MC.ln2_lo, lma));
-    lb = fma(kb, MC.ln2_hi, fma(kb, MC.ln2_lo, lmb));
-}
-
-// ln(t) for normal t > 0 by table lookup: t = 2^k m, m in [1, 2), i = top 6 mantissa
-// bits, ln t = k ln2 + ln c_i + log1p(r), r = fma(m, 1/c_i, -1) (|r| <= 2^-7, one
-// rounding), log1p(r) = r + r^2 L(r).  ~10 FP64 ops and no MUFU against ~22 + a MUFU
-// for the atanh form; the 1 KB table stays L1-resident (__ldg).
-__device__ __forceinline__ void fast_log_tab_x2(double ta, double tb, double& la, double& lb) {
-    const int ha = __double2hiint(ta), hb = __double2hiint(tb);
-    const double ma = __hiloint2double((ha & 0x000FFFFF) | 0x3FF00000, __double2loint(ta));
-    const double mb = __hiloint2double((hb & 0x000FFFFF) | 0x3FF00000, __double2loint(tb));
-    const double ka = (double)((ha >> 20) - 1023), kb = (double)((hb >> 20) - 1023);
-    const double2 ca = __ldg(reinterpret_cast<const double2*>(LOG_TAB) + ((ha >> 14) & 63));
-    const double2 cb = __ldg(reinterpret_cast<const double2*>(LOG_TAB) + ((hb >> 14) & 63));
-    const double ra = fma(ma, ca.x, -MC.one), rb = fma(mb, cb.x, -MC.one);
-    double pa = LOG1P_L[5], pb = LOG1P_L[5];
-#pragma unroll
-    for (int j = 4; j >= 0; --j) {
-        pa = fma(pa, ra, LOG1P_L[j]);
-        pb = fma(pb, rb, LOG1P_L[j]);
-    }
-    const double sa = fma(ra * ra, pa, ra) + ca.y, sb = fma(rb * rb, pb, rb) + cb.y;
-    la = fma(ka, MC.ln2_hi, fma(ka, MC.ln2_lo, sa));
-    lb = fma(kb, MC.ln2_hi, fma(kb, MC.ln2_lo, sb));
-}
-
 __device__ __noinline__ double icdf_tail_poly(double w) {
     const double v = sqrt(w) - ICDF_TAIL_CENTER;
     double p = ICDF_TAIL[24];
@@ -211,7 +171,7 @@ __device__ __forceinline__ void normal_from_u32_x2(uint32_t ya, uint32_t yb, dou
     const double za = fma(MC.two, ua, -MC.one), zb = fma(MC.two, ub, -MC.one);
     const double ta = (MC.four * ua) * (MC.one - ua), tb = (MC.four * ub) * (MC.one - ub);
     double wa, wb;
-    fast_log_tab_x2(ta, tb, wa, wb);
+    fast_log_x2(ta, tb, wa, wb);
     wa = -wa;
     wb = -wb;
     const double va = wa - ICDF_CENTRAL_CENTER, vb = wb - ICDF_CENTRAL_CENTER;
