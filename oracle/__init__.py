@@ -20,7 +20,7 @@ ARITH, BINARY, LOOKBACK, GEOM_CALL, GEOM_DIGITAL = 0, 1, 2, 100, 101
 STD, BB, PCA = 0, 1, 2
 W1, X1 = 0, 1
 QMC_CPW, LR_MC, MC_CPW, MC_AV_CPW = 0, 1, 2, 3
-RAND_LMS_SHIFT, RAND_SHIFT, RAND_NONE = 0, 1, 3
+RAND_LMS_SHIFT, RAND_SHIFT, RAND_NONE, RAND_OWEN = 0, 1, 3, 4
 DEFAULT_SEED = 2209113370
 
 
@@ -74,6 +74,8 @@ def lib():
                                    ctypes.c_uint64, P(Config), u32p]
         L.or_sobol_from_vectors.argtypes = [u32p, u32p, ctypes.c_uint32, ctypes.c_uint32, ctypes.c_uint64,
                                             ctypes.c_uint64, u32p]
+        L.or_owen_scramble.argtypes = [ctypes.c_uint32, ctypes.c_uint32]
+        L.or_owen_scramble.restype = ctypes.c_uint32
         L.or_inv_normal_cdf.argtypes = [ctypes.c_double]
         L.or_inv_normal_cdf.restype = ctypes.c_double
         L.or_normal_from_u32.argtypes = [ctypes.c_uint32]
@@ -152,6 +154,10 @@ def randomization(seed, rep, d, mode=RAND_LMS_SHIFT):
     c = np.zeros(d, np.uint32)
     _check(lib().or_randomization(seed, rep, d, mode, _u32(v), _u32(c)))
     return v, c
+
+
+def owen_scramble(y, seed):
+    return int(lib().or_owen_scramble(int(y) & 0xFFFFFFFF, int(seed) & 0xFFFFFFFF))
 
 
 def sobol_u32(rep, dim_begin, dim_end, k_begin, k_end, cfg=None):

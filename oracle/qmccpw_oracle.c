@@ -148,6 +148,36 @@ static int parity32(uint32_t x) {
     return p;
 }
 
+/* O2b  Nested uniform scrambling (Owen 1995; P:179-181 names it).
+ * Reading 27: the random permutations of Owen's tree are drawn by a hash, the
+ * Laine-Karras construction with Burley's constants (JCGT 9(4), 2020): on the
+ * bit-reversed coordinate r (r's bit i = y's digit i, MSB first),
+ *     r <- r + seed;  r <- r XOR (r * C_m) for the four constants C_m;
+ * then reversed back.  Addition carries and products with even constants only
+ * move information from lower to higher bits of r, so digit i of the output is
+ * digit i of y XOR a function of (seed, digits 0..i-1): a nested scramble.
+ * Written out digit by digit, without machine multiplication, so that it reads
+ * against that definition (the pins in tests/test_oracle_owen.py check the
+ * nesting, bijectivity and net properties it must have). */
+static uint32_t reverse32(uint32_t y) {
+    uint32_t r = 0;
+    for (int i = 0; i < 32; i++) r |= ((y >> i) & 1u) << (31 - i);
+    return r;
+}
+static uint32_t mul_mod32(uint32_t a, uint32_t c) { /* a * c mod 2^32 as a sum of shifted copies */
+    uint32_t s = 0;
+    for (int b = 0; b < 32; b++)
+        if ((c >> b) & 1u) s += a << b;
+    return s;
+}
+uint32_t or_owen_scramble(uint32_t y, uint32_t seed) {
+    static const uint32_t C[4] = {0x6c50b47cu, 0xb82f1e52u, 0xc7afe638u, 0x8d22f6e6u};
+    uint32_t r = reverse32(y);
+    r += seed;
+    for (int m = 0; m < 4; m++) r ^= mul_mod32(r, C[m]);
+    return reverse32(r);
+}
+
 /* Randomisation of dimension j in replicate rep (reading 10):
  * 32 Philox words from counters (j, w, 0, (rep<<8)|0x01), w = 0..7, key = seed.
  * word 0 -> digital shift; word i -> row i of a lower-triangular (MSB-first)
@@ -176,9 +206,18 @@ int or_randomization(uint64_t seed, uint32_t rep, int32_t d, int32_t randomizati
             for (int i = 0; i < 32; i++) out |= (uint32_t)parity32(rows[i] & v[b]) << (31 - i);
             vscr[32 * j + b] = out;
         }
+        /* OWEN: plain direction numbers; word 0 is the dimension's scramble seed */
         shift[j] = (randomization == OR_RAND_NONE) ? 0u : w[0];
     }
     return 0;
+}
+
+/* coordinate j of point k under the config's randomisation: for OWEN the shift
+ * slot c holds the scramble seed and the plain Sobol' integer is scrambled */
+static uint32_t sobol_direct(const uint32_t* v32, uint32_t shift, uint64_t k);
+static uint32_t sobol_point(const uint32_t* v32, uint32_t c, uint64_t k, int32_t randomization) {
+    if (randomization == OR_RAND_OWEN) return or_owen_scramble(sobol_direct(v32, 0u, k), c);
+    return sobol_direct(v32, c, k);
 }
 
 /* ------------------------------------------------------------------------ */
@@ -209,7 +248,12 @@ int or_sobol_u32(uint32_t rep, uint32_t dim_begin, uint32_t dim_end, uint64_t k_
     uint32_t* c = malloc(sizeof(uint32_t) * (dim_end ? dim_end : 1));
     int rc = 0;
     if (dim_end > 0) rc = or_randomization(cfg->seed, rep, (int32_t)dim_end, cfg->randomization, v, c);
-    if (rc == 0) rc = or_sobol_from_vectors(v, c, dim_begin, dim_end, k_begin, k_end, out);
+    if (rc == 0) {
+        uint64_t nk = k_end - k_begin;
+        for (uint32_t j = dim_begin; j < dim_end; j++)
+            for (uint64_t k = k_begin; k < k_end; k++)
+                out[(uint64_t)(j - dim_begin) * nk + (k - k_begin)] = sobol_point(v + 32 * j, c[j], k, cfg->randomization);
+    }
     free(v);
     free(c);
     return rc;
@@ -280,7 +324,7 @@ int or_normals(uint32_t rep, int32_t d, uint64_t k_begin, uint64_t k_end, const 
     if (rc == 0)
         for (uint64_t k = k_begin; k < k_end; k++)
             for (int j = 0; j < d; j++)
-                out[(k - k_begin) * d + j] = or_normal_from_u32(sobol_direct(v + 32 * j, c[j], k));
+                out[(k - k_begin) * d + j] = or_normal_from_u32(sobol_point(v + 32 * j, c[j], k, cfg->randomization));
     free(v);
     free(c);
     return rc;
@@ -794,7 +838,8 @@ static void* worker(void* arg) {
             if (jb->cfg->method != OR_QMC_CPW) {
                 for (int j = 0; j < d; j++) x[j] = lr_normal(jb->cfg->seed, (uint32_t)rep, k, j);
             } else {
-                for (int j = 0; j < d; j++) x[j] = or_normal_from_u32(sobol_direct(v + 32 * j, c[j], k));
+                for (int j = 0; j < d; j++)
+                    x[j] = or_normal_from_u32(sobol_point(v + 32 * j, c[j], k, jb->cfg->randomization));
             }
             for (int o = 0; o < n_opt && rc == 0; o++) {
                 double f[4];

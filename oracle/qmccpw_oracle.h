@@ -30,8 +30,9 @@ enum { OR_COND_W1 = 0, OR_COND_X1 = 1 };
  * MC+AV-CPW (pseudo-random normals, antithetic pairs averaged) */
 enum { OR_QMC_CPW = 0, OR_LR_MC = 1, OR_MC_CPW = 2, OR_MC_AV_CPW = 3 };
 /* randomisation of the Sobol' points: per-replicate left-matrix scramble +
- * digital shift, shift only, none (plain Sobol'), or caller-supplied vectors */
-enum { OR_RAND_LMS_SHIFT = 0, OR_RAND_SHIFT = 1, OR_RAND_NONE = 3 };
+ * digital shift, shift only, none (plain Sobol'), or nested (Owen) scrambling
+ * of every coordinate (reading 27) */
+enum { OR_RAND_LMS_SHIFT = 0, OR_RAND_SHIFT = 1, OR_RAND_NONE = 3, OR_RAND_OWEN = 4 };
 
 typedef struct {
     double S0, r, sigma, T;
@@ -69,6 +70,11 @@ void or_philox4x32_10(const uint32_t ctr[4], const uint32_t key[2], uint32_t out
 /* O2: randomised direction numbers v'[j*32+b] and shifts c[j] for replicate rep */
 int or_randomization(uint64_t seed, uint32_t rep, int32_t d, int32_t randomization,
                      uint32_t* vscr, uint32_t* shift);
+
+/* O2b: nested uniform (Owen) scramble of one 32-bit coordinate with a per-(replicate,
+ * dimension) seed: digit i of the result (MSB first) is digit i of y flipped by a
+ * function of the seed and digits 0..i-1 only (reading 27) */
+uint32_t or_owen_scramble(uint32_t y, uint32_t seed);
 
 /* O3: Sobol' integers y(rep, j, k) = c ^ XOR_{b in gray(k)} v'_b (direct formula),
  * out[(j-dim_begin)*(k_end-k_begin) + (k-k_begin)] */
