@@ -177,6 +177,8 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--construction", type=int, default=W.BB)
     ap.add_argument("--conditioning", type=int, default=W.W1)
+    ap.add_argument("--randomization", type=int, default=0,
+                    help="0 LMS + digital shift (default), 1 shift, 3 none, 4 nested Owen scrambling (row f4)")
     ap.add_argument("--workload", default="C4", choices=["C4", "C5"],
                     help="C4: 3 exotics fused, d=64 (the BASELINE metric); C5: 1024-option portfolio, d=128")
     ap.add_argument("--points", type=int, default=None)
@@ -217,7 +219,9 @@ def main():
         N = args.points or c["n_points"]
         L = (args.reps_per_gpu or c["n_replicates"]) * world
         plist = [q.params(S0=W.S0, K=100.0, r=W.R, sigma=W.SIGMA, T=W.T, d=d) for _ in options]
-    cfg = q.config(construction=args.construction, conditioning=args.conditioning, seed=W.SEED, device=local)
+    ckw = dict(construction=args.construction, conditioning=args.conditioning, randomization=args.randomization,
+               seed=W.SEED, device=local)
+    cfg = q.config(**ckw)
     pricer = DistributedPricer(options, plist, N, L, cfg, dev, rank, world)
 
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)  # > 126 MB L2
@@ -263,9 +267,7 @@ def main():
     # clean e2e measurement (host wall time around each public call, max over ranks);
     # one untimed call first so the library's scratch allocation is not inside the timing
     if world == 1:
-        q.qmccpw_price_greeks_batch(options, plist, N, L, q.config(construction=args.construction,
-                                                                   conditioning=args.conditioning, seed=W.SEED,
-                                                                   device=local))
+        q.qmccpw_price_greeks_batch(options, plist, N, L, q.config(**ckw))
     else:
         pricer.step()
     e2e_total = 0.0
@@ -276,9 +278,7 @@ def main():
             dist.barrier()
         t1 = time.perf_counter()
         if world == 1:
-            q.qmccpw_price_greeks_batch(options, plist, N, L, q.config(construction=args.construction,
-                                                                       conditioning=args.conditioning, seed=W.SEED,
-                                                                       device=local))
+            q.qmccpw_price_greeks_batch(options, plist, N, L, q.config(**ckw))
         else:
             pricer.step()
         e2e_total += time.perf_counter() - t1
@@ -303,7 +303,8 @@ def main():
     achieved = 2.0 * per_path * launch_paths / (kernel_avg_ms / 1e3) / 1e12
     traffic = None
     tpath = os.path.join(ROOT, "profiles", "ncu_traffic.json")
-    if os.path.exists(tpath) and args.workload == "C4" and (args.construction, args.conditioning) == (W.BB, W.W1):
+    if (os.path.exists(tpath) and args.workload == "C4" and args.randomization == 0
+            and (args.construction, args.conditioning) == (W.BB, W.W1)):
         try:
             traffic = json.load(open(tpath)).get("bytes_per_launch")
         except Exception:
@@ -327,7 +328,9 @@ def main():
                             ("C4: arithmetic+binary+lookback Asian calls fused on shared paths, S0=K=100, sigma=0.2, "
                              "r=0.1, T=1, d=64, " + {(1, 0): "BB-W1 (QMC+BB-CPW)", (0, 0): "STD-W1 (QMC-CPW)",
                                                      (2, 0): "PCA-W1", (2, 1): "PCA-X1 (Newton)"}.get(
-                                 (args.construction, args.conditioning), "custom")),
+                                 (args.construction, args.conditioning), "custom"))
+                            + {1: ", digital shift only", 3: ", plain Sobol'", 4: ", nested Owen scrambling (f4)"}.get(
+                                args.randomization, ""),
                 "points_per_replicate": N, "replicates_per_gpu": L // world, "replicates_total": L,
                 "global_batch": N * L, "seq_len": d, "parallelism": f"dp{world} (replicate-partitioned)",
                 "option_paths_per_s": value * len(options), "greek_sets_per_s": value * len(options),

@@ -78,7 +78,11 @@ typedef enum {
     QMCCPW_RAND_LMS_SHIFT = 0,     /* per-replicate left-matrix scramble + digital shift (reading 10) */
     QMCCPW_RAND_SHIFT = 1,         /* per-replicate digital shift only */
     QMCCPW_RAND_CURAND_COMPAT = 2, /* cuRAND QUASI_SCRAMBLED_SOBOL32; identical for every replicate */
-    QMCCPW_RAND_NONE = 3           /* plain Sobol' (cuRAND QUASI_SOBOL32) */
+    QMCCPW_RAND_NONE = 3,          /* plain Sobol' (cuRAND QUASI_SOBOL32) */
+    QMCCPW_RAND_OWEN = 4           /* nested uniform (Owen) scrambling of every coordinate, per-replicate
+                                      per-dimension seeds (reading 27): a hash-drawn
+                                      random permutation tree (Laine-Karras / Burley 2020) on top of plain
+                                      Sobol', so each replicate is an Owen-scrambled (t, m, s)-net */
 } qmccpw_randomization;
 
 /* ---- parameter blocks ------------------------------------------------- */

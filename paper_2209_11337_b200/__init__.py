@@ -19,7 +19,7 @@ ARITH_ASIAN_CALL, BINARY_ASIAN_CALL, LOOKBACK_CALL = 0, 1, 2
 STD, BB, PCA = 0, 1, 2
 COND_W1, COND_X1 = 0, 1
 QMC_CPW, LR_MC, MC_CPW, MC_AV_CPW = 0, 1, 2, 3
-RAND_LMS_SHIFT, RAND_SHIFT, RAND_CURAND_COMPAT, RAND_NONE = 0, 1, 2, 3
+RAND_LMS_SHIFT, RAND_SHIFT, RAND_CURAND_COMPAT, RAND_NONE, RAND_OWEN = 0, 1, 2, 3, 4
 DEFAULT_SEED = 2209113370
 CELL_POINTS = 4096
 OUTPUTS = ("price", "delta", "vega", "gamma")

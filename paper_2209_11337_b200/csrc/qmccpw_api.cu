@@ -146,7 +146,7 @@ int validate_config(const qmccpw_config& c, int d, uint64_t n_points, uint32_t n
     if (c.method < QMCCPW_QMC_CPW || c.method > QMCCPW_MC_AV_CPW) return fail(QMCCPW_EINVAL, "unknown method");
     if (c.construction < 0 || c.construction > 2) return fail(QMCCPW_EINVAL, "unknown construction");
     if (c.conditioning < 0 || c.conditioning > 1) return fail(QMCCPW_EINVAL, "unknown conditioning");
-    if (c.randomization < 0 || c.randomization > 3) return fail(QMCCPW_EINVAL, "unknown randomization");
+    if (c.randomization < 0 || c.randomization > 4) return fail(QMCCPW_EINVAL, "unknown randomization");
     if (n_points == 0) return fail(QMCCPW_EINVAL, "n_points must be >= 1");
     if (c.point_offset + n_points > (1ull << 32)) return fail(QMCCPW_EINVAL, "point_offset + n_points > 2^32");
     if (n_reps == 0 || n_reps >= (1u << 24)) return fail(QMCCPW_EINVAL, "n_replicates must be in [1, 2^24)");
@@ -328,6 +328,7 @@ int build_tables(DeviceCache* c, const Plan& pl, uint32_t rep_base, uint32_t tab
         int mode = 0;
         if (cfg.randomization == QMCCPW_RAND_SHIFT) mode = 1;
         if (cfg.randomization == QMCCPW_RAND_NONE) mode = 2;
+        if (cfg.randomization == QMCCPW_RAND_OWEN) mode = 3;  // plain vectors + per-dimension scramble seeds
         if (cfg.randomization == QMCCPW_RAND_CURAND_COMPAT) {
             mode = 2;
             base_v = c->base_v_scr;
@@ -426,6 +427,7 @@ PathArgs make_args(const Plan& pl, const Scratch& s) {
     a.partial_stride = pl.stride;
     a.path_out = nullptr;
     a.hook_option = -1;
+    a.owen = pl.cfg.randomization == QMCCPW_RAND_OWEN;
     return a;
 }
 
@@ -525,6 +527,7 @@ int launch_portfolio_plan(DeviceCache* c, const Plan& pl, const Scratch& s, uint
     a.S0 = p0.S0;
     a.r = p0.r;
     a.lnS0 = std::log(p0.S0);
+    a.owen = pl.cfg.randomization == QMCCPW_RAND_OWEN;
     a.has_lookback = 0;
     for (int o = 0; o < pl.n_opt; ++o) a.has_lookback |= pl.types[o] == QMCCPW_LOOKBACK_CALL;
     for (int f = 0; f < pl.n_fam; ++f) {
@@ -746,7 +749,8 @@ int qmccpw_sobol_u32(uint32_t replicate, uint32_t dim_begin, uint32_t dim_end, u
     const size_t n = (size_t)(dim_end - dim_begin) * (k_end - k_begin);
     uint32_t* d_out = nullptr;
     CUDA_TRY(cudaMalloc(&d_out, n * 4));
-    cudaError_t e = launch_sobol_hook(s.vscr, s.shift, pl.d, dim_begin, dim_end, k_begin, k_end, d_out, st);
+    cudaError_t e = launch_sobol_hook(s.vscr, s.shift, pl.d, dim_begin, dim_end, k_begin, k_end,
+                                      pl.cfg.randomization == QMCCPW_RAND_OWEN, d_out, st);
     if (e == cudaSuccess) e = cudaMemcpyAsync(out, d_out, n * 4, cudaMemcpyDeviceToHost, st);
     if (e == cudaSuccess) e = cudaStreamSynchronize(st);
     cudaFree(d_out);
@@ -784,7 +788,8 @@ int qmccpw_normals(uint32_t replicate, int32_t d, uint64_t k_begin, uint64_t k_e
     const size_t n = (size_t)d * (k_end - k_begin);
     double* d_out = nullptr;
     CUDA_TRY(cudaMalloc(&d_out, n * 8));
-    cudaError_t e = launch_normals_hook(s.vscr, s.shift, d, k_begin, k_end, method, pl.cfg.seed, replicate, d_out, st);
+    cudaError_t e = launch_normals_hook(s.vscr, s.shift, d, k_begin, k_end, method, pl.cfg.seed, replicate,
+                                        pl.cfg.randomization == QMCCPW_RAND_OWEN, d_out, st);
     if (e == cudaSuccess) e = cudaMemcpyAsync(out, d_out, n * 8, cudaMemcpyDeviceToHost, st);
     if (e == cudaSuccess) e = cudaStreamSynchronize(st);
     cudaFree(d_out);

@@ -74,6 +74,7 @@ struct PathArgs {
     // parity hook: per-path values out[(point index within range)][4] (NULL in production)
     double* path_out;
     int hook_option;         // option index whose values go to path_out
+    int owen;                // 1: nested (Owen) scrambling, shift[] holds the per-dimension seeds
 };
 
 // ---- portfolio (C5): up to kMaxPortfolio options in up to kMaxFamilies (sigma, T) families
@@ -107,6 +108,7 @@ struct PortfolioArgs {
     double* partials;
     int partial_stride;            // 8 n_opt + 3
     double* path_out;              // hook: [point][n_opt][4] or NULL
+    int owen;                      // 1: nested (Owen) scrambling (see PathArgs)
 };
 
 cudaError_t launch_portfolio(const PortfolioArgs& args, cudaStream_t st);
@@ -122,10 +124,10 @@ cudaError_t launch_paths(const PathArgs& args, int construction, int conditionin
 cudaError_t launch_reduce_cells(const double* d_partials, int stride, uint32_t rep_begin, uint32_t rep_end,
                                 uint32_t cells_per_rep, double* d_rep_sums, cudaStream_t st);
 cudaError_t launch_sobol_hook(const uint32_t* d_vscr, const uint32_t* d_shift, int d, uint32_t dim_begin,
-                              uint32_t dim_end, uint64_t k_begin, uint64_t k_end, uint32_t* d_out,
+                              uint32_t dim_end, uint64_t k_begin, uint64_t k_end, int owen, uint32_t* d_out,
                               cudaStream_t st);
 cudaError_t launch_normals_hook(const uint32_t* d_vscr, const uint32_t* d_shift, int d, uint64_t k_begin,
-                                uint64_t k_end, int method, uint64_t seed, uint32_t rep, double* d_out,
+                                uint64_t k_end, int method, uint64_t seed, uint32_t rep, int owen, double* d_out,
                                 cudaStream_t st);
 
 uint64_t& launch_counter();  // thread-local count of kernel launches

@@ -60,8 +60,8 @@ __global__ void randomization_kernel(const uint32_t* __restrict__ base_v, const 
         w[4 * blk + 2] = c[2];
         w[4 * blk + 3] = c[3];
     }
-    if (b == 0) shift[rj] = w[0];
-    if (mode == 1) {  // shift only
+    if (b == 0) shift[rj] = w[0];  // modes 0, 1: digital shift; mode 3 (Owen): the dimension's scramble seed
+    if (mode == 1 || mode == 3) {  // shift only / Owen: plain direction numbers
         vscr[gid] = v;
         return;
     }
@@ -148,12 +148,30 @@ cudaError_t launch_path_matrix(int construction, int d, int ld, double T, double
 // built for A and A+1 (f = 0, 1).  Per dimension a thread does two
 // shared-memory loads and one XOR; nothing is stored per thread.
 // ---------------------------------------------------------------------------
+// (a2, row f4) nested uniform (Owen) scramble of one coordinate: on the bit-reversed
+// integer (digit i of y -> bit i), add the dimension's seed and apply four
+// xor-multiplies by even constants (Laine-Karras hash, Burley's constants): carries
+// and even products only move information towards higher bits, so output digit i is
+// input digit i flipped by a function of (seed, digits 0..i-1).  BREV + 4 IMAD + 4 LOP3.
+__device__ __forceinline__ uint32_t owen_scramble(uint32_t y, uint32_t seed) {
+    uint32_t r = __brev(y) + seed;
+    r ^= r * 0x6c50b47cu;
+    r ^= r * 0xb82f1e52u;
+    r ^= r * 0xc7afe638u;
+    r ^= r * 0x8d22f6e6u;
+    return __brev(r);
+}
+
 struct SobolBlock {
     const uint32_t* G;   // smem [d][32]
     const uint32_t* HW;  // smem, current buffer [2][nw][d]
     int d, nw;
     int lane_t, w_t, f_t;
-    __device__ __forceinline__ uint32_t get(int j) const { return HW[(f_t * nw + w_t) * d + j] ^ G[j * 32 + lane_t]; }
+    const uint32_t* os = nullptr;  // Owen seeds [d] (smem) or nullptr (LMS / shift / plain: folded into HW)
+    __device__ __forceinline__ uint32_t get(int j) const {
+        const uint32_t y = HW[(f_t * nw + w_t) * d + j] ^ G[j * 32 + lane_t];
+        return os != nullptr ? owen_scramble(y, os[j]) : y;
+    }
 };
 
 __device__ __forceinline__ void sobol_build_g(const uint32_t* vt, int d, uint32_t* G, int tid, int tpb) {
@@ -177,7 +195,7 @@ __device__ __forceinline__ void sobol_build_hw(const uint32_t* vt, const uint32_
         const int w = rest % nw, f = rest / nw;
         const uint64_t A = A0 + (uint64_t)f;
         const uint32_t* v = vt + j * 32;
-        uint32_t y = sh[j];
+        uint32_t y = sh != nullptr ? sh[j] : 0u;  // nullptr: unshifted (Owen: sh holds the seeds)
         if (A & 1) y ^= v[p - 1];
         if (w & 1) y ^= v[4];
         const int gw = w ^ (w >> 1);
@@ -732,7 +750,8 @@ __global__ void __launch_bounds__(128, paths_min_blocks<CONSTR, COND, METHOD>())
     const uint64_t K0 = P.point_offset + i0;
     const uint64_t Ab = K0 >> tpb_log2;
     const uint64_t kt = K0 + (uint64_t)tid;
-    SobolBlock sob{G, HW, d, nw, (int)(kt & 31), (int)((kt >> 5) & (uint64_t)(nw - 1)), (int)((kt >> tpb_log2) - Ab)};
+    SobolBlock sob{G, HW, d, nw, (int)(kt & 31), (int)((kt >> 5) & (uint64_t)(nw - 1)), (int)((kt >> tpb_log2) - Ab),
+                   P.owen ? sh : nullptr};
     if (METHOD == kQmc) {
         const uint32_t* src = P.vscr + (size_t)rep_local * d * 32;
         for (int idx = tid; idx < d * 32; idx += tpb) vt[idx] = src[idx];
@@ -751,7 +770,7 @@ __global__ void __launch_bounds__(128, paths_min_blocks<CONSTR, COND, METHOD>())
         if (i0 + ((uint64_t)a << tpb_log2) >= P.n_points) break;  // block-uniform: ragged last cell
         if (METHOD == kQmc) {
             uint32_t* HWb = HW + (a & 1) * hw_size;  // double-buffered: one barrier per iteration
-            sobol_build_hw(vt, sh, d, P.dim_begin, tpb_log2, nw, Ab + (uint64_t)a, HWb, tid, tpb);
+            sobol_build_hw(vt, P.owen ? nullptr : sh, d, P.dim_begin, tpb_log2, nw, Ab + (uint64_t)a, HWb, tid, tpb);
             __syncthreads();
             sob.HW = HWb;
         }
@@ -1229,7 +1248,7 @@ __global__ void __launch_bounds__(128, pca_min_blocks<COND, KF>()) pca_kernel(co
     for (int a = 0; a < ppt; ++a) {
         if (i0 + ((uint64_t)a << tpb_log2) >= P.n_points) break;  // block-uniform
         uint32_t* HWb = HW + (a & 1) * hw_size;
-        sobol_build_hw(vt, sh, d, 0, tpb_log2, nw, Ab + (uint64_t)a, HWb, tid, tpb);
+        sobol_build_hw(vt, P.owen ? nullptr : sh, d, 0, tpb_log2, nw, Ab + (uint64_t)a, HWb, tid, tpb);
         __syncthreads();
         // W1: statistics of this lane's own path, handed over by its quad after each row tile
         W1Acc w1own;
@@ -1241,7 +1260,7 @@ __global__ void __launch_bounds__(128, pca_min_blocks<COND, KF>()) pca_kernel(co
             const uint64_t ip = i0 + (uint64_t)tp + ((uint64_t)a << tpb_log2);
             const bool valid = ip < P.n_points;
             const SobolBlock sp{G, HWb, d, nw, (int)(kp0 & 31), (int)((kp0 >> 5) & (uint64_t)(nw - 1)),
-                                (int)((kp0 >> tpb_log2) - Ab)};
+                                (int)((kp0 >> tpb_log2) - Ab), P.owen ? sh : nullptr};
             // A fragments: x[path][4 f + r4]
             double afr[KF];
 #pragma unroll
@@ -1576,7 +1595,7 @@ __global__ void __launch_bounds__(128) portfolio_kernel(const PortfolioArgs P) {
     for (int a = 0; a < ppt; ++a) {
         if (i0 + ((uint64_t)a << tpb_log2) >= P.n_points) break;  // block-uniform
         uint32_t* HWb = HW + (a & 1) * hw_size;
-        sobol_build_hw(vt, sh, d, 0, tpb_log2, nw, Ab + (uint64_t)a, HWb, tid, tpb);
+        sobol_build_hw(vt, P.owen ? nullptr : sh, d, 0, tpb_log2, nw, Ab + (uint64_t)a, HWb, tid, tpb);
         __syncthreads();  // also: every thread has left phase B of the previous point
         // ---- phase A -------------------------------------------------------
 #pragma unroll 1
@@ -1584,7 +1603,7 @@ __global__ void __launch_bounds__(128) portfolio_kernel(const PortfolioArgs P) {
             const int tp = wbase + 8 * rt + q;
             const uint64_t kp0 = K0 + (uint64_t)tp;
             const SobolBlock sp{G, HWb, d, nw, (int)(kp0 & 31), (int)((kp0 >> 5) & (uint64_t)(nw - 1)),
-                                (int)((kp0 >> tpb_log2) - Ab)};
+                                (int)((kp0 >> tpb_log2) - Ab), P.owen ? sh : nullptr};
             double afr[KF];
 #pragma unroll
             for (int f = 0; f < KF; f += 2) {
@@ -1919,7 +1938,7 @@ __device__ __forceinline__ HookSmem hook_setup(unsigned char* raw, const uint32_
 }
 
 __global__ void sobol_hook_kernel(const uint32_t* __restrict__ vscr, const uint32_t* __restrict__ shift, int d,
-                                  uint32_t dim_begin, uint32_t dim_end, uint64_t k_begin, uint64_t k_end,
+                                  uint32_t dim_begin, uint32_t dim_end, uint64_t k_begin, uint64_t k_end, int owen,
                                   uint32_t* __restrict__ out) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const int tpb_log2 = 7, tpb = 128, tid = threadIdx.x, nw = 4;
@@ -1927,11 +1946,12 @@ __global__ void sobol_hook_kernel(const uint32_t* __restrict__ vscr, const uint3
     const uint64_t nk = k_end - k_begin;
     const uint64_t K0 = k_begin + (uint64_t)blockIdx.x * kCellPoints;
     const uint64_t Ab = K0 >> tpb_log2, kt = K0 + tid;
-    SobolBlock sob{h.G, h.HW, d, nw, (int)(kt & 31), (int)((kt >> 5) & 3), (int)((kt >> tpb_log2) - Ab)};
+    SobolBlock sob{h.G, h.HW, d, nw, (int)(kt & 31), (int)((kt >> 5) & 3), (int)((kt >> tpb_log2) - Ab),
+                   owen ? h.sh : nullptr};
     for (int a = 0; a < kCellPoints / tpb; ++a) {
         if (K0 + ((uint64_t)a << tpb_log2) >= k_end) break;
         uint32_t* HWb = h.HW + (a & 1) * 2 * nw * d;
-        sobol_build_hw(h.vt, h.sh, d, 0, tpb_log2, nw, Ab + (uint64_t)a, HWb, tid, tpb);
+        sobol_build_hw(h.vt, owen ? nullptr : h.sh, d, 0, tpb_log2, nw, Ab + (uint64_t)a, HWb, tid, tpb);
         __syncthreads();
         sob.HW = HWb;
         const uint64_t k = K0 + tid + ((uint64_t)a << tpb_log2);
@@ -1942,7 +1962,7 @@ __global__ void sobol_hook_kernel(const uint32_t* __restrict__ vscr, const uint3
 
 __global__ void normals_hook_kernel(const uint32_t* __restrict__ vscr, const uint32_t* __restrict__ shift, int d,
                                     uint64_t k_begin, uint64_t k_end, int method, uint64_t seed, uint32_t rep,
-                                    double* __restrict__ out) {
+                                    int owen, double* __restrict__ out) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const int tpb_log2 = 7, tpb = 128, tid = threadIdx.x, nw = 4;
     const uint64_t K0 = k_begin + (uint64_t)blockIdx.x * kCellPoints;
@@ -1963,11 +1983,12 @@ __global__ void normals_hook_kernel(const uint32_t* __restrict__ vscr, const uin
     }
     HookSmem h = hook_setup(smem_raw, vscr, shift, d, tid, tpb);
     const uint64_t Ab = K0 >> tpb_log2, kt = K0 + tid;
-    SobolBlock sob{h.G, h.HW, d, nw, (int)(kt & 31), (int)((kt >> 5) & 3), (int)((kt >> tpb_log2) - Ab)};
+    SobolBlock sob{h.G, h.HW, d, nw, (int)(kt & 31), (int)((kt >> 5) & 3), (int)((kt >> tpb_log2) - Ab),
+                   owen ? h.sh : nullptr};
     for (int a = 0; a < kCellPoints / tpb; ++a) {
         if (K0 + ((uint64_t)a << tpb_log2) >= k_end) break;
         uint32_t* HWb = h.HW + (a & 1) * 2 * nw * d;
-        sobol_build_hw(h.vt, h.sh, d, 0, tpb_log2, nw, Ab + (uint64_t)a, HWb, tid, tpb);
+        sobol_build_hw(h.vt, owen ? nullptr : h.sh, d, 0, tpb_log2, nw, Ab + (uint64_t)a, HWb, tid, tpb);
         __syncthreads();
         sob.HW = HWb;
         const uint64_t k = K0 + tid + ((uint64_t)a << tpb_log2);
@@ -1984,20 +2005,20 @@ __global__ void normals_hook_kernel(const uint32_t* __restrict__ vscr, const uin
 }
 
 cudaError_t launch_sobol_hook(const uint32_t* d_vscr, const uint32_t* d_shift, int d, uint32_t dim_begin,
-                              uint32_t dim_end, uint64_t k_begin, uint64_t k_end, uint32_t* d_out,
+                              uint32_t dim_end, uint64_t k_begin, uint64_t k_end, int owen, uint32_t* d_out,
                               cudaStream_t st) {
     const uint64_t nk = k_end - k_begin;
     const unsigned grid = (unsigned)((nk + kCellPoints - 1) / kCellPoints);
     const size_t smem = ((size_t)d * 64 + d + 2 * 2 * 4 * d) * 4;
     cudaError_t e = cudaFuncSetAttribute(sobol_hook_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
-    sobol_hook_kernel<<<grid, 128, smem, st>>>(d_vscr, d_shift, d, dim_begin, dim_end, k_begin, k_end, d_out);
+    sobol_hook_kernel<<<grid, 128, smem, st>>>(d_vscr, d_shift, d, dim_begin, dim_end, k_begin, k_end, owen, d_out);
     ++launch_counter();
     return cudaGetLastError();
 }
 
 cudaError_t launch_normals_hook(const uint32_t* d_vscr, const uint32_t* d_shift, int d, uint64_t k_begin,
-                                uint64_t k_end, int method, uint64_t seed, uint32_t rep, double* d_out,
+                                uint64_t k_end, int method, uint64_t seed, uint32_t rep, int owen, double* d_out,
                                 cudaStream_t st) {
     const uint64_t nk = k_end - k_begin;
     const unsigned grid = (unsigned)((nk + kCellPoints - 1) / kCellPoints);
@@ -2005,7 +2026,7 @@ cudaError_t launch_normals_hook(const uint32_t* d_vscr, const uint32_t* d_shift,
     cudaError_t e =
         cudaFuncSetAttribute(normals_hook_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
-    normals_hook_kernel<<<grid, 128, smem, st>>>(d_vscr, d_shift, d, k_begin, k_end, method, seed, rep, d_out);
+    normals_hook_kernel<<<grid, 128, smem, st>>>(d_vscr, d_shift, d, k_begin, k_end, method, seed, rep, owen, d_out);
     ++launch_counter();
     return cudaGetLastError();
 }

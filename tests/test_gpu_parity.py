@@ -48,7 +48,7 @@ def ocfg(O, constr=1, cond=0, method=0, rand=0, offset=0, seed=W.SEED):
 
 
 # ------------------------------------------------------------------ (a2) Sobol'
-@pytest.mark.parametrize("rand", [0, 1, 3])
+@pytest.mark.parametrize("rand", [0, 1, 3, 4])
 @pytest.mark.parametrize("rep", [0, 5, 63])
 @pytest.mark.parametrize("krange", [(0, 4096), (12345, 12345 + 9000), ((1 << 20) - 777, (1 << 20) + 333)])
 def test_sobol_bit_exact(q, O, rand, rep, krange):
@@ -68,9 +68,10 @@ def test_sobol_curand_compat_matches_libcurand(q):
 
 
 def test_sobol_high_dims_and_period_end(q, O):
-    g = q.qmccpw_sobol_u32(2, 200, 256, (1 << 32) - 5000, 1 << 32, qcfg(q))
-    o = O.sobol_u32(2, 200, 256, (1 << 32) - 5000, 1 << 32, ocfg(O))
-    assert np.array_equal(g, o)
+    for rand in (0, 4):
+        g = q.qmccpw_sobol_u32(2, 200, 256, (1 << 32) - 5000, 1 << 32, qcfg(q, rand=rand))
+        o = O.sobol_u32(2, 200, 256, (1 << 32) - 5000, 1 << 32, ocfg(O, rand=rand))
+        assert np.array_equal(g, o)
 
 
 # ------------------------------------------------------------------ (a3) normals
@@ -85,11 +86,11 @@ def test_normals(q, O, method):
 
 
 # ------------------------------------------------------------------ (a4-a7, a9) per-path values
-def _pv_check(q, O, otype, K, d, constr, cond, method, rep, k0, k1, S0=W.S0, sigma=W.SIGMA, T=W.T, r=W.R):
+def _pv_check(q, O, otype, K, d, constr, cond, method, rep, k0, k1, S0=W.S0, sigma=W.SIGMA, T=W.T, r=W.R, rand=0):
     p = q.params(S0=S0, K=K, r=r, sigma=sigma, T=T, d=d)
-    g = q.qmccpw_path_values(otype, p, rep, k0, k1, qcfg(q, constr, cond, method))
+    g = q.qmccpw_path_values(otype, p, rep, k0, k1, qcfg(q, constr, cond, method, rand=rand))
     mk = O.market(S0, r, sigma, T, d)
-    o = O.path_values(otype, K, mk, ocfg(O, constr, cond, method), rep, k0, k1)
+    o = O.path_values(otype, K, mk, ocfg(O, constr, cond, method, rand=rand), rep, k0, k1)
     piv = np.abs(O.pivots(otype, K, mk)) + np.abs(O.pivots(otype, S0, mk))
     err = np.abs(g - o) / (np.abs(o) + piv)
     s2 = sigma * sigma * T / d
@@ -105,6 +106,29 @@ def test_path_values(q, O, constr, cond, otype, d):
     for K in W.STRIKES:
         _pv_check(q, O, otype, K, d, constr, cond, 0, 3, 1000, 1000 + 700)
     _pv_check(q, O, otype, 100.0, d, constr, cond, 0, 0, 0, 300)
+
+
+# ------------------------------------------------------------------ row f4: nested (Owen) scrambling
+def test_normals_owen(q, O):
+    for d, k0, k1, rep in ((64, 0, 5000, 0), (16, 777, 9000, 3), (5, 100, 700, 1)):
+        g = q.qmccpw_normals(rep, d, k0, k1, qcfg(q, rand=4))
+        o = O.normals(rep, d, k0, k1, ocfg(O, rand=4))
+        assert np.all(np.abs(g - o) <= 2e-15 * np.maximum(1.0, np.abs(o)))
+
+
+@pytest.mark.parametrize("constr,cond", MODES_ALL)
+def test_path_values_owen(q, O, constr, cond):
+    for otype in (0, 1, 2):
+        for d in (4, 64):
+            _pv_check(q, O, otype, 100.0, d, constr, cond, 0, 2, 4000, 4000 + 600, rand=4)
+
+
+def test_full_runs_owen(q, O):
+    N, L = 2 * 4096 + 77, 6
+    for constr, cond in ((1, 0), (0, 0), (2, 0), (2, 1)):
+        g = q.qmccpw_price_greeks_batch([0, 1, 2], [q.params(K=95.0, d=64)] * 3, N, L, qcfg(q, constr, cond, rand=4))
+        o, _ = O.price_greeks([(0, 95.0), (1, 95.0), (2, 95.0)], O.market(d=64), N, L, ocfg(O, constr, cond, rand=4))
+        _means_check(g, o)
 
 
 @pytest.mark.parametrize("otype", [0, 1, 2])
@@ -269,16 +293,17 @@ def _c5_subset(q, d, picks):
                                       for o in sel], sel
 
 
+@pytest.mark.parametrize("rand", [0, 4])
 @pytest.mark.parametrize("d", [16, 128])
-def test_portfolio_path_values(q, O, d):
+def test_portfolio_path_values(q, O, d, rand):
     # 8 (sigma, T) families x 3 option types, strikes across the C5 range
     picks = [f * 128 + m for f in range(8) for m in (5, 64, 127)]
     types, ps, sel = _c5_subset(q, d, picks)
-    cfg = qcfg(q, 2, 0)
+    cfg = qcfg(q, 2, 0, rand=rand)
     g = q.qmccpw_portfolio_path_values(types, ps, 1, 13, 13 + 300, cfg)
     for j, o in enumerate(sel):
         mk = O.market(o["S0"], o["r"], o["sigma"], o["T"], d)
-        ref = O.path_values(o["type"], o["K"], mk, ocfg(O, 2, 0), 1, 13, 13 + 300)
+        ref = O.path_values(o["type"], o["K"], mk, ocfg(O, 2, 0, rand=rand), 1, 13, 13 + 300)
         piv = np.abs(O.pivots(o["type"], o["K"], mk)) + np.abs(O.pivots(o["type"], o["S0"], mk))
         err = np.abs(g[:, j, :] - ref) / (np.abs(ref) + piv)
         s2 = o["sigma"] ** 2 * o["T"] / d
