@@ -17,7 +17,7 @@ LIB = os.path.join(HERE, "libqmccpw_oracle.so")
 JOE_KUO = os.path.join(HERE, "data", "new-joe-kuo-6.1024.txt")
 
 ARITH, BINARY, LOOKBACK, GEOM_CALL, GEOM_DIGITAL = 0, 1, 2, 100, 101
-STD, BB, PCA = 0, 1, 2
+STD, BB, PCA, GPCA = 0, 1, 2, 3
 W1, X1 = 0, 1
 QMC_CPW, LR_MC, MC_CPW, MC_AV_CPW = 0, 1, 2, 3
 RAND_LMS_SHIFT, RAND_SHIFT, RAND_NONE, RAND_OWEN = 0, 1, 3, 4
@@ -85,6 +85,7 @@ def lib():
                                     ctypes.c_uint64, f64p]
         L.or_path_matrix.argtypes = [ctypes.c_int32, ctypes.c_int32, ctypes.c_double, f64p]
         L.or_construct.argtypes = [ctypes.c_int32, ctypes.c_int32, ctypes.c_double, f64p, f64p]
+        L.or_path_matrix_gpca.argtypes = [P(Market), f64p]
         L.or_estimate.argtypes = [P(Option), P(Market), ctypes.c_int32, ctypes.c_int32, ctypes.c_int32, f64p, f64p]
         L.or_path_values.argtypes = [P(Option), P(Market), P(Config), ctypes.c_uint32, ctypes.c_uint64,
                                      ctypes.c_uint64, f64p]
@@ -199,6 +200,12 @@ def lr_normals(rep, d, k_begin, k_end, seed=DEFAULT_SEED):
 def path_matrix(construction, d, T=1.0):
     M = np.zeros((d, d))
     _check(lib().or_path_matrix(construction, d, T, _f64(M)))
+    return M
+
+
+def path_matrix_gpca(mk):
+    M = np.zeros((mk.d, mk.d))
+    _check(lib().or_path_matrix_gpca(ctypes.byref(mk), _f64(M)))
     return M
 
 

@@ -414,11 +414,57 @@ int or_construct(int32_t construction, int32_t d, double T, const double* x, dou
             W[j] = s;
         }
         free(M);
+    } else if (construction == OR_GPCA) {
+        return set_err(-1, "GPCA depends on the market: use or_path_matrix_gpca");
     } else {
         return set_err(-1, "unknown construction");
     }
     return 0;
 }
+
+/* O5b GPCA (P:883, P:904-906 name it, reading 28).  The
+ * gradient of the arithmetic average A = (1/d) sum_j S0 exp(omega t_j + sigma W_j)
+ * at W = 0 is proportional to s_j = exp(omega t_j).  With the PCA matrix M (M M^T
+ * = C), q = M^T s / |M^T s| and the Householder reflection H = I - 2 v v^T/(v^T v),
+ * v = e_1 - q (H e_1 = q, H orthogonal), the GPCA matrix is M H: still M H (M H)^T
+ * = C, and (M H)^T s = H q |M^T s| = e_1 |M^T s|, so the linear part of the average
+ * depends on x_1 alone.  Its first column is C s / sqrt(s^T C s) > 0. */
+static void gpca_matrix(int d, double T, double omega, double* M) {
+    double* s = malloc(sizeof(double) * d);
+    double* v = malloc(sizeof(double) * d);
+    pca_matrix(d, T, M);
+    for (int j = 0; j < d; j++) s[j] = exp(omega * (j + 1) * (T / d));
+    double norm2 = 0.0;
+    for (int k = 0; k < d; k++) {
+        double qk = 0.0; /* (M^T s)_k */
+        for (int j = 0; j < d; j++) qk += M[j * d + k] * s[j];
+        v[k] = qk;
+        norm2 += qk * qk;
+    }
+    double norm = sqrt(norm2), vv = 0.0;
+    for (int k = 0; k < d; k++) {
+        v[k] = (k == 0 ? 1.0 : 0.0) - v[k] / norm; /* v = e_1 - q */
+        vv += v[k] * v[k];
+    }
+    if (vv > 0.0) {
+        for (int j = 0; j < d; j++) {
+            double u = 0.0; /* (M v)_j */
+            for (int k = 0; k < d; k++) u += M[j * d + k] * v[k];
+            for (int k = 0; k < d; k++) M[j * d + k] -= 2.0 * u * v[k] / vv;
+        }
+    }
+    free(s);
+    free(v);
+}
+
+int or_path_matrix_gpca(const or_market* mk, double* M) {
+    if (mk->d < 1 || mk->d > OR_MAX_DIM) return set_err(-1, "d out of range");
+    gpca_matrix(mk->d, mk->T, mk->r - 0.5 * mk->sigma * mk->sigma, M);
+    return 0;
+}
+
+/* the path matrix a config needs for a market */
+static int path_matrix_mk(int32_t construction, const or_market* mk, double* M);
 
 /* M[:,k] = construct(e_k): the path matrix of any of the three constructions */
 int or_path_matrix(int32_t construction, int32_t d, double T, double* M) {
@@ -438,6 +484,11 @@ int or_path_matrix(int32_t construction, int32_t d, double T, double* M) {
     free(e);
     free(col);
     return rc;
+}
+
+static int path_matrix_mk(int32_t construction, const or_market* mk, double* M) {
+    if (construction == OR_GPCA) return or_path_matrix_gpca(mk, M);
+    return or_path_matrix(construction, mk->d, mk->T, M);
 }
 
 /* ------------------------------------------------------------------------ */
@@ -694,7 +745,16 @@ static int estimate_impl(const or_option* opt, const or_market* mk, int method, 
     if (conditioning == OR_COND_X1)
         return opt->type == OR_LOOKBACK ? estimate_x1_lookback(&m, M, x, out) : estimate_x1(opt->type, &m, M, x, out);
     double* W = malloc(sizeof(double) * mk->d);
-    int rc = or_construct(construction, mk->d, mk->T, x, W);
+    int rc = 0;
+    if (construction == OR_GPCA) { /* W = M x with the market's GPCA matrix */
+        for (int j = 0; j < mk->d; j++) {
+            double acc = 0.0;
+            for (int k = 0; k < mk->d; k++) acc += M[j * mk->d + k] * x[k];
+            W[j] = acc;
+        }
+    } else {
+        rc = or_construct(construction, mk->d, mk->T, x, W);
+    }
     if (rc == 0) rc = estimate_w1(opt->type, &m, W, out, opt->type == OR_LOOKBACK ? near_tie : NULL);
     free(W);
     return rc;
@@ -708,7 +768,8 @@ static int validate(const or_option* opt, const or_market* mk, int method, int c
     if (mk->d < 1 || mk->d > OR_MAX_DIM) return set_err(-1, "d out of range");
     if (construction == OR_BB && !is_pow2(mk->d)) return set_err(-2, "BB needs d = 2^m");
     if (method == OR_LR_MC && construction != OR_STD) return set_err(-2, "LR+MC uses the STD path");
-    if ((method == OR_MC_CPW || method == OR_MC_AV_CPW) && (construction == OR_PCA || conditioning != OR_COND_W1))
+    if (construction < OR_STD || construction > OR_GPCA) return set_err(-1, "unknown construction");
+    if ((method == OR_MC_CPW || method == OR_MC_AV_CPW) && (construction >= OR_PCA || conditioning != OR_COND_W1))
         return set_err(-2, "MC-CPW / MC+AV-CPW: STD or BB construction, W1 conditioning");
     if (method < 0 || method > 3) return set_err(-1, "unknown method");
     if (method == OR_QMC_CPW && conditioning == OR_COND_X1 && opt->type != OR_ARITH && opt->type != OR_BINARY &&
@@ -722,9 +783,9 @@ int or_estimate(const or_option* opt, const or_market* mk, int32_t method, int32
     int rc = validate(opt, mk, method, construction, conditioning);
     if (rc) return rc;
     double* M = NULL;
-    if (method == OR_QMC_CPW && conditioning == OR_COND_X1) {
+    if (method == OR_QMC_CPW && (conditioning == OR_COND_X1 || construction == OR_GPCA)) {
         M = malloc(sizeof(double) * mk->d * mk->d);
-        or_path_matrix(construction, mk->d, mk->T, M);
+        path_matrix_mk(construction, mk, M);
     }
     rc = estimate_impl(opt, mk, method, construction, conditioning, M, x, out, NULL);
     free(M);
@@ -739,9 +800,9 @@ int or_path_values(const or_option* opt, const or_market* mk, const or_config* c
     int d = mk->d;
     double* x = malloc(sizeof(double) * d);
     double* M = NULL;
-    if (cfg->method == OR_QMC_CPW && cfg->conditioning == OR_COND_X1) {
+    if (cfg->method == OR_QMC_CPW && (cfg->conditioning == OR_COND_X1 || cfg->construction == OR_GPCA)) {
         M = malloc(sizeof(double) * d * d);
-        or_path_matrix(cfg->construction, d, mk->T, M);
+        path_matrix_mk(cfg->construction, mk, M);
     }
     for (uint64_t k = k_begin; k < k_end && rc == 0; k++) {
         if (cfg->method != OR_QMC_CPW) rc = or_lr_normals(rep, d, k, k + 1, cfg->seed, x);
@@ -885,9 +946,9 @@ int or_price_greeks(const or_option* opts, int32_t n_opt, const or_market* mk, u
     memset(&jb, 0, sizeof jb);
     jb.opts = opts; jb.n_opt = n_opt; jb.mk = mk; jb.cfg = cfg; jb.N = n_points; jb.L = n_replicates;
     double* M = NULL;
-    if (cfg->method == OR_QMC_CPW && cfg->conditioning == OR_COND_X1) {
+    if (cfg->method == OR_QMC_CPW && (cfg->conditioning == OR_COND_X1 || cfg->construction == OR_GPCA)) {
         M = malloc(sizeof(double) * d * d);
-        or_path_matrix(cfg->construction, d, mk->T, M);
+        path_matrix_mk(cfg->construction, mk, M);
     }
     jb.M = M;
     double* piv = malloc(sizeof(double) * n_opt * 4);

@@ -23,7 +23,9 @@ extern "C" {
 /* option types; 100/101 are TEST-ONLY geometric products used by
  * the closed-form pin of SURVEY.md B3 */
 enum { OR_ARITH = 0, OR_BINARY = 1, OR_LOOKBACK = 2, OR_GEOM_CALL = 100, OR_GEOM_DIGITAL = 101 };
-enum { OR_STD = 0, OR_BB = 1, OR_PCA = 2 };
+/* OR_GPCA (row f3, reading 28): the PCA basis rotated by a Householder reflection so
+ * that x_1 carries the whole gradient of the arithmetic average at the origin */
+enum { OR_STD = 0, OR_BB = 1, OR_PCA = 2, OR_GPCA = 3 };
 enum { OR_COND_W1 = 0, OR_COND_X1 = 1 };
 /* methods compared in the paper: QMC-CPW (with the construction of the
  * config: STD = the paper's QMC-CPW, BB = QMC+BB-CPW), LR+MC, MC-CPW and
@@ -95,6 +97,8 @@ int or_lr_normals(uint32_t rep, int32_t d, uint64_t k_begin, uint64_t k_end, uin
 /* O5: path matrix M (row-major M[j*d+k]) of a construction, and W = construct(x) */
 int or_path_matrix(int32_t construction, int32_t d, double T, double* M);
 int or_construct(int32_t construction, int32_t d, double T, const double* x, double* W);
+/* O5b: the GPCA path matrix of a market (it depends on omega = r - sigma^2/2 through the gradient) */
+int or_path_matrix_gpca(const or_market* mk, double* M);
 
 /* O6-O9: per-path estimator values for explicit normals x[d]; out[4] = G, delta, vega, gamma */
 int or_estimate(const or_option* opt, const or_market* mk, int32_t method, int32_t construction,
