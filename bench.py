@@ -46,7 +46,7 @@ def fp64_model_per_path(d, constr, cond, n_opt, arith_x1=0):
     c_icdf = 50 (branch-light FP64 inverse normal), c_exp = 17, c_tail = 160
     per option (log + 2 erfc + exp + ~30 FMA), c_W = 1 (STD) / 2 (BB) / d (PCA)."""
     c_icdf, c_exp, c_tail = 50, 17, 160
-    c_w = {0: 1, 1: 2, 2: d}[constr]
+    c_w = {0: 1, 1: 2, 2: d, 3: d}[constr]  # GPCA: a rotated PCA matrix, same dense contraction
     d_icdf = d - 1 if (cond == 1 or constr == 0) else d
     if cond == 0:
         return d_icdf * c_icdf + d * (c_exp + c_w + 6) + n_opt * c_tail
@@ -327,7 +327,8 @@ def main():
                              "r=0.1, d=128, PCA-W1 (portfolio kernel)") if args.workload == "C5" else
                             ("C4: arithmetic+binary+lookback Asian calls fused on shared paths, S0=K=100, sigma=0.2, "
                              "r=0.1, T=1, d=64, " + {(1, 0): "BB-W1 (QMC+BB-CPW)", (0, 0): "STD-W1 (QMC-CPW)",
-                                                     (2, 0): "PCA-W1", (2, 1): "PCA-X1 (Newton)"}.get(
+                                                     (2, 0): "PCA-W1", (2, 1): "PCA-X1 (Newton)",
+                                                     (3, 0): "GPCA-W1 (f3)", (3, 1): "GPCA-X1 (Newton, f3)"}.get(
                                  (args.construction, args.conditioning), "custom"))
                             + {1: ", digital shift only", 3: ", plain Sobol'", 4: ", nested Owen scrambling (f4)"}.get(
                                 args.randomization, ""),

@@ -55,7 +55,11 @@ typedef enum {
 typedef enum {
     QMCCPW_STD = 0, /* standard recursion, Alg. 3 */
     QMCCPW_BB = 1,  /* Brownian bridge, Alg. 4; d must be 2^m */
-    QMCCPW_PCA = 2  /* principal components of min(t_i,t_j) */
+    QMCCPW_PCA = 2, /* principal components of min(t_i,t_j) */
+    QMCCPW_GPCA = 3 /* gradient-aligned PCA (reading 28): the PCA basis rotated by
+                       a Householder reflection so that x_1 carries the whole gradient of the arithmetic
+                       average at W = 0 (first column C s / sqrt(s^T C s), s_j = e^{omega t_j}); one market
+                       per call (not for portfolios), same kernels and cost as PCA */
 } qmccpw_construction;
 
 typedef enum {

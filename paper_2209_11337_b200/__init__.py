@@ -16,7 +16,7 @@ LIB_PATH = os.environ.get("QMCCPW_LIB") or os.path.join(_PKG, "libqmccpw.so")  #
 
 OK, EINVAL, EUNSUPPORTED, ECUDA, ENOMEM = 0, -1, -2, -3, -4
 ARITH_ASIAN_CALL, BINARY_ASIAN_CALL, LOOKBACK_CALL = 0, 1, 2
-STD, BB, PCA = 0, 1, 2
+STD, BB, PCA, GPCA = 0, 1, 2, 3
 COND_W1, COND_X1 = 0, 1
 QMC_CPW, LR_MC, MC_CPW, MC_AV_CPW = 0, 1, 2, 3
 RAND_LMS_SHIFT, RAND_SHIFT, RAND_CURAND_COMPAT, RAND_NONE, RAND_OWEN = 0, 1, 2, 3, 4

@@ -7,6 +7,7 @@
 #include <cuda_runtime.h>
 #include <curand.h>
 
+#include <algorithm>
 #include <cmath>
 #include <cstdio>
 #include <cstring>
@@ -144,7 +145,7 @@ int validate_params(const qmccpw_params* p) {
 
 int validate_config(const qmccpw_config& c, int d, uint64_t n_points, uint32_t n_reps) {
     if (c.method < QMCCPW_QMC_CPW || c.method > QMCCPW_MC_AV_CPW) return fail(QMCCPW_EINVAL, "unknown method");
-    if (c.construction < 0 || c.construction > 2) return fail(QMCCPW_EINVAL, "unknown construction");
+    if (c.construction < 0 || c.construction > 3) return fail(QMCCPW_EINVAL, "unknown construction");
     if (c.conditioning < 0 || c.conditioning > 1) return fail(QMCCPW_EINVAL, "unknown conditioning");
     if (c.randomization < 0 || c.randomization > 4) return fail(QMCCPW_EINVAL, "unknown randomization");
     if (n_points == 0) return fail(QMCCPW_EINVAL, "n_points must be >= 1");
@@ -155,7 +156,7 @@ int validate_config(const qmccpw_config& c, int d, uint64_t n_points, uint32_t n
     if (c.method == QMCCPW_LR_MC && c.construction != QMCCPW_STD)
         return fail(QMCCPW_EUNSUPPORTED, "LR+MC uses the standard construction");
     if ((c.method == QMCCPW_MC_CPW || c.method == QMCCPW_MC_AV_CPW) &&
-        (c.construction == QMCCPW_PCA || c.conditioning != QMCCPW_COND_W1))
+        (c.construction >= QMCCPW_PCA || c.conditioning != QMCCPW_COND_W1))
         return fail(QMCCPW_EUNSUPPORTED, "MC-CPW / MC+AV-CPW: STD or BB construction with W1 conditioning");
     if (d > kMaxDimGpu) return fail(QMCCPW_EUNSUPPORTED, "d > 256 is not supported by the sm_100a kernels");
     return QMCCPW_OK;
@@ -198,9 +199,19 @@ int tpb_log2_for(const qmccpw_config& c, int d, int n_opt) {
 }
 
 // mean of the first path-matrix column a_j (only seeds Newton's start, X1)
-double mean_first_column(int construction, int d, double T) {
+double mean_first_column(int construction, int d, double T, bool gpca, double omega) {
     const double dt = T / d;
     double s = 0.0;
+    if (gpca) {  // a = C e / sqrt(e^T C e), e_j = exp(omega t_j), C_ij = min(t_i, t_j)
+        double num = 0.0, q = 0.0;
+        for (int j = 1; j <= d; ++j) {
+            double cs = 0.0;
+            for (int i = 1; i <= d; ++i) cs += std::min(i, j) * dt * std::exp(omega * i * dt);
+            num += cs;
+            q += std::exp(omega * j * dt) * cs;
+        }
+        return num / std::sqrt(q) / d;
+    }
     for (int j = 1; j <= d; ++j) {
         if (construction == QMCCPW_STD) s += std::sqrt(dt);
         else if (construction == QMCCPW_BB) s += j * dt / std::sqrt(T);
@@ -223,6 +234,7 @@ struct Plan {
     uint64_t n_cells;
     int stride;
     bool portfolio;            // > 3 options or several (sigma, T) families: the C5 portfolio kernel
+    bool gpca;                 // QMCCPW_GPCA requested: cfg.construction is PCA, M rotated after it is built
     int n_fam;
     int fam_of[kMaxPortfolio];
     int fam_rep[kMaxFamilies];  // an option index representing each family
@@ -247,6 +259,11 @@ int make_plan(const int32_t* options, const qmccpw_params* p, int32_t n_options,
     int rc = validate_config(pl->cfg, p[0].d, n_points, n_reps);
     if (rc) return rc;
     pl->portfolio = !(same_market && n_options <= kMaxOpt);
+    pl->gpca = pl->cfg.construction == QMCCPW_GPCA;
+    if (pl->gpca) {
+        if (pl->portfolio) return fail(QMCCPW_EUNSUPPORTED, "GPCA: one market per call (not for portfolios)");
+        pl->cfg.construction = QMCCPW_PCA;  // same kernels; build_tables rotates M
+    }
     pl->n_fam = 0;
     for (int o = 0; o < n_options; ++o) {
         int f = 0;
@@ -341,6 +358,11 @@ int build_tables(DeviceCache* c, const Plan& pl, uint32_t rep_base, uint32_t tab
         CUDA_TRY(launch_path_matrix(cfg.construction, pl.d, (pl.d + 7) & ~7, pl.portfolio ? 1.0 : pl.p[0].T,
                                     pl.p[0].sigma,
                                     cfg.construction == QMCCPW_PCA ? s.M : nullptr, s.a, s.inv_sa, st));
+    if (cfg.method == QMCCPW_QMC_CPW && pl.gpca) {
+        const qmccpw_params& q = pl.p[0];
+        CUDA_TRY(launch_gpca_rotate(s.M, (pl.d + 7) & ~7, pl.d, q.T, q.r - 0.5 * q.sigma * q.sigma, q.sigma, s.a,
+                                    s.inv_sa, st));
+    }
     return QMCCPW_OK;
 }
 
@@ -416,7 +438,7 @@ PathArgs make_args(const Plan& pl, const Scratch& s) {
         for (int q = 0; q < pl.n_opt; ++q)
             if (a.tail_leader[q] == o && pl.types[q] == QMCCPW_ARITH_ASIAN_CALL) a.x1_need_arith[o] = 1;
     }
-    a.mean_a = mean_first_column(pl.cfg.construction, d, p.T);
+    a.mean_a = mean_first_column(pl.cfg.construction, d, p.T, pl.gpca, p.r - 0.5 * p.sigma * p.sigma);
     a.vscr = s.vscr;
     a.shift = s.shift;
     a.M = s.M;
@@ -848,6 +870,7 @@ int qmccpw_portfolio_path_values(const int32_t* options, const qmccpw_params* p,
     static thread_local Plan pl;  // large (1024 options): not on the stack twice
     int rc = make_plan(options, p, n_options, k_end - k_begin, 1, &c0, &pl);
     if (rc) return rc;
+    if (pl.gpca) return fail(QMCCPW_EUNSUPPORTED, "portfolio kernel: PCA (not GPCA)");
     pl.portfolio = true;  // force the portfolio kernel (also for <= 3 options)
     const int ld = (pl.d + 7) & ~7;
     if (pl.cfg.method != QMCCPW_QMC_CPW || pl.cfg.construction != QMCCPW_PCA || pl.cfg.conditioning != QMCCPW_COND_W1 ||

@@ -119,6 +119,8 @@ cudaError_t launch_randomization(const uint32_t* d_base_v, const uint32_t* d_bas
                                  cudaStream_t st);
 cudaError_t launch_path_matrix(int construction, int d, int ld, double T, double sigma, double* d_M, double* d_a,
                                double* d_inv_sa, cudaStream_t st);
+cudaError_t launch_gpca_rotate(double* d_M, int ld, int d, double T, double omega, double sigma, double* d_a,
+                               double* d_inv_sa, cudaStream_t st);
 cudaError_t launch_paths(const PathArgs& args, int construction, int conditioning, int method, cudaStream_t st,
                          int* smem_bytes_out);
 cudaError_t launch_reduce_cells(const double* d_partials, int stride, uint32_t rep_begin, uint32_t rep_end,

@@ -136,6 +136,75 @@ cudaError_t launch_path_matrix(int construction, int d, int ld, double T, double
 }
 
 // ---------------------------------------------------------------------------
+// (a1, row f3) GPCA: rotate the PCA matrix in place, M <- M H, by the Householder
+// reflection H = I - 2 v v^T / (v^T v), v = e_1 - q, q = M^T s / |M^T s|, s_j =
+// exp(omega t_j) (the arithmetic average's gradient at W = 0): H e_1 = q, so the
+// new first column is C s / sqrt(s^T C s) and M^T s is parallel to e_1.  One
+// block; then a_j = M_j1 and 1/(sigma a_j) for X1.  Runs once per call.
+// ---------------------------------------------------------------------------
+__global__ void gpca_rotate_kernel(double* __restrict__ M, int ld, int d, double dt, double omega, double sigma,
+                                   double* __restrict__ a, double* __restrict__ inv_sa) {
+    extern __shared__ double gsm[];
+    double* sv = gsm;       // s_j, then v_k
+    double* u = gsm + d;    // (M^T s)_k, then (M v)_j
+    __shared__ double red[32];
+    const int tid = threadIdx.x, nt = blockDim.x;
+    for (int j = tid; j < d; j += nt) sv[j] = exp(omega * (double)(j + 1) * dt);
+    __syncthreads();
+    for (int k = tid; k < d; k += nt) {
+        double w = 0.0;
+        for (int j = 0; j < d; ++j) w = fma(M[(size_t)j * ld + k], sv[j], w);
+        u[k] = w;
+    }
+    __syncthreads();
+    auto block_sum = [&](double x) {  // deterministic: warp butterflies, then warps in order
+        for (int off = 16; off > 0; off >>= 1) x += __shfl_xor_sync(0xffffffffu, x, off);
+        if ((tid & 31) == 0) red[tid >> 5] = x;
+        __syncthreads();
+        double t = 0.0;
+        for (int w = 0; w < (nt + 31) / 32; ++w) t += red[w];
+        __syncthreads();
+        return t;
+    };
+    double part = 0.0;
+    for (int k = tid; k < d; k += nt) part = fma(u[k], u[k], part);
+    const double norm = sqrt(block_sum(part));
+    part = 0.0;
+    for (int k = tid; k < d; k += nt) {
+        const double vk = (k == 0 ? 1.0 : 0.0) - u[k] / norm;
+        sv[k] = vk;
+        part = fma(vk, vk, part);
+    }
+    const double vv = block_sum(part);  // its barriers also publish sv
+    if (vv > 0.0) {
+        for (int j = tid; j < d; j += nt) {
+            double w = 0.0;
+            for (int k = 0; k < d; ++k) w = fma(M[(size_t)j * ld + k], sv[k], w);
+            u[j] = w;
+        }
+        __syncthreads();
+        const double c = 2.0 / vv;
+        for (int idx = tid; idx < d * d; idx += nt) {
+            const int j = idx / d, k = idx % d;
+            M[(size_t)j * ld + k] -= c * u[j] * sv[k];
+        }
+        __syncthreads();
+    }
+    for (int j = tid; j < d; j += nt) {
+        const double aj = M[(size_t)j * ld];
+        a[j] = aj;
+        inv_sa[j] = 1.0 / (sigma * aj);
+    }
+}
+
+cudaError_t launch_gpca_rotate(double* d_M, int ld, int d, double T, double omega, double sigma, double* d_a,
+                               double* d_inv_sa, cudaStream_t st) {
+    gpca_rotate_kernel<<<1, 256, (size_t)2 * d * sizeof(double), st>>>(d_M, ld, d, T / d, omega, sigma, d_a, d_inv_sa);
+    ++launch_counter();
+    return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------------------
 // (a2) Sobol' integers without per-thread state.  A block of 2^p threads visits
 // the points k = K0 + tid + a 2^p (a = 0, 1, ...).  With k = A 2^p + tau and
 // tau = 32 w + l (l the lane slot), the Gray code g(k) = k ^ (k >> 1) splits as

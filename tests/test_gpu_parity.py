@@ -131,6 +131,35 @@ def test_full_runs_owen(q, O):
         _means_check(g, o)
 
 
+# ------------------------------------------------------------------ row f3: GPCA
+@pytest.mark.parametrize("cond", [0, 1])
+@pytest.mark.parametrize("d", [4, 16, 64, 128, 200])
+def test_path_values_gpca(q, O, cond, d):
+    for otype in (0, 1, 2):
+        for K in (90.0, 110.0):
+            _pv_check(q, O, otype, K, d, 3, cond, 0, 1, 2000, 2000 + (300 if d > 64 else 600))
+
+
+def test_full_runs_gpca_and_other_markets(q, O):
+    N, L = 2 * 4096 + 77, 5
+    for cond in (0, 1):
+        g = q.qmccpw_price_greeks_batch([0, 1, 2], [q.params(K=105.0, d=64)] * 3, N, L, qcfg(q, 3, cond))
+        o, _ = O.price_greeks([(0, 105.0), (1, 105.0), (2, 105.0)], O.market(d=64), N, L, ocfg(O, 3, cond))
+        _means_check(g, o)
+    # a market with omega < 0 (the gradient direction decays in t)
+    p = q.params(S0=100.0, K=100.0, r=0.01, sigma=0.5, T=2.0, d=16)
+    g = q.qmccpw_price_greeks(0, p, N, L, qcfg(q, 3, 1))
+    o, _ = O.price_greeks([(0, 100.0)], O.market(100.0, 0.01, 0.5, 2.0, 16), N, L, ocfg(O, 3, 1))
+    _means_check([g], o)
+
+
+def test_gpca_rejected_for_portfolios(q):
+    ps = [q.params(K=90.0 + o, d=16) for o in range(5)]
+    with pytest.raises(q.QmcCpwError) as e:
+        q.qmccpw_price_greeks_batch([0, 1, 2, 0, 1], ps, 4096, 2, qcfg(q, 3, 0))
+    assert e.value.code == q.EUNSUPPORTED
+
+
 @pytest.mark.parametrize("otype", [0, 1, 2])
 def test_path_values_lr(q, O, otype):
     for d in (1, 4, 64):
