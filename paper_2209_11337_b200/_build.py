@@ -1,17 +1,25 @@
-"""Build libqmccpw.so in-tree for sm_100a (nvcc cross-compiles without a GPU)."""
+"""Build libqmccpw.so in-tree for sm_100a (nvcc cross-compiles without a GPU).
+
+The kernels are split over several translation units (path kernels W1 / X1, PCA
+W1 / X1, portfolio, tables + hooks, the C ABI, the roof microbenchmark) that are
+compiled in parallel and linked into one shared library."""
 import os
 import subprocess
 
 PKG = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
-SOURCES = [os.path.join(CSRC, f) for f in ("qmccpw_kernels.cu", "qmccpw_api.cu", "qmccpw_microbench.cu")]
-HEADERS = [os.path.join(CSRC, f) for f in ("qmccpw_internal.h", "qmccpw_math.cuh")] + \
-    [os.path.join(ROOT, "include", "qmccpw.h")]
+SOURCES = [os.path.join(CSRC, f) for f in (
+    "qmccpw_paths_w1.cu", "qmccpw_paths_x1.cu", "qmccpw_pca_w1.cu", "qmccpw_pca_x1.cu", "qmccpw_pca_x1_owen.cu",
+    "qmccpw_portfolio.cu",
+    "qmccpw_kernels.cu", "qmccpw_api.cu", "qmccpw_microbench.cu")]
+HEADERS = [os.path.join(CSRC, f) for f in (
+    "qmccpw_internal.h", "qmccpw_math.cuh", "qmccpw_coeffs.cuh", "qmccpw_device.cuh", "qmccpw_paths.cuh",
+    "qmccpw_pca.cuh")] + [os.path.join(ROOT, "include", "qmccpw.h")]
 LIB = os.path.join(PKG, "libqmccpw.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
-FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
-         "-Xcompiler", "-fPIC", "-shared", "-Xptxas", "-v"]
+ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
+CFLAGS = ARCH + ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xptxas", "-v", "-c"]
 
 
 def stale():
@@ -22,19 +30,37 @@ def stale():
 
 
 def build(force=False, verbose=False, defines=(), out=None):
-    """defines/out: build an experimental variant (e.g. -DQMCCPW_ACC_SMEM=1) to another
+    """defines/out: build an experimental variant (e.g. -DQMCCPW_BB_MINB=7) to another
     file, selected at load time with QMCCPW_LIB=<path> (A/B timing in one GPU session)."""
     if out is None and not force and not stale():
         return LIB
-    cmd = [NVCC] + FLAGS + [f"-D{d}" for d in defines] + ["-o", out or LIB] + SOURCES + ["-lcurand"]
-    res = subprocess.run(cmd, capture_output=True, text=True)
+    target = out or LIB
+    objdir = os.path.join(PKG, "build", os.path.basename(target) + ".o.d")
+    os.makedirs(objdir, exist_ok=True)
+    procs = []
+    for src in SOURCES:
+        obj = os.path.join(objdir, os.path.basename(src)[:-3] + ".o")
+        cmd = [NVCC] + CFLAGS + [f"-D{d}" for d in defines] + ["-o", obj, src]
+        procs.append((src, obj, subprocess.Popen(cmd, stdout=subprocess.PIPE, stderr=subprocess.PIPE, text=True)))
+    logs, objs, failed = [], [], []
+    for src, obj, p in procs:
+        so, se = p.communicate()
+        logs.append(f"==== {os.path.basename(src)}\n{so}{se}")
+        objs.append(obj)
+        if p.returncode != 0:
+            failed.append(src)
+    info = os.path.join(PKG, "ptxas_info.txt" if out is None else os.path.basename(out) + ".ptxas.txt")
+    with open(info, "w") as f:
+        f.write("\n".join(logs))
+    if failed:
+        raise RuntimeError("nvcc failed for " + ", ".join(failed) + ":\n" + "\n".join(logs))
+    res = subprocess.run([NVCC] + ARCH + ["-shared", "-o", target] + objs + ["-lcurand"], capture_output=True,
+                         text=True)
     if res.returncode != 0:
-        raise RuntimeError("nvcc failed:\n" + res.stdout + res.stderr)
-    with open(os.path.join(PKG, "ptxas_info.txt" if out is None else os.path.basename(out) + ".ptxas.txt"), "w") as f:
-        f.write(res.stderr)
+        raise RuntimeError("link failed:\n" + res.stdout + res.stderr)
     if verbose:
-        print(res.stderr)
-    return out or LIB
+        print("\n".join(logs))
+    return target
 
 
 if __name__ == "__main__":

@@ -1,0 +1,600 @@
+// qmccpw_device.cuh -- device building blocks shared by the sm_100a kernels of the
+// QMC-CPW hot path (arXiv 2209.11337): stateless Sobol' tables, the W1 accumulators,
+// the option tails, X1 threshold solvers, the LR path and the block reductions.
+//
+// One thread carries one path at a time through the whole pipeline in FP64
+// ("each thread will be responsible for the simulation of one
+// path"), but nothing is materialised in HBM: Sobol' integers come from two
+// per-block shared-memory tables, the normals are consumed as they are produced,
+// the Brownian bridge is generated in time order from a log2(d)-deep stack, and
+// each block reduces its cell of 4096 points to one row of partial sums.  The
+// paper instead materialises normals and the bridge in global memory and names
+// that round trip as its 4x slowdown.
+//
+// Device code here is independent of oracle/: it is written from the paper
+// and SURVEY.md Sec. 8(a); tests compare the two on the same points.
+#pragma once
+#include <cuda_runtime.h>
+#include <math_constants.h>
+#include <stdint.h>
+
+#include "qmccpw_internal.h"
+#include "qmccpw_math.cuh"
+
+namespace qmccpw {
+
+// ---------------------------------------------------------------------------
+// (a2) Sobol' integers without per-thread state.  A block of 2^p threads visits
+// the points k = K0 + tid + a 2^p (a = 0, 1, ...).  With k = A 2^p + tau and
+// tau = 32 w + l (l the lane slot), the Gray code g(k) = k ^ (k >> 1) splits as
+//   g(k) = (g(A) << p) ^ ((A & 1) << (p-1)) ^ g(l) ^ ((w & 1) << 4) ^ (g(w) << 5)
+// (P:147-151 XOR form), so y_j(k) = HW_j(A, w) ^ G_j(l) with
+//   G_j(l)    = XOR_{b in g(l)} v'_{j,b}                       (per block,  [d][32])
+//   HW_j(A,w) = c_j ^ XOR_{b in g(A)} v'_{j,p+b} ^ (A&1) v'_{j,p-1}
+//               ^ (w&1) v'_{j,4} ^ XOR_{b in g(w)} v'_{j,5+b}      (per point iteration)
+// Threads of a block share A up to +1 (first index not 2^p-aligned), so HW is
+// built for A and A+1 (f = 0, 1).  Per dimension a thread does two
+// shared-memory loads and one XOR; nothing is stored per thread.
+// ---------------------------------------------------------------------------
+// (a2, row f4) nested uniform (Owen) scramble of one coordinate: on the bit-reversed
+// integer (digit i of y -> bit i), add the dimension's seed and apply four
+// xor-multiplies by even constants (Laine-Karras hash, Burley's constants): carries
+// and even products only move information towards higher bits, so output digit i is
+// input digit i flipped by a function of (seed, digits 0..i-1).  BREV + 4 IMAD + 4 LOP3.
+__device__ __forceinline__ uint32_t owen_scramble(uint32_t y, uint32_t seed) {
+    uint32_t r = __brev(y) + seed;
+    r ^= r * 0x6c50b47cu;
+    r ^= r * 0xb82f1e52u;
+    r ^= r * 0xc7afe638u;
+    r ^= r * 0x8d22f6e6u;
+    return __brev(r);
+}
+
+struct SobolBlock {
+    const uint32_t* G;   // smem [d][32]
+    const uint32_t* HW;  // smem, current buffer [2][nw][d]
+    int d, nw;
+    int lane_t, w_t, f_t;
+    const uint32_t* os = nullptr;  // Owen seeds [d] (smem) or nullptr (LMS / shift / plain: folded into HW)
+    __device__ __forceinline__ uint32_t get(int j) const {
+        const uint32_t y = HW[(f_t * nw + w_t) * d + j] ^ G[j * 32 + lane_t];
+        return os != nullptr ? owen_scramble(y, os[j]) : y;
+    }
+};
+
+__device__ __forceinline__ void sobol_build_g(const uint32_t* vt, int d, uint32_t* G, int tid, int tpb) {
+    for (int idx = tid; idx < d * 32; idx += tpb) {
+        const int j = idx >> 5, l = idx & 31;
+        const int g = l ^ (l >> 1);
+        uint32_t y = 0;
+#pragma unroll
+        for (int b = 0; b < 5; ++b)
+            if ((g >> b) & 1) y ^= vt[j * 32 + b];
+        G[idx] = y;
+    }
+}
+
+__device__ __forceinline__ void sobol_build_hw(const uint32_t* vt, const uint32_t* sh, int d, int j0, int p, int nw,
+                                               uint64_t A0, uint32_t* HW, int tid, int tpb) {
+    const int n = 2 * nw * d;
+    for (int idx = tid; idx < n; idx += tpb) {
+        const int j = idx % d, rest = idx / d;
+        if (j < j0) continue;
+        const int w = rest % nw, f = rest / nw;
+        const uint64_t A = A0 + (uint64_t)f;
+        const uint32_t* v = vt + j * 32;
+        uint32_t y = sh != nullptr ? sh[j] : 0u;  // nullptr: unshifted (Owen: sh holds the seeds)
+        if (A & 1) y ^= v[p - 1];
+        if (w & 1) y ^= v[4];
+        const int gw = w ^ (w >> 1);
+        if (gw & 1) y ^= v[5];
+        if (gw & 2) y ^= v[6];
+        uint32_t gA = (uint32_t)(A ^ (A >> 1)) & ((p >= 32) ? 0u : (0xFFFFFFFFu >> p));
+        while (gA) {
+            const int b = __ffs(gA) - 1;
+            y ^= v[p + b];
+            gA &= gA - 1;
+        }
+        HW[idx] = y;
+    }
+}
+
+// ---------------------------------------------------------------------------
+// (a5) W1-mode accumulators over the separated path S~(t_j):
+// S~_A, I_A (vega inner sum), and the lookback's S~_max with the
+// lowest argmax j* and I_max = S~_{j*}(W~_{j*} - sigma(t_{j*} - t_1))
+// (P:599 with the 1/d removed, reading 3).  Near-ties are tracked with the
+// runner-up exponent.
+// ---------------------------------------------------------------------------
+// MC-CPW / MC+AV-CPW / LR+MC normals: Philox4x32-10, counter (k_lo, k_hi, j/4,
+// (rep<<8)|0x02), word j%4 (the paper's PSEUDO generator).
+__device__ __forceinline__ uint32_t pick4(const uint32_t c[4], int w) {
+    return w == 0 ? c[0] : (w == 1 ? c[1] : (w == 2 ? c[2] : c[3]));
+}
+__device__ __forceinline__ void mc_normal_pair(const PathArgs& P, uint32_t rep, uint64_t k, int ja, int jb, double& xa,
+                                               double& xb) {
+    uint32_t ca[4] = {(uint32_t)k, (uint32_t)(k >> 32), (uint32_t)(ja >> 2), (rep << 8) | 0x02u};
+    philox4x32_10(ca, (uint32_t)P.seed, (uint32_t)(P.seed >> 32));
+    const uint32_t ya = pick4(ca, ja & 3);
+    uint32_t yb;
+    if ((jb >> 2) == (ja >> 2)) {
+        yb = pick4(ca, jb & 3);
+    } else {
+        uint32_t cb[4] = {(uint32_t)k, (uint32_t)(k >> 32), (uint32_t)(jb >> 2), (rep << 8) | 0x02u};
+        philox4x32_10(cb, (uint32_t)P.seed, (uint32_t)(P.seed >> 32));
+        yb = pick4(cb, jb & 3);
+    }
+    normal_from_u32_x2(ya, yb, xa, xb);
+}
+
+struct W1Acc {
+    double sumS, sumI, emax, esec, ymax;
+    __device__ __forceinline__ void reset() {
+        sumS = 0.0; sumI = 0.0; emax = -CUDART_INF; esec = -CUDART_INF; ymax = 0.0;
+    }
+    // lookback: lowest argmax of e_j (= argmax of S~_j) and the runner-up exponent,
+    // with plain compare-selects (no NaN-aware fmax/fmin: e is always finite)
+    __device__ __forceinline__ void track(double e, double y) {
+        const bool gt = e > emax;
+        const double cand = gt ? emax : e;
+        esec = cand > esec ? cand : esec;
+        ymax = gt ? y : ymax;
+        emax = gt ? e : emax;
+    }
+    // date index j (0-based, t_{j+1} - t_1 = j dt), Wt = W~(t_{j+1} - t_1)
+    __device__ __forceinline__ void push(const PathArgs& P, int j, double Wt) {
+        const double tt = (double)j * P.t1;
+        const double e = fma(P.sigma, Wt, P.omega * tt);
+        const double St = P.S0 * fast_exp(e);
+        const double y = fma(-P.sigma, tt, Wt);
+        sumS += St;
+        sumI = fma(St, y, sumI);
+        if (P.has_lookback) track(e, y);
+    }
+    // dates j and j+1 together (paired exp)
+    __device__ __forceinline__ void push2(const PathArgs& P, int j, double Wa, double Wb) {
+        const double ta = (double)j * P.t1, tb = ta + P.t1;
+        const double ea = fma(P.sigma, Wa, P.omega * ta), eb = fma(P.sigma, Wb, P.omega * tb);
+        double Xa, Xb;
+        fast_exp_x2(ea, eb, Xa, Xb);
+        const double Sa = P.S0 * Xa, Sb = P.S0 * Xb;
+        const double ya = fma(-P.sigma, ta, Wa), yb = fma(-P.sigma, tb, Wb);
+        sumS += Sa;
+        sumI = fma(Sa, ya, sumI);
+        sumS += Sb;
+        sumI = fma(Sb, yb, sumI);
+        if (P.has_lookback) {
+            track(ea, ya);
+            track(eb, yb);
+        }
+    }
+    // S~_max and I_max = S~_{j*} (W~_{j*} - sigma (t_{j*} - t_1)), rebuilt once per path
+    __device__ __forceinline__ double smax(const PathArgs& P) const { return P.S0 * fast_exp(emax); }
+};
+
+// Two-slot FIFO of standard normals drawn in a fixed dimension order, two
+// lattice points per refill (normal_from_u32_x2): the construction loops
+// consume one normal at a time while the special functions run paired.
+struct NormalFifo {
+    double x0, x1;
+    int have;
+    __device__ __forceinline__ void reset() { have = 0; }
+    template <class DimAt>
+    __device__ __forceinline__ double next(const SobolBlock& sob, DimAt dim_at) {
+        if (have == 0) {
+            normal_from_u32_x2(sob.get(dim_at(0)), sob.get(dim_at(1)), x0, x1);
+            have = 2;
+        }
+        const double r = (have == 2) ? x0 : x1;
+        --have;
+        return r;
+    }
+    // same, with an arbitrary pair drawer draw(dim_a, dim_b, x_a, x_b)
+    template <class Draw, class DimAt>
+    __device__ __forceinline__ double next_from(Draw draw, DimAt dim_at) {
+        if (have == 0) {
+            draw(dim_at(0), dim_at(1), x0, x1);
+            have = 2;
+        }
+        const double r = (have == 2) ? x0 : x1;
+        --have;
+        return r;
+    }
+};
+
+// (a6)+(a7) W1 threshold psi_d and the closed-form smoothed
+// payoff and Greeks (readings 1-5), all options of the
+// launch at once.  Options with the same strike and statistic (the arithmetic
+// and binary Asians of C4) share psi, phi(psi), Phibar(psi), Phibar(psi - s):
+// P.tail_leader[o] names the first such option.
+__device__ __forceinline__ void tail_w1_all(const PathArgs& P, const W1Acc& acc, double f[kMaxOpt][4]) {
+    const double inv_d = 1.0 / (double)P.d;
+    const double SA = acc.sumS * inv_d, IA = acc.sumI * inv_d;
+    const double Smax = P.has_lookback ? acc.smax(P) : SA;
+    const double Imax = Smax * acc.ymax;
+    double lnSA, lnSmax;
+    fast_log_x2(SA, Smax, lnSA, lnSmax);
+    double psi[kMaxOpt], Q0[kMaxOpt], Q1[kMaxOpt], ph[kMaxOpt];
+#pragma unroll
+    for (int o = 0; o < kMaxOpt; ++o) {
+        if (o >= P.n_opt) break;
+        const bool lb = P.type[o] == kLookback;
+        const int ld = P.tail_leader[o];
+        if (ld == o) {
+            psi[o] = (P.lnK[o] - (lb ? lnSmax : lnSA) - P.omega * P.t1) * P.inv_s;
+            double phs;
+            phibar_phi_x2(psi[o], psi[o] - P.s, Q0[o], Q1[o], ph[o], phs);
+        } else {
+            // leader index ld < o, resolved with selects (no dynamic register indexing)
+            psi[o] = ld == 0 ? psi[0] : psi[ld == 1 ? 1 : 0];
+            Q0[o] = ld == 0 ? Q0[0] : Q0[ld == 1 ? 1 : 0];
+            Q1[o] = ld == 0 ? Q1[0] : Q1[ld == 1 ? 1 : 0];
+            ph[o] = ld == 0 ? ph[0] : ph[ld == 1 ? 1 : 0];
+        }
+        const double stat = lb ? Smax : SA;
+        const double I = lb ? Imax : IA;
+        const double K = P.K[o], D = P.Dfac, S0 = P.S0;
+        if (P.type[o] == kBinary) {
+            f[o][0] = D * Q0[o];
+            f[o][1] = D * ph[o] * P.inv_s / S0;
+            f[o][2] = D * ph[o] * (I * P.inv_s / stat + psi[o] * P.inv_sigma - P.sqrt_t1);
+            f[o][3] = D * ph[o] * P.inv_s / (S0 * S0) * (psi[o] * P.inv_s - 1.0);
+        } else {
+            f[o][0] = P.Afac * stat * Q1[o] - D * K * Q0[o];
+            f[o][1] = P.Afac * (stat / S0) * Q1[o];
+            f[o][2] = P.Afac * Q1[o] * I + K * D * ph[o] * P.sqrt_t1;
+            f[o][3] = K * D * ph[o] * P.inv_s / (S0 * S0);
+        }
+    }
+}
+
+// (a6)+(a7) X1 mode: u* solves sum_j exp(c_j + sigma a_j u) = dK
+// by Newton from the AM-GM start, warp-uniform iteration count, clamped to the
+// bracket; then the conditional payoff and Greeks.  cb = per-thread c_j column.
+struct X1Sums {
+    double u, Dst, Qst, Vst, sumW, sumWv;
+};
+
+__device__ __forceinline__ X1Sums x1_solve(const PathArgs& P, int o, bool arith, const double* cb, int stride,
+                                           unsigned& unconverged) {
+    const int d = P.d;
+    const double lnK = P.lnK[o], lndK = P.lndK[o], sg = P.sigma;
+    double u_lo = CUDART_INF, u_hi = CUDART_INF, sumc = 0.0;
+    for (int j = 0; j < d; ++j) {
+        const double cj = cb[j * stride];
+        const double isa = P.inv_sa[j];
+        u_lo = fmin(u_lo, (lnK - cj) * isa);
+        u_hi = fmin(u_hi, (lndK - cj) * isa);
+        sumc += cj;
+    }
+    double u = fmin(u_hi, (lnK - sumc / d) / (sg * P.mean_a));
+    bool conv = false;
+    for (int it = 0; it < kNewtonMax; ++it) {
+        double S = 0.0, SA = 0.0;
+        int j = 0;
+#pragma unroll 1
+        for (; j + 1 < d; j += 2) {
+            const double aa = P.a[j], ab = P.a[j + 1];
+            double Ea, Eb;
+            fast_exp_x2(fma(sg * aa, u, cb[j * stride]), fma(sg * ab, u, cb[(j + 1) * stride]), Ea, Eb);
+            S += Ea;
+            SA = fma(aa, Ea, SA);
+            S += Eb;
+            SA = fma(ab, Eb, SA);
+        }
+        if (j < d) {
+            const double aj = P.a[j];
+            const double E = fast_exp(fma(sg * aj, u, cb[j * stride]));
+            S += E;
+            SA = fma(aj, E, SA);
+        }
+        const double h = fast_log(S) - lndK;
+        const double du = h * S / (sg * SA);
+        conv = fabs(du) <= 1e-13 * fmax(1.0, fabs(u));
+        u = fmin(fmax(u - du, u_lo), u_hi);
+        if (it + 1 >= kNewtonIt && __all_sync(__activemask(), conv)) break;
+    }
+    unconverged += conv ? 0u : 1u;
+    double Dst = 0.0, Qst = 0.0, Vst = 0.0, sumW = 0.0, sumWv = 0.0;
+#pragma unroll 1
+    for (int j = 0; j < d; j += 2) {
+        const int jb = (j + 1 < d) ? j + 1 : j;
+        const double wgt = (j + 1 < d) ? 1.0 : 0.0;  // odd d: the duplicate pair member counts 0
+        const double aa = P.a[j], ab = P.a[jb], ca = cb[j * stride], cbb = cb[jb * stride];
+        const double ta = (double)(j + 1) * P.t1, tb = (double)(jb + 1) * P.t1;
+        const double Ra = (ca - P.lnS0 - P.omega * ta) * P.inv_sigma, Rb = (cbb - P.lnS0 - P.omega * tb) * P.inv_sigma;
+        double Ea, Eb;
+        fast_exp_x2(fma(sg * aa, u, ca), fma(sg * ab, u, cbb), Ea, Eb);
+        Eb *= wgt;
+        Dst = fma(aa, Ea, Dst);
+        Qst = fma(aa * aa, Ea, Qst);
+        Vst = fma(Ea, Ra - sg * ta + aa * u, Vst);
+        Dst = fma(ab, Eb, Dst);
+        Qst = fma(ab * ab, Eb, Qst);
+        Vst = fma(Eb, Rb - sg * tb + ab * u, Vst);
+        if (arith) {
+            double wa, wb, Pa, Pb, pa, pb;
+            fast_exp_x2(fma(0.5 * sg * sg * aa, aa, ca), fma(0.5 * sg * sg * ab, ab, cbb), wa, wb);
+            phibar_phi_x2(u - sg * aa, u - sg * ab, Pa, Pb, pa, pb);  // Phi(sigma a - u) = Phibar(u - sigma a)
+            wb *= wgt;
+            sumW = fma(wa, Pa, sumW);
+            sumWv = fma(wa * (Ra - sg * ta + sg * aa * aa), Pa, sumWv);
+            sumW = fma(wb, Pb, sumW);
+            sumWv = fma(wb * (Rb - sg * tb + sg * ab * ab), Pb, sumWv);
+        }
+    }
+    return X1Sums{u, Dst, Qst, Vst, sumW, sumWv};
+}
+
+// outputs of option o from the shared sums of its strike
+__device__ __forceinline__ void x1_outputs(const PathArgs& P, int o, const X1Sums& x, double f[4]) {
+    const double D = P.Dfac, S0 = P.S0, K = P.K[o], dd = (double)P.d, sg = P.sigma, u = x.u;
+    const double Dst = x.Dst, Qst = x.Qst, Vst = x.Vst, sumW = x.sumW, sumWv = x.sumWv;
+    const bool arith = P.type[o] == kArith;
+    double ph, Qu, Q2, ph2;
+    phibar_phi_x2(u, u, Qu, Q2, ph, ph2);
+    if (arith) {
+        f[0] = D * (sumW / dd - K * Qu);
+        f[1] = D * sumW / (dd * S0);
+        f[2] = D * (sumWv / dd + ph * Dst / dd);
+        f[3] = D * dd * K * K * ph / (S0 * S0 * sg * Dst);
+    } else {
+        const double up = -dd * K / (S0 * sg * Dst);
+        f[0] = D * Qu;
+        f[1] = D * ph * dd * K / (S0 * sg * Dst);
+        f[2] = D * ph * Vst / (sg * Dst);
+        f[3] = D * (dd * K / sg) * ph / (S0 * Dst) * (-u * up - 2.0 / S0 - sg * up * Qst / Dst);
+    }
+}
+
+// Lookback under X1 (next-row f1).  Lines l_j(u) = c_j + b_j u,
+// b_j = sigma a_j; u* = min_j (ln K - c_j)/b_j in closed form; G integrates
+// exp(max_j l_j(u)) phi(u) over [u*, inf), walking the upper envelope from u*:
+// on each segment the next breakpoint is the first steeper line to overtake.
+__device__ __forceinline__ void x1_lookback(const PathArgs& P, int o, const double* cb, int stride, double f[4]) {
+    const int d = P.d;
+    const double sg = P.sigma, lnK = P.lnK[o];
+    double ustar = CUDART_INF;
+    int j0 = 0;
+    for (int j = 0; j < d; ++j) {
+        const double uj = (lnK - cb[j * stride]) * P.inv_sa[j];
+        if (uj < ustar) {
+            ustar = uj;
+            j0 = j;
+        }
+    }
+    // active line at u*: the maximum there; on ties the steeper one (it dominates just after)
+    int act = 0;
+    double best = -CUDART_INF, bact = 0.0;
+    for (int j = 0; j < d; ++j) {
+        const double bj = sg * __ldg(P.a + j);
+        const double v = fma(bj, ustar, cb[j * stride]);
+        if (v > best || (v == best && bj > bact)) {
+            best = v;
+            act = j;
+            bact = bj;
+        }
+    }
+    double J = 0.0, V = 0.0, lo = ustar;
+    for (int seg = 0; seg < d; ++seg) {
+        const double cact = cb[act * stride];
+        double hi = CUDART_INF, bn = 0.0;
+        int nxt = -1;
+        for (int i = 0; i < d; ++i) {
+            const double bi = sg * __ldg(P.a + i);
+            if (bi > bact) {
+                const double x = (cact - cb[i * stride]) / (bi - bact);
+                if (x < hi || (x == hi && bi > bn)) {
+                    hi = x;
+                    nxt = i;
+                    bn = bi;
+                }
+            }
+        }
+        hi = fmax(hi, lo);
+        const double aa = bact / sg;
+        const double tj = (double)(act + 1) * P.t1;
+        const double Rj = (cact - P.lnS0 - P.omega * tj) * P.inv_sigma;
+        const double w = fast_exp(fma(0.5 * bact, bact, cact));
+        double Qlo, Qhi, plo, phi_hi;
+        phibar_phi_x2(lo - bact, (nxt < 0) ? 0.0 : hi - bact, Qlo, Qhi, plo, phi_hi);
+        if (nxt < 0) {
+            Qhi = 0.0;
+            phi_hi = 0.0;
+        }
+        J = fma(w, Qlo - Qhi, J);
+        V = fma(w, (Rj - sg * tj + sg * aa * aa) * (Qlo - Qhi) + aa * (plo - phi_hi), V);
+        if (nxt < 0) break;
+        lo = hi;
+        act = nxt;
+        bact = bn;
+    }
+    const double D = P.Dfac, S0 = P.S0, K = P.K[o];
+    double Qu, Q2, ph, ph2;
+    phibar_phi_x2(ustar, ustar, Qu, Q2, ph, ph2);
+    f[0] = D * (J - K * Qu);
+    f[1] = D * J / S0;
+    f[2] = D * V;
+    f[3] = D * K * ph / (S0 * S0 * sg * __ldg(P.a + j0));
+}
+
+// all options of the launch: one Newton solve (and one set of E*-sums) per distinct strike
+__device__ __forceinline__ void tail_x1_all(const PathArgs& P, const double* cb, int stride, double f[kMaxOpt][4],
+                                            unsigned& unconverged) {
+    X1Sums xs[kMaxOpt];
+#pragma unroll
+    for (int o = 0; o < kMaxOpt; ++o) {
+        if (o >= P.n_opt) break;
+        if (P.type[o] == kLookback) {
+            x1_lookback(P, o, cb, stride, f[o]);
+            xs[o] = X1Sums{0, 0, 0, 0, 0, 0};
+            continue;
+        }
+        const int ld = P.tail_leader[o];
+        if (ld == o) {
+            xs[o] = x1_solve(P, o, P.x1_need_arith[o] != 0, cb, stride, unconverged);
+        } else {
+            xs[o] = ld == 0 ? xs[0] : xs[ld == 1 ? 1 : 0];
+        }
+        x1_outputs(P, o, xs[o], f[o]);
+    }
+}
+
+// (a9) LR+MC: Philox normals (counter (k_lo, k_hi, j/4, (rep<<8)|0x02)),
+// STD path of full prices, payoff x score.
+__device__ __forceinline__ void lr_path(const PathArgs& P, uint32_t rep, uint64_t k, double f[kMaxOpt][4]) {
+    const int d = P.d;
+    double W = 0.0, sumS = 0.0, Smax = 0.0, vscore = 0.0, Z1 = 0.0;
+    for (int jq = 0; jq < d; jq += 4) {
+        uint32_t c[4] = {(uint32_t)k, (uint32_t)(k >> 32), (uint32_t)(jq >> 2), (rep << 8) | 0x02u};
+        philox4x32_10(c, (uint32_t)P.seed, (uint32_t)(P.seed >> 32));
+        double xs[4];
+        normal_from_u32_x2(c[0], c[1], xs[0], xs[1]);
+        if (jq + 2 < d) normal_from_u32_x2(c[2], c[3], xs[2], xs[3]);
+#pragma unroll
+        for (int w = 0; w < 4; ++w) {
+            const int j = jq + w;
+            if (j < d) {
+                const double x = xs[w];
+                if (j == 0) Z1 = x;
+                W = fma(P.sqrt_t1, x, W);
+                const double S = P.S0 * fast_exp(fma(P.sigma, W, P.omega * (double)(j + 1) * P.t1));
+                sumS += S;
+                Smax = fmax(Smax, S);
+                vscore += (x * x - 1.0) * P.inv_sigma - x * P.sqrt_t1;
+            }
+        }
+    }
+    const double SA = sumS / d, S0 = P.S0, sg = P.sigma, t1 = P.t1;
+    const double sd = Z1 / (S0 * sg * P.sqrt_t1);
+    const double sgm = (Z1 * Z1 - 1.0) / (S0 * S0 * sg * sg * t1) - Z1 / (S0 * S0 * sg * P.sqrt_t1);
+#pragma unroll
+    for (int o = 0; o < kMaxOpt; ++o) {
+        if (o >= P.n_opt) break;
+        double pay;
+        if (P.type[o] == kArith) pay = P.Dfac * fmax(SA - P.K[o], 0.0);
+        else if (P.type[o] == kBinary) pay = (SA > P.K[o]) ? P.Dfac : 0.0;
+        else pay = P.Dfac * fmax(Smax - P.K[o], 0.0);
+        f[o][0] = pay;
+        f[o][1] = pay * sd;
+        f[o][2] = pay * vscore;
+        f[o][3] = pay * sgm;
+    }
+}
+
+// ---------------------------------------------------------------------------
+// The fused path kernel: one block = one cell (replicate, 4096 points).
+// ---------------------------------------------------------------------------
+// (a8) per-iteration warp reduction of the centred sums of option o (8 slots: S1, S2
+// per Greek, slot 2q + {0,1}, the partials layout): a reduce-scatter that halves
+// the slot set at xor 16, 8, 4 (each lane sends the half it drops), then a butterfly
+// over xor 2, 1; lanes 4s..4s+3 end with the warp total of slot s = lane >> 2, and
+// lane 4s adds it to the warp's running sums wacc[o*8 + s] in shared memory (no
+// per-thread accumulators, nothing live in registers across paths).
+__device__ __forceinline__ void warp_slot_sums(const double (&f)[kMaxOpt][4], const PathArgs& P, bool valid,
+                                               int lane, double* wacc) {
+#pragma unroll
+    for (int o = 0; o < kMaxOpt; ++o) {
+        if (o >= P.n_opt) break;  // warp-uniform
+        double v[8];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            const double y = valid ? f[o][q] - P.piv[o][q] : 0.0;
+            v[2 * q] = y;
+            v[2 * q + 1] = y * y;
+        }
+#pragma unroll
+        for (int half = 4; half > 0; half >>= 1) {
+            const bool up = (lane & (half * 4)) != 0;
+#pragma unroll
+            for (int j = 0; j < half; ++j) {
+                const double send = up ? v[j] : v[j + half];
+                const double keep = up ? v[j + half] : v[j];
+                v[j] = keep + __shfl_xor_sync(0xffffffffu, send, half * 4);
+            }
+        }
+        v[0] += __shfl_xor_sync(0xffffffffu, v[0], 2);
+        v[0] += __shfl_xor_sync(0xffffffffu, v[0], 1);
+        if ((lane & 3) == 0) wacc[o * 8 + (lane >> 2)] += v[0];
+    }
+}
+
+// per-thread (S1, S2) double2 accumulators in smem: cheaper in issue slots than the warp
+// reduction, so kernels with smem to spare (pca_kernel, register-limited) use it; the
+// path kernel, at its smem limit, uses warp_slot_sums (measured: BB-W1 -8%, PCA-W1 +4%)
+__device__ __forceinline__ void thread_acc2(const double (&f)[kMaxOpt][4], const PathArgs& P, bool valid,
+                                            double2* acc2, int tpb, int tid) {
+    if (!valid) return;
+#pragma unroll
+    for (int o = 0; o < kMaxOpt; ++o) {
+        if (o >= P.n_opt) break;
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            const double y = f[o][q] - P.piv[o][q];
+            double2* a = acc2 + (size_t)(o * 4 + q) * tpb + tid;
+            double2 t = *a;
+            t.x += y;
+            t.y = fma(y, y, t.y);
+            *a = t;
+        }
+    }
+}
+__device__ __forceinline__ void acc2_to_wacc(const PathArgs& P, const double2* acc2, double* wacc, int tpb, int tid) {
+    const int lane = tid & 31;
+    for (int v = 0; v < P.n_opt * 8; ++v) {
+        const double2 t = acc2[(size_t)(v >> 1) * tpb + tid];
+        double s1 = (v & 1) ? t.y : t.x;
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) s1 += __shfl_xor_sync(0xffffffffu, s1, off);
+        if (lane == 0) wacc[(tid >> 5) * 32 + v] = s1;
+    }
+}
+
+// (a8) fixed-shape reduction of a block's accumulators into its cell's partials:
+// warp butterfly, then the warps in order (deterministic for a given block size).
+__device__ __forceinline__ void block_epilogue(const PathArgs& P, const double* accs, const double* wacc, double* red,
+                                               int n_acc, int tpb, int tid, uint64_t cell, unsigned unconverged,
+                                               unsigned ties, unsigned npts) {
+    const int lane = tid & 31, warp = tid >> 5, nwarps = tpb >> 5;
+    const int n_out = P.partial_stride;
+    __syncthreads();  // red aliases the Sobol' tables
+    if (accs == nullptr) {  // per-warp sums (warp_slot_sums)
+        if (lane < n_acc) red[warp * 32 + lane] = wacc[warp * 32 + lane];
+    } else {
+        for (int v = 0; v < n_acc; ++v) {
+            double s1 = accs[v * tpb + tid];
+#pragma unroll
+            for (int off = 16; off > 0; off >>= 1) s1 += __shfl_xor_sync(0xffffffffu, s1, off);
+            if (lane == 0) red[warp * 32 + v] = s1;
+        }
+    }
+    unsigned uc = unconverged, tc = ties, nc = npts;
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) {
+        uc += __shfl_xor_sync(0xffffffffu, uc, off);
+        tc += __shfl_xor_sync(0xffffffffu, tc, off);
+        nc += __shfl_xor_sync(0xffffffffu, nc, off);
+    }
+    if (lane == 0) {
+        red[warp * 32 + P.n_opt * 8 + 0] = (double)uc;
+        red[warp * 32 + P.n_opt * 8 + 1] = (double)tc;
+        red[warp * 32 + P.n_opt * 8 + 2] = (double)nc;  // points this cell evaluated (completeness check)
+    }
+    __syncthreads();
+    if (tid < n_out) {
+        double s = 0.0;
+        for (int w = 0; w < nwarps; ++w) s += red[w * 32 + tid];
+        P.partials[(size_t)cell * n_out + tid] = s;
+    }
+}
+
+__device__ __forceinline__ double quad_sum(double v) {
+    v += __shfl_xor_sync(0xffffffffu, v, 1);
+    return v + __shfl_xor_sync(0xffffffffu, v, 2);
+}
+__device__ __forceinline__ double quad_min(double v) {
+    v = fmin(v, __shfl_xor_sync(0xffffffffu, v, 1));
+    return fmin(v, __shfl_xor_sync(0xffffffffu, v, 2));
+}
+
+}  // namespace qmccpw

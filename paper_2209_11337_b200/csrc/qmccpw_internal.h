@@ -121,6 +121,9 @@ cudaError_t launch_path_matrix(int construction, int d, int ld, double T, double
                                double* d_inv_sa, cudaStream_t st);
 cudaError_t launch_gpca_rotate(double* d_M, int ld, int d, double T, double omega, double sigma, double* d_a,
                                double* d_inv_sa, cudaStream_t st);
+cudaError_t launch_paths_x1(const PathArgs& args, int construction, cudaStream_t st, int* smem_out);
+cudaError_t launch_pca_w1(const PathArgs& args, cudaStream_t st, bool* handled);  // handled = false: d not tiled
+cudaError_t launch_pca_x1(const PathArgs& args, cudaStream_t st, bool* handled);
 cudaError_t launch_paths(const PathArgs& args, int construction, int conditioning, int method, cudaStream_t st,
                          int* smem_bytes_out);
 cudaError_t launch_reduce_cells(const double* d_partials, int stride, uint32_t rep_begin, uint32_t rep_end,

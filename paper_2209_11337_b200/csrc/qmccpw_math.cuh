@@ -155,7 +155,7 @@ __device__ __forceinline__ void fast_exp_x2(double xa, double xb, double& ra, do
     rb = __hiloint2double(__double2hiint(pb) + (nb << 20), __double2loint(pb));
 }
 
-__device__ __noinline__ double icdf_tail_poly(double w) {
+static __device__ __noinline__ double icdf_tail_poly(double w) {
     const double v = sqrt(w) - ICDF_TAIL_CENTER;
     double p = ICDF_TAIL[24];
 #pragma unroll

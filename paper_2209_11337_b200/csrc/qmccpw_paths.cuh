@@ -1,0 +1,539 @@
+// qmccpw_paths.cuh -- the fused path kernel (STD / BB / PCA-fallback x W1 / X1 x
+// QMC / LR / MC / MC+AV) and its launcher template; instantiated by
+// qmccpw_paths_w1.cu and qmccpw_paths_x1.cu (separate translation units so the
+// build compiles them in parallel).
+#pragma once
+#include "qmccpw_device.cuh"
+
+namespace qmccpw {
+
+#ifndef QMCCPW_BB_MINB
+#define QMCCPW_BB_MINB 8
+#endif
+#ifndef QMCCPW_STD_MINB
+#define QMCCPW_STD_MINB 6
+#endif
+// resident blocks per SM the register allocator must allow (128 threads each); 0 = ptxas'
+// own choice.  Measured on C4 (ms/step): BB-W1 34.3 (ptxas, 96 regs) / 33.8 (7) / 33.4
+// (8: 64 regs, a few spills to L1); STD-W1 33.1 (4) / 31.9 (5) / 31.2 (6)
+template <int CONSTR, int COND, int METHOD>
+constexpr int paths_min_blocks() {
+    return (COND == kW1 && METHOD == kQmc) ? (CONSTR == kBB ? QMCCPW_BB_MINB : CONSTR == kStd ? QMCCPW_STD_MINB : 0) : 0;
+}
+// OWEN: nested scrambling of the Sobol' coordinates (row f4) -- a template flag so
+// that the other randomisations pay nothing for it (measured 0.5-4 % as a runtime test)
+template <int CONSTR, int COND, int METHOD, bool OWEN>
+__global__ void __launch_bounds__(128, paths_min_blocks<CONSTR, COND, METHOD>())
+    paths_kernel(const PathArgs P) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    const int tpb_log2 = P.tpb_log2;
+    const int tpb = 1 << tpb_log2;
+    const int tid = threadIdx.x;
+    const int d = P.d;
+    const uint64_t cell = P.cell_begin + blockIdx.x;
+    const uint32_t rep_local = (uint32_t)(cell / P.cells_per_rep);
+    const uint64_t blk = cell % P.cells_per_rep;
+    const uint64_t i0 = blk * (uint64_t)kCellPoints;
+    const int ppt = kCellPoints >> tpb_log2;
+    constexpr bool kNeedBuf = (METHOD == kQmc) && (CONSTR == kPca || COND == kX1);
+    constexpr bool kTwoBuf = (METHOD == kQmc) && (CONSTR == kPca && COND == kX1);
+    constexpr bool kWarpMma = (METHOD == kQmc) && (CONSTR == kPca && COND == kW1);
+
+    // shared memory carve-up (8-byte aligned first):
+    //   buf0, buf1 [d][tpb] | vt [d][32] | sh [d] | G [d][32] | pad | HW [2][2][nw][d] (>= 1 KB)
+    // the reduction scratch red [4 warps][32] aliases HW after the point loop; the
+    // centred sums live in one register per lane (warp_slot_sums).
+    const int nw = tpb >> 5;
+    const int n_acc = P.n_opt * 8;
+    const int lane = tid & 31;
+    double* buf0 = reinterpret_cast<double*>(smem_raw);
+    double* buf1 = buf0 + (kWarpMma ? (size_t)P.M_ld * (tpb + 8) : (kNeedBuf ? (size_t)d * tpb : 0));
+    uint32_t* vt = reinterpret_cast<uint32_t*>(buf1 + (kTwoBuf ? (size_t)d * tpb : 0));
+    uint32_t* sh = vt + (METHOD == kQmc ? (size_t)d * 32 : 0);
+    uint32_t* G = sh + (METHOD == kQmc ? d : 0);
+    uint32_t* HW = G + (METHOD == kQmc ? (size_t)d * 32 : 0);
+    HW += ((uintptr_t)HW & 7) ? 1 : 0;
+    double* red = reinterpret_cast<double*>(HW);
+    const int hw_size = 2 * nw * d;
+
+    const uint64_t K0 = P.point_offset + i0;
+    const uint64_t Ab = K0 >> tpb_log2;
+    const uint64_t kt = K0 + (uint64_t)tid;
+    SobolBlock sob{G, HW, d, nw, (int)(kt & 31), (int)((kt >> 5) & (uint64_t)(nw - 1)), (int)((kt >> tpb_log2) - Ab),
+                   OWEN ? sh : nullptr};
+    if (METHOD == kQmc) {
+        const uint32_t* src = P.vscr + (size_t)rep_local * d * 32;
+        for (int idx = tid; idx < d * 32; idx += tpb) vt[idx] = src[idx];
+        for (int idx = tid; idx < d; idx += tpb) sh[idx] = P.shift[(size_t)rep_local * d + idx];
+        __syncthreads();
+        sobol_build_g(vt, d, G, tid, tpb);
+    }
+    __shared__ double wacc[4 * 32];  // per-warp centred sums (tpb <= 128)
+    wacc[tid] = 0.0;
+    __syncwarp();
+    if (kWarpMma)  // zero X rows d..dp-1 (the padded K of the mma tiles)
+        for (int r = d; r < P.M_ld; ++r) buf0[(size_t)r * (tpb + 8) + tid] = 0.0;
+    unsigned unconverged = 0, ties = 0, npts = 0;
+
+    for (int a = 0; a < ppt; ++a) {
+        if (i0 + ((uint64_t)a << tpb_log2) >= P.n_points) break;  // block-uniform: ragged last cell
+        if (METHOD == kQmc) {
+            uint32_t* HWb = HW + (a & 1) * hw_size;  // double-buffered: one barrier per iteration
+            sobol_build_hw(vt, OWEN ? nullptr : sh, d, P.dim_begin, tpb_log2, nw, Ab + (uint64_t)a, HWb, tid, tpb);
+            __syncthreads();
+            sob.HW = HWb;
+        }
+        const uint64_t i = i0 + tid + ((uint64_t)a << tpb_log2);
+        // every lane runs (the warp reduction and the mma.sync tiles need the whole warp);
+        // lanes past N in a ragged last iteration evaluate a real lattice point whose
+        // result and counters are dropped
+        const bool valid = i < P.n_points;
+        const unsigned unconverged0 = unconverged, ties0 = ties;
+        npts += valid ? 1u : 0u;
+        const uint64_t k = P.point_offset + i;
+        double f[kMaxOpt][4];
+
+        if (METHOD == kLr) {
+            lr_path(P, P.rep_base + rep_local, k, f);
+        } else if (METHOD == kMc || METHOD == kMcAv) {
+            // MC-CPW and MC+AV-CPW: pseudo-random normals through the
+            // same W1 estimator; the antithetic path of -x has W~ -> -W~ (the constructions
+            // are linear), so one traversal feeds both accumulators.
+            const uint32_t rep = P.rep_base + rep_local;
+            W1Acc w1, w1m;
+            w1.reset();
+            w1m.reset();
+            if (CONSTR == kStd) {
+                double Wt = 0.0;
+                w1.push(P, 0, 0.0);
+                if (METHOD == kMcAv) w1m.push(P, 0, 0.0);
+#pragma unroll 1
+                for (int jq = 0; jq < d; jq += 4) {
+                    uint32_t c[4] = {(uint32_t)k, (uint32_t)(k >> 32), (uint32_t)(jq >> 2), (rep << 8) | 0x02u};
+                    philox4x32_10(c, (uint32_t)P.seed, (uint32_t)(P.seed >> 32));
+                    double xs[4];
+                    normal_from_u32_x2(c[0], c[1], xs[0], xs[1]);
+                    normal_from_u32_x2(c[2], c[3], xs[2], xs[3]);
+#pragma unroll
+                    for (int w = 0; w < 4; ++w) {
+                        const int j = jq + w;
+                        if (j >= 1 && j < d) {
+                            Wt = fma(P.sqrt_t1, xs[w], Wt);
+                            w1.push(P, j, Wt);
+                            if (METHOD == kMcAv) w1m.push(P, j, -Wt);
+                        }
+                    }
+                }
+            } else {
+                NormalFifo fifo;
+                fifo.reset();
+                int pos = 0;
+                auto dim_at = [&](int o) { return (int)P.bb_seq[pos + o]; };
+                auto draw = [&](int da, int db, double& xa, double& xb) { mc_normal_pair(P, rep, k, da, db, xa, xb); };
+                double stW[12];
+                int sp = 0;
+                stW[0] = P.sqrtT * fifo.next_from(draw, dim_at);
+                pos += 2;
+                double Wl = 0.0, W1 = 0.0, Wpend = 0.0;
+                const int m = P.bb_m;
+#pragma unroll 1
+                for (int j = 1; j <= d; ++j) {
+                    const int e = (j == 1) ? m : (__ffs(j - 1) - 1);
+                    double Wj;
+                    if (e == 0) {
+                        Wj = stW[sp];
+                        --sp;
+                    } else {
+                        double Wr = stW[sp];
+#pragma unroll 1
+                        for (int c = e - 1; c >= 0; --c) {
+                            const bool refill = fifo.have == 0;
+                            const double x = fifo.next_from(draw, dim_at);
+                            pos += refill ? 2 : 0;
+                            const double Wm = fma(P.bb_b[m - c], x, 0.5 * (Wl + Wr));
+                            if (c > 0) stW[++sp] = Wm;
+                            Wr = Wm;
+                        }
+                        Wj = Wr;
+                    }
+                    if (j == 1) W1 = Wj;
+                    if (j & 1) {
+                        Wpend = Wj - W1;
+                    } else {
+                        w1.push2(P, j - 2, Wpend, Wj - W1);
+                        if (METHOD == kMcAv) w1m.push2(P, j - 2, -Wpend, -(Wj - W1));
+                    }
+                    Wl = Wj;
+                }
+                if (d & 1) {
+                    w1.push(P, d - 1, Wpend);
+                    if (METHOD == kMcAv) w1m.push(P, d - 1, -Wpend);
+                }
+            }
+            if (P.has_lookback && w1.emax - w1.esec < 1e-12) ++ties;
+            tail_w1_all(P, w1, f);
+            if (METHOD == kMcAv) {
+                if (P.has_lookback && w1m.emax - w1m.esec < 1e-12) ++ties;
+                double fm[kMaxOpt][4];
+                tail_w1_all(P, w1m, fm);
+#pragma unroll
+                for (int o = 0; o < kMaxOpt; ++o)
+#pragma unroll
+                    for (int qq = 0; qq < 4; ++qq) f[o][qq] = 0.5 * (f[o][qq] + fm[o][qq]);
+            }
+        } else if (COND == kW1) {
+            W1Acc w1;
+            w1.reset();
+            if (CONSTR == kStd) {
+                // Alg. 3: W~ accumulates sqrt(dt) x_j for j >= 2; x_1 cancels in
+                // W - W(t_1).  Normals and exps two dates at a time.
+                double Wt = 0.0;
+                w1.push(P, 0, 0.0);
+                int j = 1;
+#pragma unroll 1
+                for (; j + 1 < d; j += 2) {
+                    double xa, xb;
+                    normal_from_u32_x2(sob.get(j), sob.get(j + 1), xa, xb);
+                    const double Wa = fma(P.sqrt_t1, xa, Wt);
+                    Wt = fma(P.sqrt_t1, xb, Wa);
+                    w1.push2(P, j, Wa, Wt);
+                }
+                if (j < d) {
+                    Wt = fma(P.sqrt_t1, normal_from_u32(sob.get(j)), Wt);
+                    w1.push(P, j, Wt);
+                }
+            } else if (CONSTR == kBB) {
+                // Alg. 4 generated in time order, two dates per step.  At odd
+                // j = 2p+1 the bridge descends e = 1 + ctz(p) levels (e = m at p = 0) from the
+                // interval (t_{j-1}, t_{j-1+2^e}]: midpoint mid = j-1+2^c (c = e-1..0) sits at
+                // level m-c, consumes the next Sobol' dimension of Alg. 4's order (bb_seq, built
+                // on the host), W(mid) = (W(l) + W(r))/2 + b_{m-c} x, and is pushed for c > 0.
+                // W(t_j) is the c = 0 midpoint; W(t_{j+1}) is then exactly the stack top.
+                NormalFifo fifo;
+                fifo.reset();
+                int pos = 0;
+                auto dim_at = [&](int o) { return (int)P.bb_seq[pos + o]; };
+                double stW[12];
+                int sp = 0;
+                stW[0] = P.sqrtT * fifo.next(sob, dim_at);
+                pos += 2;
+                const int m = P.bb_m;
+                if (d == 1) {
+                    w1.push(P, 0, 0.0);
+                } else {
+                    double Wl = 0.0, W1 = 0.0;
+#pragma unroll 1
+                    for (int pp = 0; pp < (d >> 1); ++pp) {
+                        const int e = (pp == 0) ? m : __ffs(pp);  // 1 + ctz(pp)
+                        double Wr = stW[sp];
+#pragma unroll 1
+                        for (int c = e - 1; c >= 0; --c) {
+                            const bool refill = fifo.have == 0;
+                            const double x = fifo.next(sob, dim_at);
+                            pos += refill ? 2 : 0;
+                            const double Wm = fma(P.bb_b[m - c], x, 0.5 * (Wl + Wr));
+                            if (c > 0) stW[++sp] = Wm;
+                            Wr = Wm;
+                        }
+                        const double Wodd = Wr, Weven = stW[sp];
+                        --sp;
+                        if (pp == 0) W1 = Wodd;
+                        w1.push2(P, 2 * pp, Wodd - W1, Weven - W1);
+                        Wl = Weven;
+                    }
+                }
+            } else {
+                // PCA: W = X M^T, the one dense contraction, on the FP64 tensor
+                // cores.  Each thread writes its path's normals as a column of X (shared
+                // memory, row stride tpb + 8 doubles: the 4 k-rows of an A fragment fall on
+                // disjoint bank halves); each warp then runs mma.sync.m8n8k4.f64 (SASS DMMA)
+                // over its 32 paths x dp times: A = X[k][path] (8 paths x 4 k), B = M[j][k]
+                // (4 k x 8 j, from L1), D = 8 paths x 8 j.  Lane (q = lane/4, r = lane%4) ends
+                // up holding W for paths 8 rt + q (rt = 0..3) at times jt + 2r + {0,1}; it
+                // accumulates those paths' S~ statistics, the quad reduces them, and the
+                // owning lane takes them over for the tail.
+                const int XS = tpb + 8;
+                const int dp = P.M_ld;
+                double* xc = buf0 + tid;
+                int kk = 0;
+#pragma unroll 1
+                for (; kk + 1 < d; kk += 2) {
+                    double xa, xc2;
+                    normal_from_u32_x2(sob.get(kk), sob.get(kk + 1), xa, xc2);
+                    xc[kk * XS] = xa;
+                    xc[(kk + 1) * XS] = xc2;
+                }
+                if (kk < d) xc[kk * XS] = normal_from_u32(sob.get(kk));
+                __syncwarp();
+                const int lane = tid & 31, q = lane >> 2, r4 = lane & 3;
+                const double* Xw = buf0 + (tid & ~31);
+                double sS[4], sI[4], em[4], es[4], ym[4], W1r[4];
+                int jm[4];
+#pragma unroll
+                for (int rt = 0; rt < 4; ++rt) {
+                    sS[rt] = 0.0; sI[rt] = 0.0; em[rt] = -CUDART_INF; es[rt] = -CUDART_INF; ym[rt] = 0.0;
+                    jm[rt] = 0x7fffffff; W1r[rt] = 0.0;
+                }
+#pragma unroll 1
+                for (int jt = 0; jt < dp; jt += 8) {
+                    double acc[4][2];
+#pragma unroll
+                    for (int rt = 0; rt < 4; ++rt) acc[rt][0] = acc[rt][1] = 0.0;
+                    const double* Mrow = P.M + (size_t)(jt + q) * dp + r4;
+                    const double* Xk = Xw + (size_t)r4 * XS + q;
+#pragma unroll 2
+                    for (int kt = 0; kt < dp; kt += 4) {
+                        const double bfrag = __ldg(Mrow + kt);
+                        const double* Xr = Xk + (size_t)kt * XS;
+#pragma unroll
+                        for (int rt = 0; rt < 4; ++rt) {
+                            const double afrag = Xr[8 * rt];
+                            asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+                                         : "+d"(acc[rt][0]), "+d"(acc[rt][1])
+                                         : "d"(afrag), "d"(bfrag));
+                        }
+                    }
+                    if (jt == 0) {
+#pragma unroll
+                        for (int rt = 0; rt < 4; ++rt) W1r[rt] = __shfl_sync(0xffffffffu, acc[rt][0], lane & ~3);
+                    }
+                    const int j0 = jt + 2 * r4;
+#pragma unroll
+                    for (int rt = 0; rt < 4; ++rt) {
+                        const double Wa = acc[rt][0] - W1r[rt], Wb = acc[rt][1] - W1r[rt];
+                        const double ta = (double)j0 * P.t1, tb = ta + P.t1;
+                        const double ea = fma(P.sigma, Wa, P.omega * ta), eb = fma(P.sigma, Wb, P.omega * tb);
+                        double Xa, Xb;
+                        fast_exp_x2(ea, eb, Xa, Xb);
+                        const double va = (j0 < d) ? 1.0 : 0.0, vb = (j0 + 1 < d) ? 1.0 : 0.0;
+                        const double Sa = P.S0 * Xa * va, Sb = P.S0 * Xb * vb;
+                        const double ya = fma(-P.sigma, ta, Wa), yb = fma(-P.sigma, tb, Wb);
+                        sS[rt] += Sa;
+                        sI[rt] = fma(Sa, ya, sI[rt]);
+                        sS[rt] += Sb;
+                        sI[rt] = fma(Sb, yb, sI[rt]);
+                        if (P.has_lookback) {
+                            const double eav = (j0 < d) ? ea : -CUDART_INF, ebv = (j0 + 1 < d) ? eb : -CUDART_INF;
+                            // lowest index wins ties (j0 < j0 + 1 < later tiles)
+                            bool gt = eav > em[rt];
+                            es[rt] = fmax(es[rt], gt ? em[rt] : eav);
+                            ym[rt] = gt ? ya : ym[rt];
+                            jm[rt] = gt ? j0 : jm[rt];
+                            em[rt] = gt ? eav : em[rt];
+                            gt = ebv > em[rt];
+                            es[rt] = fmax(es[rt], gt ? em[rt] : ebv);
+                            ym[rt] = gt ? yb : ym[rt];
+                            jm[rt] = gt ? j0 + 1 : jm[rt];
+                            em[rt] = gt ? ebv : em[rt];
+                        }
+                    }
+                }
+                __syncwarp();  // X may be overwritten by the next point only after every lane's mma
+                // quad reduction (lanes 4q..4q+3 hold disjoint j's of the same paths)
+#pragma unroll
+                for (int rt = 0; rt < 4; ++rt) {
+#pragma unroll
+                    for (int off = 1; off <= 2; off <<= 1) {
+                        sS[rt] += __shfl_xor_sync(0xffffffffu, sS[rt], off);
+                        sI[rt] += __shfl_xor_sync(0xffffffffu, sI[rt], off);
+                        if (P.has_lookback) {
+                            const double pe = __shfl_xor_sync(0xffffffffu, em[rt], off);
+                            const double pes = __shfl_xor_sync(0xffffffffu, es[rt], off);
+                            const double py = __shfl_xor_sync(0xffffffffu, ym[rt], off);
+                            const int pj = __shfl_xor_sync(0xffffffffu, jm[rt], off);
+                            const bool take = pe > em[rt] || (pe == em[rt] && pj < jm[rt]);
+                            es[rt] = fmax(fmax(es[rt], pes), fmin(em[rt], pe));
+                            em[rt] = take ? pe : em[rt];
+                            ym[rt] = take ? py : ym[rt];
+                            jm[rt] = take ? pj : jm[rt];
+                        }
+                    }
+                }
+                // hand path 8 rt + q's statistics to its owner lane (lane = 8 rt + q)
+                const int src = 4 * (lane & 7), mine = lane >> 3;
+#pragma unroll
+                for (int rt = 0; rt < 4; ++rt) {
+                    const double a0 = __shfl_sync(0xffffffffu, sS[rt], src);
+                    const double a1 = __shfl_sync(0xffffffffu, sI[rt], src);
+                    const double a2 = __shfl_sync(0xffffffffu, em[rt], src);
+                    const double a3 = __shfl_sync(0xffffffffu, es[rt], src);
+                    const double a4 = __shfl_sync(0xffffffffu, ym[rt], src);
+                    if (rt == mine) {
+                        w1.sumS = a0;
+                        w1.sumI = a1;
+                        w1.emax = a2;
+                        w1.esec = a3;
+                        w1.ymax = a4;
+                    }
+                }
+            }
+            if (P.has_lookback && w1.emax - w1.esec < 1e-12) ++ties;
+            tail_w1_all(P, w1, f);
+        } else {
+            // X1: c_j = ln S0 + omega t_j + sigma R_j, R = M x with x_1 := 0
+            double* cb = (CONSTR == kPca ? buf1 : buf0) + tid;
+            if (CONSTR == kStd) {
+                double R = 0.0;
+                cb[0] = P.lnS0 + P.omega * P.t1;
+                int j = 1;
+#pragma unroll 1
+                for (; j + 1 < d; j += 2) {
+                    double xa, xb2;
+                    normal_from_u32_x2(sob.get(j), sob.get(j + 1), xa, xb2);
+                    R = fma(P.sqrt_t1, xa, R);
+                    cb[j * tpb] = P.lnS0 + P.omega * (double)(j + 1) * P.t1 + P.sigma * R;
+                    R = fma(P.sqrt_t1, xb2, R);
+                    cb[(j + 1) * tpb] = P.lnS0 + P.omega * (double)(j + 2) * P.t1 + P.sigma * R;
+                }
+                if (j < d) {
+                    R = fma(P.sqrt_t1, normal_from_u32(sob.get(j)), R);
+                    cb[j * tpb] = P.lnS0 + P.omega * (double)(j + 1) * P.t1 + P.sigma * R;
+                }
+            } else if (CONSTR == kBB) {
+                // same time-order bridge with the terminal loading of x_1 removed (R = M x, x_1 := 0);
+                // normals in Alg. 4 order from bb_seq[1..]
+                NormalFifo fifo;
+                fifo.reset();
+                int pos = 1;
+                auto dim_at = [&](int o) { return (int)P.bb_seq[pos + o]; };
+                double stW[12];
+                int sp = 0;
+                stW[0] = 0.0;
+                double Wl = 0.0;
+                const int m = P.bb_m;
+#pragma unroll 1
+                for (int j = 1; j <= d; ++j) {
+                    const int e = (j == 1) ? m : (__ffs(j - 1) - 1);
+                    double Rj;
+                    if (e == 0) {
+                        Rj = stW[sp];
+                        --sp;
+                    } else {
+                        double Wr = stW[sp];
+#pragma unroll 1
+                        for (int c = e - 1; c >= 0; --c) {
+                            const bool refill = fifo.have == 0;
+                            const double x = fifo.next(sob, dim_at);
+                            pos += refill ? 2 : 0;
+                            const double Wm = fma(P.bb_b[m - c], x, 0.5 * (Wl + Wr));
+                            if (c > 0) stW[++sp] = Wm;
+                            Wr = Wm;
+                        }
+                        Rj = Wr;
+                    }
+                    cb[(j - 1) * tpb] = P.lnS0 + P.omega * (double)j * P.t1 + P.sigma * Rj;
+                    Wl = Rj;
+                }
+            } else {
+                double* xb = buf0 + tid;
+                int kk = 1;
+#pragma unroll 1
+                for (; kk + 1 < d; kk += 2) {
+                    double xa, xc;
+                    normal_from_u32_x2(sob.get(kk), sob.get(kk + 1), xa, xc);
+                    xb[kk * tpb] = xa;
+                    xb[(kk + 1) * tpb] = xc;
+                }
+                if (kk < d) xb[kk * tpb] = normal_from_u32(sob.get(kk));
+                int j = 0;
+#pragma unroll 1
+                for (; j + 1 < d; j += 2) {
+                    const double* Ma = P.M + (size_t)j * P.M_ld;
+                    const double* Mb = Ma + P.M_ld;
+                    double Ra = 0.0, Rb = 0.0;
+#pragma unroll 4
+                    for (int q = 1; q < d; ++q) {
+                        const double xq = xb[q * tpb];
+                        Ra = fma(__ldg(Ma + q), xq, Ra);
+                        Rb = fma(__ldg(Mb + q), xq, Rb);
+                    }
+                    cb[j * tpb] = P.lnS0 + P.omega * (double)(j + 1) * P.t1 + P.sigma * Ra;
+                    cb[(j + 1) * tpb] = P.lnS0 + P.omega * (double)(j + 2) * P.t1 + P.sigma * Rb;
+                }
+                if (j < d) {
+                    const double* Ma = P.M + (size_t)j * P.M_ld;
+                    double Ra = 0.0;
+                    for (int q = 1; q < d; ++q) Ra = fma(__ldg(Ma + q), xb[q * tpb], Ra);
+                    cb[j * tpb] = P.lnS0 + P.omega * (double)(j + 1) * P.t1 + P.sigma * Ra;
+                }
+            }
+            tail_x1_all(P, cb, tpb, f, unconverged);
+        }
+
+        if (!valid) {
+            unconverged = unconverged0;
+            ties = ties0;
+        }
+        if (P.path_out != nullptr && valid) {
+#pragma unroll
+            for (int o = 0; o < kMaxOpt; ++o)
+                if (o == P.hook_option)
+                    for (int q = 0; q < 4; ++q) P.path_out[i * 4 + q] = f[o][q];
+        }
+        warp_slot_sums(f, P, valid, lane, wacc + (tid >> 5) * 32);
+        (void)k;
+    }
+
+    block_epilogue(P, nullptr, wacc, red, n_acc, tpb, tid, cell, unconverged, ties, npts);
+}
+
+
+static size_t path_smem_bytes(const PathArgs& a, int constr, int cond, int method) {
+    const size_t tpb = (size_t)1 << a.tpb_log2, nw = tpb / 32;
+    const bool need_buf = method == kQmc && (constr == kPca || cond == kX1);
+    const bool two_buf = method == kQmc && constr == kPca && cond == kX1;
+    size_t b = 0;
+    if (method == kQmc && constr == kPca && cond == kW1) b += (size_t)a.M_ld * (tpb + 8) * sizeof(double);
+    else if (need_buf) b += (size_t)a.d * tpb * sizeof(double);
+    if (two_buf) b += (size_t)a.d * tpb * sizeof(double);
+    size_t hw = 0;
+    if (method == kQmc) {
+        b += ((size_t)a.d * 32 * 2 + a.d) * sizeof(uint32_t) + 4;  // vt, sh, G, alignment pad
+        hw = 2 * 2 * nw * a.d * sizeof(uint32_t);
+    }
+    const size_t red = 4 * 32 * sizeof(double);
+    return b + (hw > red ? hw : red);
+}
+
+template <int C, int K, int M, bool OW>
+static cudaError_t launch_paths_t(const PathArgs& args_in, cudaStream_t st, int* smem_out) {
+    // raise the dynamic-smem limit once per device (not on every call: it is a driver round trip)
+    static thread_local int set_for[64] = {0};
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (set_for[dev & 63] == 0) {
+        cudaError_t e = cudaFuncSetAttribute(paths_kernel<C, K, M, OW>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             200 * 1024);
+        if (e != cudaSuccess) return e;
+        set_for[dev & 63] = 1;
+    }
+    // block size: the candidate (128, 64, 32 threads) with the most resident warps per SM
+    // (registers and shared memory both counted by the occupancy calculator); a deterministic
+    // function of (mode, d, n_opt), so results stay independent of the GPU count.
+    PathArgs args = args_in;
+    int best_lg = -1, best_warps = -1;
+    for (int lg = 7; lg >= 5; --lg) {
+        args.tpb_log2 = lg;
+        const size_t smem = path_smem_bytes(args, C, K, M);
+        if (smem > 200 * 1024) continue;
+        int nb = 0;
+        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, paths_kernel<C, K, M, OW>, 1 << lg, smem) != cudaSuccess)
+            continue;
+        const int warps = nb * (1 << lg) / 32;
+        if (warps > best_warps) {
+            best_warps = warps;
+            best_lg = lg;
+        }
+    }
+    if (best_lg < 0) return cudaErrorInvalidConfiguration;
+    args.tpb_log2 = best_lg;
+    const size_t smem = path_smem_bytes(args, C, K, M);
+    if (smem_out) *smem_out = (int)smem;
+    const uint64_t nblocks = args.cell_end - args.cell_begin;
+    if (nblocks == 0) return cudaSuccess;
+    paths_kernel<C, K, M, OW><<<(unsigned)nblocks, 1 << args.tpb_log2, smem, st>>>(args);
+    ++launch_counter();
+    return cudaGetLastError();
+}
+
+}  // namespace qmccpw

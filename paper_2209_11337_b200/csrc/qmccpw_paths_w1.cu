@@ -1,0 +1,32 @@
+// qmccpw_paths_w1.cu -- path kernels with W1 conditioning (all methods) and the
+// launch_paths dispatcher (X1 kernels: qmccpw_paths_x1.cu; PCA on DMMA: qmccpw_pca_*.cu).
+#include "qmccpw_paths.cuh"
+
+namespace qmccpw {
+
+cudaError_t launch_paths(const PathArgs& args, int construction, int conditioning, int method, cudaStream_t st,
+                         int* smem_out) {
+    if (method == kLr) return launch_paths_t<kStd, kW1, kLr, false>(args, st, smem_out);
+    if (method == kMc) return construction == kBB ? launch_paths_t<kBB, kW1, kMc, false>(args, st, smem_out)
+                                                  : launch_paths_t<kStd, kW1, kMc, false>(args, st, smem_out);
+    if (method == kMcAv) return construction == kBB ? launch_paths_t<kBB, kW1, kMcAv, false>(args, st, smem_out)
+                                                    : launch_paths_t<kStd, kW1, kMcAv, false>(args, st, smem_out);
+    if (construction == kPca && method == kQmc && !(conditioning == kX1 && args.has_lookback)) {
+        // fragment-native tensor-core path for d <= 128 (the X1 lookback walks its envelope per thread)
+        bool handled = false;
+        cudaError_t e = conditioning == kW1 ? launch_pca_w1(args, st, &handled) : launch_pca_x1(args, st, &handled);
+        if (handled) return e;
+    }
+    if (conditioning == kX1) return launch_paths_x1(args, construction, st, smem_out);
+    const bool ow = args.owen != 0;
+    if (construction == kStd)
+        return ow ? launch_paths_t<kStd, kW1, kQmc, true>(args, st, smem_out)
+                  : launch_paths_t<kStd, kW1, kQmc, false>(args, st, smem_out);
+    if (construction == kBB)
+        return ow ? launch_paths_t<kBB, kW1, kQmc, true>(args, st, smem_out)
+                  : launch_paths_t<kBB, kW1, kQmc, false>(args, st, smem_out);
+    return ow ? launch_paths_t<kPca, kW1, kQmc, true>(args, st, smem_out)
+              : launch_paths_t<kPca, kW1, kQmc, false>(args, st, smem_out);
+}
+
+}  // namespace qmccpw

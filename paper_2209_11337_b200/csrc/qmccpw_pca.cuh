@@ -1,0 +1,373 @@
+// qmccpw_pca.cuh -- PCA paths on the FP64 tensor cores (fragment-native DMMA) and
+// its launcher templates; instantiated by qmccpw_pca_w1.cu and qmccpw_pca_x1.cu.
+#pragma once
+#include "qmccpw_device.cuh"
+
+namespace qmccpw {
+
+// ---------------------------------------------------------------------------
+// PCA on the FP64 tensor cores, fragment-native (no per-path shared memory).
+//
+// W = X M^T (or R = X M[:,1:]^T for X1) is the one dense contraction of the
+// path.  A warp works on its 32 points as 4 row tiles of 8 paths.
+// Lane (q = lane/4, r = lane%4) draws, for path 8 rt + q, exactly the normals
+// of its m8n8k4 A fragments -- x[path][4 f + r], f = 0..KF-1 -- straight from
+// the block's Sobol' tables (any lane can form any path's y_j), so X never goes
+// through shared memory.  mma.sync.m8n8k4.f64 (SASS DMMA) against B = M[j][k]
+// (L1) leaves lane (q, r) with W(t_j) of its path at j = 8 jt + 2 r + {0, 1}.
+//  * W1: the quad accumulates the S~ statistics of its path from those
+//    values, reduces them, and the owning lane runs the option tails.
+//  * X1: c_j stays in the quad's registers; Newton's sums over j are
+//    quad-reduced, so the threshold is solved by the 4 lanes together.
+// ---------------------------------------------------------------------------
+#ifndef QMCCPW_PCA_W1_MINB
+#define QMCCPW_PCA_W1_MINB 4
+#endif
+#ifndef QMCCPW_PCA_X1_MINB
+#define QMCCPW_PCA_X1_MINB 5
+#endif
+// d <= 64: shared memory allows 5 blocks/SM, so cap registers to match (measured on C4:
+// PCA-W1 72.4 -> 69.4 ms, PCA-X1 175 -> 165 ms); larger d is smem-limited anyway
+template <int COND, int KF>
+constexpr int pca_min_blocks() {
+    return KF > 16 ? 0 : (COND == kW1 ? QMCCPW_PCA_W1_MINB : QMCCPW_PCA_X1_MINB);
+}
+template <int COND, int KF, bool OWEN>
+__global__ void __launch_bounds__(128, pca_min_blocks<COND, KF>()) pca_kernel(const PathArgs P) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    constexpr int DP = 4 * KF;  // padded dimension (multiple of 8)
+    constexpr int JT = DP / 8;  // column tiles of 8 dates
+    const int tpb_log2 = P.tpb_log2, tpb = 1 << tpb_log2, tid = threadIdx.x, d = P.d;
+    const int lane = tid & 31, q = lane >> 2, r4 = lane & 3, wbase = tid & ~31;
+    const uint64_t cell = P.cell_begin + blockIdx.x;
+    const uint32_t rep_local = (uint32_t)(cell / P.cells_per_rep);
+    const uint64_t blk = cell % P.cells_per_rep;
+    const uint64_t i0 = blk * (uint64_t)kCellPoints;
+    const int ppt = kCellPoints >> tpb_log2;
+    const int nw = tpb >> 5;
+    const int n_acc = P.n_opt * 8;
+    // per-path accumulators in smem: X1 as scalars (one quad lane per path), W1 as (S1, S2) pairs
+    double* accs = reinterpret_cast<double*>(smem_raw);
+    double2* acc2 = reinterpret_cast<double2*>(smem_raw);
+    uint32_t* vt = reinterpret_cast<uint32_t*>(accs + (size_t)n_acc * tpb);
+    uint32_t* sh = vt + (size_t)d * 32;
+    uint32_t* G = sh + d;
+    uint32_t* HW = G + (size_t)d * 32;
+    HW += ((uintptr_t)HW & 7) ? 1 : 0;
+    double* red = reinterpret_cast<double*>(HW);
+    const int hw_size = 2 * nw * d;
+    const uint64_t K0 = P.point_offset + i0;
+    const uint64_t Ab = K0 >> tpb_log2;
+    {
+        const uint32_t* src = P.vscr + (size_t)rep_local * d * 32;
+        for (int idx = tid; idx < d * 32; idx += tpb) vt[idx] = src[idx];
+        for (int idx = tid; idx < d; idx += tpb) sh[idx] = P.shift[(size_t)rep_local * d + idx];
+        __syncthreads();
+        sobol_build_g(vt, d, G, tid, tpb);
+    }
+    for (int v = 0; v < n_acc; ++v) accs[v * tpb + tid] = 0.0;
+    __shared__ double wacc[4 * 32];  // per-warp centred sums (tpb <= 128)
+    wacc[tid] = 0.0;
+    __syncwarp();
+    unsigned unconverged = 0, ties = 0, npts = 0;
+    const double sg = P.sigma;
+
+    for (int a = 0; a < ppt; ++a) {
+        if (i0 + ((uint64_t)a << tpb_log2) >= P.n_points) break;  // block-uniform
+        uint32_t* HWb = HW + (a & 1) * hw_size;
+        sobol_build_hw(vt, OWEN ? nullptr : sh, d, 0, tpb_log2, nw, Ab + (uint64_t)a, HWb, tid, tpb);
+        __syncthreads();
+        // W1: statistics of this lane's own path, handed over by its quad after each row tile
+        W1Acc w1own;
+        w1own.reset();
+#pragma unroll 1
+        for (int rt = 0; rt < 4; ++rt) {
+            const int tp = wbase + 8 * rt + q;  // block slot of this quad's path
+            const uint64_t kp0 = K0 + (uint64_t)tp;
+            const uint64_t ip = i0 + (uint64_t)tp + ((uint64_t)a << tpb_log2);
+            const bool valid = ip < P.n_points;
+            const SobolBlock sp{G, HWb, d, nw, (int)(kp0 & 31), (int)((kp0 >> 5) & (uint64_t)(nw - 1)),
+                                (int)((kp0 >> tpb_log2) - Ab), OWEN ? sh : nullptr};
+            // A fragments: x[path][4 f + r4]
+            double afr[KF];
+#pragma unroll
+            for (int f = 0; f < KF; f += 2) {
+                const int ja = 4 * f + r4, jb = 4 * (f + 1) + r4;
+                double xa, xb;
+                normal_from_u32_x2(sp.get(ja < d ? ja : d - 1), sp.get(jb < d ? jb : d - 1), xa, xb);
+                afr[f] = (ja < d && !(COND == kX1 && ja == 0)) ? xa : 0.0;
+                afr[f + 1] = (jb < d && !(COND == kX1 && jb == 0)) ? xb : 0.0;
+            }
+            double cv[2 * JT];  // W(t_j) (W1) or c_j (X1) at j = 8 jt + 2 r4 + e
+            double W1v = 0.0;
+#pragma unroll
+            for (int jt = 0; jt < JT; ++jt) {
+                double acc0 = 0.0, acc1 = 0.0;
+                const double* Mrow = P.M + (size_t)(8 * jt + q) * DP + r4;
+#pragma unroll
+                for (int f = 0; f < KF; ++f) {
+                    const double bfrag = __ldg(Mrow + 4 * f);
+                    asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+                                 : "+d"(acc0), "+d"(acc1)
+                                 : "d"(afr[f]), "d"(bfrag));
+                }
+                cv[2 * jt] = acc0;
+                cv[2 * jt + 1] = acc1;
+            }
+            if (COND == kW1) {
+                W1v = __shfl_sync(0xffffffffu, cv[0], lane & ~3);  // W(t_1) of this path
+                double sS = 0.0, sI = 0.0, em = -CUDART_INF, es = -CUDART_INF, ym = 0.0;
+#pragma unroll
+                for (int jt = 0; jt < JT; ++jt) {
+                    const int j0 = 8 * jt + 2 * r4;
+                    const double Wa = cv[2 * jt] - W1v, Wb = cv[2 * jt + 1] - W1v;
+                    const double ta = (double)j0 * P.t1, tb = ta + P.t1;
+                    const double ea = fma(sg, Wa, P.omega * ta), eb = fma(sg, Wb, P.omega * tb);
+                    double Xa, Xb;
+                    fast_exp_x2(ea, eb, Xa, Xb);
+                    const double Sa = (j0 < d) ? P.S0 * Xa : 0.0, Sb = (j0 + 1 < d) ? P.S0 * Xb : 0.0;
+                    const double ya = fma(-sg, ta, Wa), yb = fma(-sg, tb, Wb);
+                    sS += Sa;
+                    sI = fma(Sa, ya, sI);
+                    sS += Sb;
+                    sI = fma(Sb, yb, sI);
+                    if (P.has_lookback) {
+                        const double eav = (j0 < d) ? ea : -CUDART_INF, ebv = (j0 + 1 < d) ? eb : -CUDART_INF;
+                        bool gt = eav > em;
+                        es = fmax(es, gt ? em : eav);
+                        ym = gt ? ya : ym;
+                        em = gt ? eav : em;
+                        gt = ebv > em;
+                        es = fmax(es, gt ? em : ebv);
+                        ym = gt ? yb : ym;
+                        em = gt ? ebv : em;
+                    }
+                }
+                // quad reduction (the 4 lanes hold disjoint dates of the same path)
+                sS = quad_sum(sS);
+                sI = quad_sum(sI);
+                if (P.has_lookback) {
+#pragma unroll
+                    for (int off = 1; off <= 2; off <<= 1) {
+                        const double pe = __shfl_xor_sync(0xffffffffu, em, off);
+                        const double pes = __shfl_xor_sync(0xffffffffu, es, off);
+                        const double py = __shfl_xor_sync(0xffffffffu, ym, off);
+                        const bool take = pe > em;  // an exact tie is a near-tie either way
+                        es = fmax(fmax(es, pes), fmin(em, pe));
+                        em = take ? pe : em;
+                        ym = take ? py : ym;
+                    }
+                }
+                // owner of path 8 rt + q is lane 8 rt + q: it reads lane 4 (its q) of this row tile
+                const int src = 4 * (lane & 7);
+                const double a0 = __shfl_sync(0xffffffffu, sS, src);
+                const double a1 = __shfl_sync(0xffffffffu, sI, src);
+                const double a2 = __shfl_sync(0xffffffffu, em, src);
+                const double a3 = __shfl_sync(0xffffffffu, es, src);
+                const double a4 = __shfl_sync(0xffffffffu, ym, src);
+                if ((lane >> 3) == rt) {
+                    w1own.sumS = a0;
+                    w1own.sumI = a1;
+                    w1own.emax = a2;
+                    w1own.esec = a3;
+                    w1own.ymax = a4;
+                }
+            } else {
+                // X1: c_j = ln S0 + omega t_j + sigma R_j, then one Newton solve per strike group
+#pragma unroll
+                for (int jt = 0; jt < JT; ++jt) {
+                    const int j0 = 8 * jt + 2 * r4;
+                    cv[2 * jt] = fma(sg, cv[2 * jt], fma(P.omega, (double)(j0 + 1) * P.t1, P.lnS0));
+                    cv[2 * jt + 1] = fma(sg, cv[2 * jt + 1], fma(P.omega, (double)(j0 + 2) * P.t1, P.lnS0));
+                }
+                double f[kMaxOpt][4];
+#pragma unroll
+                for (int o = 0; o < kMaxOpt; ++o) {
+                    if (o >= P.n_opt) break;
+                    if (P.tail_leader[o] != o) continue;
+                    const double lnK = P.lnK[o], lndK = P.lndK[o];
+                    // bracket [min_j (lnK - c_j)/(sigma a_j), min_j (ln dK - c_j)/(sigma a_j)] and mean c
+                    double ulo = CUDART_INF, uhi = CUDART_INF, sumc = 0.0;
+#pragma unroll
+                    for (int v = 0; v < 2 * JT; ++v) {
+                        const int j = 8 * (v >> 1) + 2 * r4 + (v & 1);
+                        if (j < d) {
+                            const double isa = __ldg(P.inv_sa + j);
+                            ulo = fmin(ulo, (lnK - cv[v]) * isa);
+                            uhi = fmin(uhi, (lndK - cv[v]) * isa);
+                            sumc += cv[v];
+                        }
+                    }
+                    ulo = quad_min(ulo);
+                    uhi = quad_min(uhi);
+                    sumc = quad_sum(sumc);
+                    double u = fmin(uhi, (lnK - sumc / d) / (sg * P.mean_a));
+                    bool conv = false;
+#pragma unroll 1
+                    for (int it = 0; it < kNewtonMax; ++it) {
+                        double S = 0.0, SA = 0.0;
+#pragma unroll
+                        for (int jt = 0; jt < JT; ++jt) {
+                            const int j0 = 8 * jt + 2 * r4;
+                            const double aa = (j0 < d) ? __ldg(P.a + j0) : 0.0;
+                            const double ab = (j0 + 1 < d) ? __ldg(P.a + j0 + 1) : 0.0;
+                            double Ea, Eb;
+                            fast_exp_x2(fma(sg * aa, u, cv[2 * jt]), fma(sg * ab, u, cv[2 * jt + 1]), Ea, Eb);
+                            Ea = (j0 < d) ? Ea : 0.0;
+                            Eb = (j0 + 1 < d) ? Eb : 0.0;
+                            S += Ea;
+                            SA = fma(aa, Ea, SA);
+                            S += Eb;
+                            SA = fma(ab, Eb, SA);
+                        }
+                        S = quad_sum(S);
+                        SA = quad_sum(SA);
+                        const double h = fast_log(S) - lndK;
+                        const double du = h * S / (sg * SA);
+                        conv = !valid || fabs(du) <= 1e-13 * fmax(1.0, fabs(u));
+                        u = fmin(fmax(u - du, ulo), uhi);
+                        if (it + 1 >= kNewtonIt && __all_sync(0xffffffffu, conv)) break;
+                    }
+                    if (r4 == 0 && valid && !conv) ++unconverged;
+                    double Dst = 0.0, Qst = 0.0, Vst = 0.0, sumW = 0.0, sumWv = 0.0;
+                    const bool need_arith = P.x1_need_arith[o] != 0;
+#pragma unroll
+                    for (int jt = 0; jt < JT; ++jt) {
+                        const int j0 = 8 * jt + 2 * r4;
+                        const double aa = (j0 < d) ? __ldg(P.a + j0) : 0.0;
+                        const double ab = (j0 + 1 < d) ? __ldg(P.a + j0 + 1) : 0.0;
+                        const double ta = (double)(j0 + 1) * P.t1, tb = ta + P.t1;
+                        const double ca = cv[2 * jt], cb2 = cv[2 * jt + 1];
+                        const double Ra = (ca - P.lnS0 - P.omega * ta) * P.inv_sigma;
+                        const double Rb = (cb2 - P.lnS0 - P.omega * tb) * P.inv_sigma;
+                        double Ea, Eb;
+                        fast_exp_x2(fma(sg * aa, u, ca), fma(sg * ab, u, cb2), Ea, Eb);
+                        Ea = (j0 < d) ? Ea : 0.0;
+                        Eb = (j0 + 1 < d) ? Eb : 0.0;
+                        Dst = fma(aa, Ea, Dst);
+                        Qst = fma(aa * aa, Ea, Qst);
+                        Vst = fma(Ea, Ra - sg * ta + aa * u, Vst);
+                        Dst = fma(ab, Eb, Dst);
+                        Qst = fma(ab * ab, Eb, Qst);
+                        Vst = fma(Eb, Rb - sg * tb + ab * u, Vst);
+                        if (need_arith) {
+                            double wa, wb, Pa, Pb, pa, pb;
+                            fast_exp_x2(fma(0.5 * sg * sg * aa, aa, ca), fma(0.5 * sg * sg * ab, ab, cb2), wa, wb);
+                            phibar_phi_x2(u - sg * aa, u - sg * ab, Pa, Pb, pa, pb);
+                            wa = (j0 < d) ? wa : 0.0;
+                            wb = (j0 + 1 < d) ? wb : 0.0;
+                            sumW = fma(wa, Pa, sumW);
+                            sumWv = fma(wa * (Ra - sg * ta + sg * aa * aa), Pa, sumWv);
+                            sumW = fma(wb, Pb, sumW);
+                            sumWv = fma(wb * (Rb - sg * tb + sg * ab * ab), Pb, sumWv);
+                        }
+                    }
+                    const X1Sums xs{u, quad_sum(Dst), quad_sum(Qst), quad_sum(Vst), quad_sum(sumW), quad_sum(sumWv)};
+#pragma unroll
+                    for (int o2 = 0; o2 < kMaxOpt; ++o2)
+                        if (o2 < P.n_opt && P.tail_leader[o2] == o) x1_outputs(P, o2, xs, f[o2]);
+                }
+                if (r4 == 0 && valid) {  // one lane per path records it
+                    ++npts;
+                    if (P.path_out != nullptr) {
+#pragma unroll
+                        for (int o = 0; o < kMaxOpt; ++o)
+                            if (o == P.hook_option)
+                                for (int qq = 0; qq < 4; ++qq) P.path_out[ip * 4 + qq] = f[o][qq];
+                    }
+#pragma unroll
+                    for (int o = 0; o < kMaxOpt; ++o) {
+                        if (o < P.n_opt) {
+#pragma unroll
+                            for (int qq = 0; qq < 4; ++qq) {
+                                const double y = f[o][qq] - P.piv[o][qq];
+                                double* a1 = accs + (size_t)(o * 8 + qq * 2) * tpb + tp;
+                                a1[0] += y;
+                                a1[tpb] = fma(y, y, a1[tpb]);
+                            }
+                        }
+                    }
+                }
+            }
+        }
+        if (COND == kW1) {
+            const W1Acc& w1 = w1own;
+            const uint64_t i = i0 + tid + ((uint64_t)a << tpb_log2);
+            const bool valid = i < P.n_points;  // all lanes run: the warp reduction needs them
+            npts += valid ? 1u : 0u;
+            if (valid && P.has_lookback && w1.emax - w1.esec < 1e-12) ++ties;
+            double f[kMaxOpt][4];
+            tail_w1_all(P, w1, f);
+            if (P.path_out != nullptr && valid) {
+#pragma unroll
+                for (int o = 0; o < kMaxOpt; ++o)
+                    if (o == P.hook_option)
+                        for (int qq = 0; qq < 4; ++qq) P.path_out[i * 4 + qq] = f[o][qq];
+            }
+            thread_acc2(f, P, valid, acc2, tpb, tid);
+        }
+    }
+    if (COND == kW1) acc2_to_wacc(P, acc2, wacc, tpb, tid);
+    block_epilogue(P, COND == kX1 ? accs : nullptr, wacc, red, n_acc, tpb, tid, cell, unconverged, ties, npts);
+}
+
+static size_t pca_smem_bytes(const PathArgs& a) {
+    const size_t tpb = (size_t)1 << a.tpb_log2, nw = tpb / 32;
+    size_t b = (size_t)a.n_opt * 8 * tpb * sizeof(double);
+    b += ((size_t)a.d * 32 * 2 + a.d) * sizeof(uint32_t) + 4;
+    const size_t hw = 2 * 2 * nw * a.d * sizeof(uint32_t), red = 4 * 32 * sizeof(double);
+    return b + (hw > red ? hw : red);
+}
+
+template <int K, int KF, bool OW>
+static cudaError_t launch_pca_t(const PathArgs& args_in, cudaStream_t st) {
+    static thread_local int set_for[64] = {0};
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (set_for[dev & 63] == 0) {
+        cudaError_t e = cudaFuncSetAttribute(pca_kernel<K, KF, OW>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+        if (e != cudaSuccess) return e;
+        set_for[dev & 63] = 1;
+    }
+    PathArgs args = args_in;
+    int best_lg = -1, best_warps = -1;
+    for (int lg = 7; lg >= 5; --lg) {
+        args.tpb_log2 = lg;
+        const size_t smem = pca_smem_bytes(args);
+        if (smem > 200 * 1024) continue;
+        int nb = 0;
+        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, pca_kernel<K, KF, OW>, 1 << lg, smem) != cudaSuccess) continue;
+        if (nb * (1 << lg) / 32 > best_warps) {
+            best_warps = nb * (1 << lg) / 32;
+            best_lg = lg;
+        }
+    }
+    if (best_lg < 0) return cudaErrorInvalidConfiguration;
+    args.tpb_log2 = best_lg;
+    const uint64_t nblocks = args.cell_end - args.cell_begin;
+    if (nblocks == 0) return cudaSuccess;
+    pca_kernel<K, KF, OW><<<(unsigned)nblocks, 1 << best_lg, pca_smem_bytes(args), st>>>(args);
+    ++launch_counter();
+    return cudaGetLastError();
+}
+
+template <int K, bool OW>
+static cudaError_t launch_pca(const PathArgs& args, cudaStream_t st, bool* handled) {
+    *handled = true;
+    switch (args.M_ld) {
+    case 8: return launch_pca_t<K, 2, OW>(args, st);
+    case 16: return launch_pca_t<K, 4, OW>(args, st);
+    case 24: return launch_pca_t<K, 6, OW>(args, st);
+    case 32: return launch_pca_t<K, 8, OW>(args, st);
+    case 40: return launch_pca_t<K, 10, OW>(args, st);
+    case 48: return launch_pca_t<K, 12, OW>(args, st);
+    case 56: return launch_pca_t<K, 14, OW>(args, st);
+    case 64: return launch_pca_t<K, 16, OW>(args, st);
+    case 96: return launch_pca_t<K, 24, OW>(args, st);
+    case 128: return launch_pca_t<K, 32, OW>(args, st);
+    default: *handled = false; return cudaSuccess;
+    }
+}
+
+
+}  // namespace qmccpw

@@ -1,0 +1,10 @@
+// qmccpw_pca_w1.cu -- PCA paths on DMMA tiles, W1 conditioning (d <= 128).
+#include "qmccpw_pca.cuh"
+
+namespace qmccpw {
+
+cudaError_t launch_pca_w1(const PathArgs& args, cudaStream_t st, bool* handled) {
+    return args.owen ? launch_pca<kW1, true>(args, st, handled) : launch_pca<kW1, false>(args, st, handled);
+}
+
+}  // namespace qmccpw
