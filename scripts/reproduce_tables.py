@@ -4,7 +4,8 @@ Tables 1-3: VRF = sigma_LR^2 / sigma_method^2 of delta,
 vega, gamma for LR+MC, MC-CPW, MC+AV-CPW, QMC-CPW (STD) and QMC+BB-CPW (BB),
 P = 2^15 paths, L = 500 runs (sigma with divisor L), S0 = 100,
 sigma = 0.2, r = 0.1, T = 1, K in {90, 100, 110}, d in {64, 256} (P:654);
-plus this build's PCA-W1 and PCA-X1 (the paper's stated future work).
+plus this build's rows (marked "ours", d = 64): Owen scrambling (f4), PCA-W1, PCA-X1
+and GPCA-X1 (f3; the paper's stated future work).
 
 Figures 3-11: the run-to-run error sigma of each Greek against
 P = 2^12 .. 2^19 at d = 256, L = 500.
@@ -51,15 +52,17 @@ PAPER = {  # (option, K, d) -> {method: (delta, vega, gamma)}; Tables 1
     },
 }
 OPT = {"arith": 0, "binary": 1, "lookback": 2}
-METHODS = {  # name -> (method, construction, conditioning)
-    "LR+MC": (1, 0, 0), "MC-CPW": (2, 0, 0), "MC+AV-CPW": (3, 0, 0), "QMC-CPW": (0, 0, 0), "QMC+BB-CPW": (0, 1, 0),
-    "PCA-W1 (ours)": (0, 2, 0), "PCA-X1 (ours)": (0, 2, 1),
+METHODS = {  # name -> (method, construction, conditioning, randomization)
+    "LR+MC": (1, 0, 0, 0), "MC-CPW": (2, 0, 0, 0), "MC+AV-CPW": (3, 0, 0, 0), "QMC-CPW": (0, 0, 0, 0),
+    "QMC+BB-CPW": (0, 1, 0, 0),
+    "QMC+BB-CPW Owen (ours)": (0, 1, 0, 4), "PCA-W1 (ours)": (0, 2, 0, 0), "PCA-X1 (ours)": (0, 2, 1, 0),
+    "PCA-X1 Owen (ours)": (0, 2, 1, 4), "GPCA-X1 (ours)": (0, 3, 1, 0),
 }
 
 
 def sigma_run(option, K, d, P, L, method):
-    m, c, k = METHODS[method]
-    cfg = q.config(method=m, construction=c, conditioning=k, device=0)
+    m, c, k, rz = METHODS[method]
+    cfg = q.config(method=m, construction=c, conditioning=k, randomization=rz, device=0)
     r = q.qmccpw_price_greeks(OPT[option], q.params(K=float(K), d=d), P, L, cfg)
     return np.array(r.sigma_run[:]), np.array(r.mean[:])
 
