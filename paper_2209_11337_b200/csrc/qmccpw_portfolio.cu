@@ -10,11 +10,15 @@ namespace qmccpw {
 //    accumulates its S~ statistics (S~_A, I_A, S~_max, I_max), quad-reduced and
 //    staged in shared memory.  Exps: families x d per point, shared by all
 //    options of a family.
-//  Phase B: thread t owns options t, t + tpb, ...; for each it runs only the
-//    per-option tail (psi, Phibar, phi, four outputs)
-//    over the block's staged points, accumulating in registers.
+//  Phase B: thread t owns options t, t + tpb, ...; it runs two of them at a time
+//    (independent chains for ILP) through the per-option tail (psi, Phibar, phi,
+//    four outputs) over the block's staged points, with
+//    per-option constants instead of divisions, accumulating in registers and
+//    then into the cell's partial row in global memory (read-modify-write by the
+//    owning thread only: deterministic, and no 64 KB of per-option smem, so two
+//    blocks fit per SM).
 // ---------------------------------------------------------------------------
-constexpr int kStatW = 7;  // staged per (point, family): SA, lnSA, IA, Smax, lnSmax, Imax, near-tie flag
+constexpr int kStatW = 8;  // staged per (point, family): SA, lnSA, IA, IA/SA, Smax, lnSmax, Imax, near-tie flag
 
 template <int KF, bool OWEN>
 __global__ void __launch_bounds__(128) portfolio_kernel(const PortfolioArgs P) {
@@ -30,9 +34,10 @@ __global__ void __launch_bounds__(128) portfolio_kernel(const PortfolioArgs P) {
     const uint64_t i0 = blk * (uint64_t)kCellPoints;
     const int ppt = kCellPoints >> tpb_log2;
     const int nw = tpb >> 5;
-    // smem: acc [8][nopt] | stats [tpb][nfam][kStatW] | vt | sh | G | HW
-    double* accs = reinterpret_cast<double*>(smem_raw);
-    double* stats = accs + (size_t)8 * nopt;
+    // smem: stats [tpb][nfam][kStatW] | vt | sh | G | HW
+    double* stats = reinterpret_cast<double*>(smem_raw);
+    double* prow = P.partials + (size_t)cell * P.partial_stride;  // this cell's row: [nopt][8] + 3 counters
+    const double inv_d = 1.0 / (double)d;
     uint32_t* vt = reinterpret_cast<uint32_t*>(stats + (size_t)tpb * nfam * kStatW);
     uint32_t* sh = vt + (size_t)d * 32;
     uint32_t* G = sh + d;
@@ -46,7 +51,9 @@ __global__ void __launch_bounds__(128) portfolio_kernel(const PortfolioArgs P) {
         const uint32_t* src = P.vscr + (size_t)rep_local * d * 32;
         for (int idx = tid; idx < d * 32; idx += tpb) vt[idx] = src[idx];
         for (int idx = tid; idx < d; idx += tpb) sh[idx] = P.shift[(size_t)rep_local * d + idx];
-        for (int idx = tid; idx < 8 * nopt; idx += tpb) accs[idx] = 0.0;
+        for (int o = tid; o < nopt; o += tpb)  // zeroed by the thread that will own the option
+#pragma unroll
+            for (int v = 0; v < 8; ++v) prow[o * 8 + v] = 0.0;
         __syncthreads();
         sobol_build_g(vt, d, G, tid, tpb);
     }
@@ -137,17 +144,18 @@ __global__ void __launch_bounds__(128) portfolio_kernel(const PortfolioArgs P) {
                     }
                 }
                 if (r4 == 0) {
-                    const double SA = sS / (double)d, Smax = P.has_lookback ? P.S0 * fast_exp(em) : SA;
+                    const double SA = sS * inv_d, Smax = P.has_lookback ? P.S0 * fast_exp(em) : SA;
                     double lnSA, lnSmax;
                     fast_log_x2(SA, Smax, lnSA, lnSmax);
                     double* st = stats + ((size_t)tp * nfam + fi) * kStatW;
                     st[0] = SA;
                     st[1] = lnSA;
-                    st[2] = sI / (double)d;
-                    st[3] = Smax;
-                    st[4] = lnSmax;
-                    st[5] = Smax * ym;
-                    st[6] = (P.has_lookback && em - es < 1e-12) ? 1.0 : 0.0;
+                    st[2] = sI * inv_d;
+                    st[3] = sI / sS;  // I_A / S~_A (binary vega)
+                    st[4] = Smax;
+                    st[5] = lnSmax;
+                    st[6] = Smax * ym;
+                    st[7] = (P.has_lookback && em - es < 1e-12) ? 1.0 : 0.0;
                 }
             }
         }
@@ -156,57 +164,100 @@ __global__ void __launch_bounds__(128) portfolio_kernel(const PortfolioArgs P) {
         const uint64_t ib = i0 + ((uint64_t)a << tpb_log2);
         const int np = (int)((P.n_points - ib) < (uint64_t)tpb ? (P.n_points - ib) : (uint64_t)tpb);
         if (tid < np) ++npts;
-#pragma unroll 1
-        for (int o = tid; o < nopt; o += tpb) {
+        // per-option constants (P:396-414, P:544-600 with the divisions hoisted)
+        struct OptC {
+            const double* st;  // stats of the option's family, point 0
+            int lb, bin;
+            double c_lnK, c_s, inv_s, K, D, Afac, sqrt_t1, inv_sigma, c1, c3;
+            double piv[4];
+        };
+        auto load_opt = [&](int o, OptC& c) {
             const PortfolioOption op = P.opts[o];
             const Family& F = P.fam[op.family];
-            const bool lb = op.type == kLookback, bin = op.type == kBinary;
-            const double K = op.K, D = F.Dfac, S0 = P.S0;
-            double s1[4] = {0, 0, 0, 0}, s2[4] = {0, 0, 0, 0};
+            const double inv_S0 = 1.0 / P.S0;
+            c.st = stats + (size_t)op.family * kStatW;
+            c.lb = op.type == kLookback;
+            c.bin = op.type == kBinary;
+            c.c_lnK = op.lnK - F.omega * F.t1;
+            c.c_s = F.s;
+            c.inv_s = F.inv_s;
+            c.K = op.K;
+            c.D = F.Dfac;
+            c.Afac = F.Afac;
+            c.sqrt_t1 = F.sqrt_t1;
+            c.inv_sigma = F.inv_sigma;
+            c.c1 = c.bin ? F.Dfac * F.inv_s * inv_S0 : F.Afac * inv_S0;                      // delta factor
+            c.c3 = (c.bin ? F.Dfac : op.K * F.Dfac) * F.inv_s * inv_S0 * inv_S0;            // gamma factor
+            for (int qq = 0; qq < 4; ++qq) c.piv[qq] = op.piv[qq];
+        };
+        // one point of one option: the four centred outputs
+        auto tail = [&](const OptC& c, const double* st, double Q0, double Q1, double ph, double psi, double f[4]) {
+            if (c.bin) {
+                f[0] = c.D * Q0;
+                f[1] = c.c1 * ph;
+                f[2] = c.D * ph * (st[3] * c.inv_s + psi * c.inv_sigma - c.sqrt_t1);
+                f[3] = c.c3 * ph * (psi * c.inv_s - 1.0);
+            } else {
+                const double stat = c.lb ? st[4] : st[0], I = c.lb ? st[6] : st[2];
+                f[0] = c.Afac * stat * Q1 - c.D * c.K * Q0;
+                f[1] = c.c1 * stat * Q1;
+                f[2] = c.Afac * Q1 * I + c.K * c.D * ph * c.sqrt_t1;
+                f[3] = c.c3 * ph;
+            }
+        };
+        const int fstride = nfam * kStatW;  // stats stride between points
+#pragma unroll 1
+        for (int o = tid; o < nopt; o += 2 * tpb) {
+            const int o2 = o + tpb;
+            const bool two = o2 < nopt;
+            OptC A, B;
+            load_opt(o, A);
+            load_opt(two ? o2 : o, B);
+            double s1a[4] = {0, 0, 0, 0}, s2a[4] = {0, 0, 0, 0}, s1b[4] = {0, 0, 0, 0}, s2b[4] = {0, 0, 0, 0};
 #pragma unroll 1
             for (int pth = 0; pth < np; ++pth) {
-                const double* st = stats + ((size_t)pth * nfam + op.family) * kStatW;
-                const double stat = lb ? st[3] : st[0];
-                const double lnst = lb ? st[4] : st[1];
-                const double I = lb ? st[5] : st[2];
-                if (lb && st[6] != 0.0) ++ties;
-                const double psi = (op.lnK - lnst - F.omega * F.t1) * F.inv_s;
-                double Q0, Q1, ph, phs;
-                phibar_phi_x2(psi, psi - F.s, Q0, Q1, ph, phs);
-                double f[4];
-                if (bin) {
-                    f[0] = D * Q0;
-                    f[1] = D * ph * F.inv_s / S0;
-                    f[2] = D * ph * (I * F.inv_s / stat + psi * F.inv_sigma - F.sqrt_t1);
-                    f[3] = D * ph * F.inv_s / (S0 * S0) * (psi * F.inv_s - 1.0);
-                } else {
-                    f[0] = F.Afac * stat * Q1 - D * K * Q0;
-                    f[1] = F.Afac * (stat / S0) * Q1;
-                    f[2] = F.Afac * Q1 * I + K * D * ph * F.sqrt_t1;
-                    f[3] = K * D * ph * F.inv_s / (S0 * S0);
+                const double* sa = A.st + (size_t)pth * fstride;
+                const double* sb = B.st + (size_t)pth * fstride;
+                if (A.lb && sa[7] != 0.0) ++ties;
+                if (two && B.lb && sb[7] != 0.0) ++ties;
+                const double psia = (A.c_lnK - (A.lb ? sa[5] : sa[1])) * A.inv_s;
+                const double psib = (B.c_lnK - (B.lb ? sb[5] : sb[1])) * B.inv_s;
+                double Q0a, Q1a, pha, phsa, Q0b, Q1b, phb, phsb;
+                phibar_phi_x2(psia, psia - A.c_s, Q0a, Q1a, pha, phsa);
+                phibar_phi_x2(psib, psib - B.c_s, Q0b, Q1b, phb, phsb);
+                double fa[4], fb[4];
+                tail(A, sa, Q0a, Q1a, pha, psia, fa);
+                tail(B, sb, Q0b, Q1b, phb, psib, fb);
+                if (P.path_out != nullptr) {
+                    for (int qq = 0; qq < 4; ++qq) P.path_out[((ib + pth) * nopt + o) * 4 + qq] = fa[qq];
+                    if (two)
+                        for (int qq = 0; qq < 4; ++qq) P.path_out[((ib + pth) * nopt + o2) * 4 + qq] = fb[qq];
                 }
-                if (P.path_out != nullptr)
-                    for (int qq = 0; qq < 4; ++qq) P.path_out[((ib + pth) * nopt + o) * 4 + qq] = f[qq];
 #pragma unroll
                 for (int qq = 0; qq < 4; ++qq) {
-                    const double y = f[qq] - op.piv[qq];
-                    s1[qq] += y;
-                    s2[qq] = fma(y, y, s2[qq]);
+                    const double ya = fa[qq] - A.piv[qq], yb = fb[qq] - B.piv[qq];
+                    s1a[qq] += ya;
+                    s2a[qq] = fma(ya, ya, s2a[qq]);
+                    s1b[qq] += yb;
+                    s2b[qq] = fma(yb, yb, s2b[qq]);
                 }
             }
 #pragma unroll
             for (int qq = 0; qq < 4; ++qq) {
-                accs[(2 * qq) * nopt + o] += s1[qq];
-                accs[(2 * qq + 1) * nopt + o] += s2[qq];
+                prow[o * 8 + 2 * qq] += s1a[qq];
+                prow[o * 8 + 2 * qq + 1] += s2a[qq];
+            }
+            if (two) {
+#pragma unroll
+                for (int qq = 0; qq < 4; ++qq) {
+                    prow[o2 * 8 + 2 * qq] += s1b[qq];
+                    prow[o2 * 8 + 2 * qq + 1] += s2b[qq];
+                }
             }
         }
     }
-    // ---- epilogue: options are owned by single threads; counters reduced -----
+    // ---- epilogue: option sums are already in the row; counters reduced -----
     __syncthreads();
-    const int stride = P.partial_stride;
-    for (int o = tid; o < nopt; o += tpb)
-#pragma unroll
-        for (int v = 0; v < 8; ++v) P.partials[(size_t)cell * stride + o * 8 + v] = accs[v * nopt + o];
     unsigned tc = ties, nc = npts;
 #pragma unroll
     for (int off = 16; off > 0; off >>= 1) {
@@ -224,15 +275,15 @@ __global__ void __launch_bounds__(128) portfolio_kernel(const PortfolioArgs P) {
             t += red[w * 2];
             n += red[w * 2 + 1];
         }
-        P.partials[(size_t)cell * stride + nopt * 8 + 0] = 0.0;  // Newton: not used (W1)
-        P.partials[(size_t)cell * stride + nopt * 8 + 1] = t;
-        P.partials[(size_t)cell * stride + nopt * 8 + 2] = n;
+        prow[nopt * 8 + 0] = 0.0;  // Newton: not used (W1)
+        prow[nopt * 8 + 1] = t;
+        prow[nopt * 8 + 2] = n;
     }
 }
 
 static size_t portfolio_smem_bytes(const PortfolioArgs& a) {
     const size_t tpb = (size_t)1 << a.tpb_log2, nw = tpb / 32;
-    size_t b = (size_t)8 * a.n_opt * sizeof(double) + tpb * a.n_fam * kStatW * sizeof(double);
+    size_t b = tpb * a.n_fam * kStatW * sizeof(double);
     b += ((size_t)a.d * 32 * 2 + a.d) * sizeof(uint32_t) + 4;
     const size_t hw = 2 * 2 * nw * a.d * sizeof(uint32_t), red = 4 * 32 * sizeof(double);
     return b + (hw > red ? hw : red);
