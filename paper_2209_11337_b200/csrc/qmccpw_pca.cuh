@@ -181,7 +181,10 @@ __global__ void __launch_bounds__(128, pca_min_blocks<COND, KF>()) pca_kernel(co
                     cv[2 * jt + 1] = fma(sg, cv[2 * jt + 1], fma(P.omega, (double)(j0 + 2) * P.t1, P.lnS0));
                 }
                 double f[kMaxOpt][4];
-#pragma unroll
+                // one Newton solve per strike group, not unrolled over the options: the
+                // body is large and the instruction cache is the limiter (ncu: 41 % of
+                // stalls were no_instructions with three unrolled copies)
+#pragma unroll 1
                 for (int o = 0; o < kMaxOpt; ++o) {
                     if (o >= P.n_opt) break;
                     if (P.tail_leader[o] != o) continue;

@@ -4,14 +4,15 @@ rows = list(csv.reader(open(raw))); a = dict(zip(rows[0], rows[2])); u = dict(zi
 for k in ['gpu__time_duration.sum', 'sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active',
           'smsp__issue_active.avg.pct_of_peak_sustained_active', 'sm__warps_active.avg.per_cycle_active',
           'launch__registers_per_thread', 'smsp__inst_executed.sum', 'dram__bytes_read.sum', 'dram__bytes_write.sum',
-          'l1tex__data_pipe_lsu_wavefronts_mem_shared.sum', 'smsp__inst_executed_pipe_uniform.sum']:
+          'l1tex__data_pipe_lsu_wavefronts_mem_shared.sum', 'sm__inst_executed_pipe_xu.avg.pct_of_peak_sustained_active',
+          'sm__pipe_alu_cycles_active.avg.pct_of_peak_sustained_active']:
     print(f"{k:70s} {a.get(k)} {u.get(k)}")
 st = [(k, float(a[k] or 0)) for k in a if 'pcsamp_warps_issue_stalled' in k and not k.endswith('not_issued')]
 tot = sum(v for _, v in st)
 print("stalls:", ", ".join(f"{k.split('stalled_')[1]}={v/tot*100:.1f}%" for k, v in sorted(st, key=lambda x: -x[1])[:8]))
 rows = list(csv.reader(open(sass))); hdr = rows[1]; ie = hdr.index("Instructions Executed"); src = hdr.index("Source")
 op = collections.Counter(); n_all = 0
-paths = 2 ** 26
+paths = int(sys.argv[4]) if len(sys.argv) > 4 else 2 ** 26  # points per launch
 for r in rows[2:]:
     try: n = int(r[ie])
     except: continue
