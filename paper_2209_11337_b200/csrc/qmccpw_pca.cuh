@@ -88,31 +88,32 @@ __global__ void __launch_bounds__(128, pca_min_blocks<COND, KF>()) pca_kernel(co
             const bool valid = ip < P.n_points;
             const SobolBlock sp{G, HWb, d, nw, (int)(kp0 & 31), (int)((kp0 >> 5) & (uint64_t)(nw - 1)),
                                 (int)((kp0 >> tpb_log2) - Ab), OWEN ? sh : nullptr};
-            // A fragments: x[path][4 f + r4]
-            double afr[KF];
+            // k-steps f (pairs) outer, not unrolled: each step draws this lane's two A
+            // elements x[path][4 f + r4] and feeds them to all JT column tiles at once, so
+            // the code holds one normal pair and 2 JT DMMAs instead of KF/2 pairs and KF JT
+            // (the unrolled form was instruction-fetch bound); same k order, same bits.
+            double cv[2 * JT];  // W(t_j) (W1) or c_j (X1) at j = 8 jt + 2 r4 + e
 #pragma unroll
+            for (int v = 0; v < 2 * JT; ++v) cv[v] = 0.0;
+            double W1v = 0.0;
+#pragma unroll 1
             for (int f = 0; f < KF; f += 2) {
                 const int ja = 4 * f + r4, jb = 4 * (f + 1) + r4;
                 double xa, xb;
                 normal_from_u32_x2(sp.get(ja < d ? ja : d - 1), sp.get(jb < d ? jb : d - 1), xa, xb);
-                afr[f] = (ja < d && !(COND == kX1 && ja == 0)) ? xa : 0.0;
-                afr[f + 1] = (jb < d && !(COND == kX1 && jb == 0)) ? xb : 0.0;
-            }
-            double cv[2 * JT];  // W(t_j) (W1) or c_j (X1) at j = 8 jt + 2 r4 + e
-            double W1v = 0.0;
+                const double a0 = (ja < d && !(COND == kX1 && ja == 0)) ? xa : 0.0;
+                const double a1 = (jb < d && !(COND == kX1 && jb == 0)) ? xb : 0.0;
 #pragma unroll
-            for (int jt = 0; jt < JT; ++jt) {
-                double acc0 = 0.0, acc1 = 0.0;
-                const double* Mrow = P.M + (size_t)(8 * jt + q) * DP + r4;
-#pragma unroll
-                for (int f = 0; f < KF; ++f) {
-                    const double bfrag = __ldg(Mrow + 4 * f);
+                for (int jt = 0; jt < JT; ++jt) {
+                    const double* Mrow = P.M + (size_t)(8 * jt + q) * DP + r4 + 4 * f;
+                    const double b0 = __ldg(Mrow), b1 = __ldg(Mrow + 4);
                     asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
-                                 : "+d"(acc0), "+d"(acc1)
-                                 : "d"(afr[f]), "d"(bfrag));
+                                 : "+d"(cv[2 * jt]), "+d"(cv[2 * jt + 1])
+                                 : "d"(a0), "d"(b0));
+                    asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+                                 : "+d"(cv[2 * jt]), "+d"(cv[2 * jt + 1])
+                                 : "d"(a1), "d"(b1));
                 }
-                cv[2 * jt] = acc0;
-                cv[2 * jt + 1] = acc1;
             }
             if (COND == kW1) {
                 W1v = __shfl_sync(0xffffffffu, cv[0], lane & ~3);  // W(t_1) of this path
