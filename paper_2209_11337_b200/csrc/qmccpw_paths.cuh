@@ -222,21 +222,39 @@ __global__ void __launch_bounds__(128, paths_min_blocks<CONSTR, COND, METHOD>())
                     w1.push(P, 0, 0.0);
                 } else {
                     double Wl = 0.0, W1 = 0.0;
+                    // e = 1 (half of the steps) and e = 2 (a quarter) in straight-line code:
+                    // no stack store, no loop, the two finest b's in registers
+                    const double bm = P.bb_b[m], bm1 = P.bb_b[m > 1 ? m - 1 : m];
+                    auto next_x = [&]() {
+                        const bool refill = fifo.have == 0;
+                        const double x = fifo.next(sob, dim_at);
+                        pos += refill ? 2 : 0;
+                        return x;
+                    };
 #pragma unroll 1
                     for (int pp = 0; pp < (d >> 1); ++pp) {
                         const int e = (pp == 0) ? m : __ffs(pp);  // 1 + ctz(pp)
-                        double Wr = stW[sp];
+                        const double top = stW[sp];
+                        double Wodd, Weven;
+                        if (e == 1) {
+                            Wodd = fma(bm, next_x(), 0.5 * (Wl + top));
+                            Weven = top;
+                            --sp;
+                        } else if (e == 2) {  // push + pop of the level m-1 midpoint cancel
+                            Weven = fma(bm1, next_x(), 0.5 * (Wl + top));
+                            Wodd = fma(bm, next_x(), 0.5 * (Wl + Weven));
+                        } else {
+                            double Wr = top;
 #pragma unroll 1
-                        for (int c = e - 1; c >= 0; --c) {
-                            const bool refill = fifo.have == 0;
-                            const double x = fifo.next(sob, dim_at);
-                            pos += refill ? 2 : 0;
-                            const double Wm = fma(P.bb_b[m - c], x, 0.5 * (Wl + Wr));
-                            if (c > 0) stW[++sp] = Wm;
-                            Wr = Wm;
+                            for (int c = e - 1; c >= 0; --c) {
+                                const double Wm = fma(P.bb_b[m - c], next_x(), 0.5 * (Wl + Wr));
+                                if (c > 0) stW[++sp] = Wm;
+                                Wr = Wm;
+                            }
+                            Wodd = Wr;
+                            Weven = stW[sp];
+                            --sp;
                         }
-                        const double Wodd = Wr, Weven = stW[sp];
-                        --sp;
                         if (pp == 0) W1 = Wodd;
                         w1.push2(P, 2 * pp, Wodd - W1, Weven - W1);
                         Wl = Weven;
