@@ -61,10 +61,15 @@ __global__ void __launch_bounds__(128, paths_min_blocks<CONSTR, COND, METHOD>())
     const uint64_t kt = K0 + (uint64_t)tid;
     SobolBlock sob{G, HW, d, nw, (int)(kt & 31), (int)((kt >> 5) & (uint64_t)(nw - 1)), (int)((kt >> tpb_log2) - Ab),
                    OWEN ? sh : nullptr};
+    // BB-W1 stages the replicate's tables in the bridge's consumption order (row i =
+    // Sobol' dimension bb_seq[i]), so the i-th normal reads row i: no per-normal
+    // dimension lookup
+    constexpr bool kPerm = (CONSTR == kBB && COND == kW1 && METHOD == kQmc);
     if (METHOD == kQmc) {
         const uint32_t* src = P.vscr + (size_t)rep_local * d * 32;
-        for (int idx = tid; idx < d * 32; idx += tpb) vt[idx] = src[idx];
-        for (int idx = tid; idx < d; idx += tpb) sh[idx] = P.shift[(size_t)rep_local * d + idx];
+        for (int idx = tid; idx < d * 32; idx += tpb)
+            vt[idx] = src[kPerm ? (int)P.bb_seq[idx >> 5] * 32 + (idx & 31) : idx];
+        for (int idx = tid; idx < d; idx += tpb) sh[idx] = P.shift[(size_t)rep_local * d + (kPerm ? P.bb_seq[idx] : idx)];
         __syncthreads();
         sobol_build_g(vt, d, G, tid, tpb);
     }
@@ -212,7 +217,7 @@ __global__ void __launch_bounds__(128, paths_min_blocks<CONSTR, COND, METHOD>())
                 NormalFifo fifo;
                 fifo.reset();
                 int pos = 0;
-                auto dim_at = [&](int o) { return (int)P.bb_seq[pos + o]; };
+                auto dim_at = [&](int o) { return pos + o; };  // tables are in consumption order (kPerm)
                 double stW[12];
                 int sp = 0;
                 stW[0] = P.sqrtT * fifo.next(sob, dim_at);
