@@ -21,7 +21,7 @@ namespace qmccpw {
 constexpr int kStatW = 8;  // staged per (point, family): SA, lnSA, IA, IA/SA, Smax, lnSmax, Imax, near-tie flag
 
 template <int KF, bool OWEN>
-__global__ void __launch_bounds__(128) portfolio_kernel(const PortfolioArgs P) {
+__global__ void __launch_bounds__(128, 3) portfolio_kernel(const PortfolioArgs P) {  // 3 blocks: 72.5 KB smem each
     extern __shared__ __align__(16) unsigned char smem_raw[];
     constexpr int DP = 4 * KF;
     constexpr int JT = DP / 8;
@@ -34,11 +34,11 @@ __global__ void __launch_bounds__(128) portfolio_kernel(const PortfolioArgs P) {
     const uint64_t i0 = blk * (uint64_t)kCellPoints;
     const int ppt = kCellPoints >> tpb_log2;
     const int nw = tpb >> 5;
-    // smem: stats [tpb][nfam][kStatW] | vt | sh | G | HW
-    double* stats = reinterpret_cast<double*>(smem_raw);
+    // smem: stats [tpb/2][nfam][kStatW] | vt | sh | G | HW
+    double* stats = reinterpret_cast<double*>(smem_raw);  // [tpb/2 slots][nfam][kStatW]
     double* prow = P.partials + (size_t)cell * P.partial_stride;  // this cell's row: [nopt][8] + 3 counters
     const double inv_d = 1.0 / (double)d;
-    uint32_t* vt = reinterpret_cast<uint32_t*>(stats + (size_t)tpb * nfam * kStatW);
+    uint32_t* vt = reinterpret_cast<uint32_t*>(stats + (size_t)(tpb / 2) * nfam * kStatW);
     uint32_t* sh = vt + (size_t)d * 32;
     uint32_t* G = sh + d;
     uint32_t* HW = G + (size_t)d * 32;
@@ -64,10 +64,18 @@ __global__ void __launch_bounds__(128) portfolio_kernel(const PortfolioArgs P) {
         uint32_t* HWb = HW + (a & 1) * hw_size;
         sobol_build_hw(vt, OWEN ? nullptr : sh, d, 0, tpb_log2, nw, Ab + (uint64_t)a, HWb, tid, tpb);
         __syncthreads();  // also: every thread has left phase B of the previous point
+        const uint64_t ib = i0 + ((uint64_t)a << tpb_log2);
+        const int np = (int)((P.n_points - ib) < (uint64_t)tpb ? (P.n_points - ib) : (uint64_t)tpb);
+        if (tid < np) ++npts;
+        // two halves of 64 points (row tiles 0-1, then 2-3 of every warp): half the staged
+        // statistics, so three blocks fit per SM
+#pragma unroll 1
+        for (int half = 0; half < 2; ++half) {
         // ---- phase A -------------------------------------------------------
 #pragma unroll 1
-        for (int rt = 0; rt < 4; ++rt) {
+        for (int rt = 2 * half; rt < 2 * half + 2; ++rt) {
             const int tp = wbase + 8 * rt + q;
+            const int slot = (wbase >> 1) + 8 * (rt - 2 * half) + q;  // 16 per warp per half
             const uint64_t kp0 = K0 + (uint64_t)tp;
             const SobolBlock sp{G, HWb, d, nw, (int)(kp0 & 31), (int)((kp0 >> 5) & (uint64_t)(nw - 1)),
                                 (int)((kp0 >> tpb_log2) - Ab), OWEN ? sh : nullptr};
@@ -147,7 +155,7 @@ __global__ void __launch_bounds__(128) portfolio_kernel(const PortfolioArgs P) {
                     const double SA = sS * inv_d, Smax = P.has_lookback ? P.S0 * fast_exp(em) : SA;
                     double lnSA, lnSmax;
                     fast_log_x2(SA, Smax, lnSA, lnSmax);
-                    double* st = stats + ((size_t)tp * nfam + fi) * kStatW;
+                    double* st = stats + ((size_t)slot * nfam + fi) * kStatW;
                     st[0] = SA;
                     st[1] = lnSA;
                     st[2] = sI * inv_d;
@@ -161,9 +169,6 @@ __global__ void __launch_bounds__(128) portfolio_kernel(const PortfolioArgs P) {
         }
         __syncthreads();
         // ---- phase B -------------------------------------------------------
-        const uint64_t ib = i0 + ((uint64_t)a << tpb_log2);
-        const int np = (int)((P.n_points - ib) < (uint64_t)tpb ? (P.n_points - ib) : (uint64_t)tpb);
-        if (tid < np) ++npts;
         // per-option constants (P:396-414, P:544-600 with the divisions hoisted)
         struct OptC {
             const double* st;  // stats of the option's family, point 0
@@ -215,9 +220,11 @@ __global__ void __launch_bounds__(128) portfolio_kernel(const PortfolioArgs P) {
             load_opt(two ? o2 : o, B);
             double s1a[4] = {0, 0, 0, 0}, s2a[4] = {0, 0, 0, 0}, s1b[4] = {0, 0, 0, 0}, s2b[4] = {0, 0, 0, 0};
 #pragma unroll 1
-            for (int pth = 0; pth < np; ++pth) {
-                const double* sa = A.st + (size_t)pth * fstride;
-                const double* sb = B.st + (size_t)pth * fstride;
+            for (int sl = 0; sl < 64; ++sl) {
+                const int pth = 32 * (sl >> 4) + 8 * (2 * half + ((sl >> 3) & 1)) + (sl & 7);  // block slot
+                if (pth >= np) continue;  // ragged last iteration (block-uniform)
+                const double* sa = A.st + (size_t)sl * fstride;
+                const double* sb = B.st + (size_t)sl * fstride;
                 if (A.lb && sa[7] != 0.0) ++ties;
                 if (two && B.lb && sb[7] != 0.0) ++ties;
                 const double psia = (A.c_lnK - (A.lb ? sa[5] : sa[1])) * A.inv_s;
@@ -255,6 +262,8 @@ __global__ void __launch_bounds__(128) portfolio_kernel(const PortfolioArgs P) {
                 }
             }
         }
+        __syncthreads();  // phase B done before the next half's phase A overwrites the stats
+        }  // half
     }
     // ---- epilogue: option sums are already in the row; counters reduced -----
     __syncthreads();
@@ -283,7 +292,7 @@ __global__ void __launch_bounds__(128) portfolio_kernel(const PortfolioArgs P) {
 
 static size_t portfolio_smem_bytes(const PortfolioArgs& a) {
     const size_t tpb = (size_t)1 << a.tpb_log2, nw = tpb / 32;
-    size_t b = tpb * a.n_fam * kStatW * sizeof(double);
+    size_t b = (tpb / 2) * a.n_fam * kStatW * sizeof(double);  // one half (64 points) staged at a time
     b += ((size_t)a.d * 32 * 2 + a.d) * sizeof(uint32_t) + 4;
     const size_t hw = 2 * 2 * nw * a.d * sizeof(uint32_t), red = 4 * 32 * sizeof(double);
     return b + (hw > red ? hw : red);
