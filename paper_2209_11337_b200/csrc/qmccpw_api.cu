@@ -191,7 +191,7 @@ int tpb_log2_for(const qmccpw_config& c, int d, int n_opt) {
         if (mma) b += (size_t)((d + 7) & ~7) * (tpb + 8) * 8;
         else if (need_buf) b += (size_t)d * tpb * 8;
         if (two_buf) b += (size_t)d * tpb * 8;
-        const size_t hw = 4 * nw * d * 4;
+        const size_t hw = (4 * nw * d + d) * 4;
         b += ((size_t)d * 64 + d) * 4 + 4 + (hw > 1024 ? hw : 1024);
         if (b <= 200 * 1024) return lg;
     }

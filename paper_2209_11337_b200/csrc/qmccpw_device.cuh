@@ -74,6 +74,49 @@ __device__ __forceinline__ void sobol_build_g(const uint32_t* vt, int d, uint32_
     }
 }
 
+// The same table built incrementally.  HW_j(A, w) = B_j(A) ^ WP_j(w) with
+//   B_j(A) = c_j ^ XOR_{b in g(A)} v'_{j,p+b} ^ (A&1) v'_{j,p-1},  WP_j(w) = (w&1) v'_{j,4} ^ XOR_{b in g(w)} v'_{j,5+b},
+// and the Gray code of A+1 differs from that of A in bit ctz(A+1) only, so
+//   B_j(A+1) = B_j(A) ^ v'_{j,p+ctz(A+1)} ^ v'_{j,p-1}:
+// one XOR pair per dimension per step instead of a popcount loop.  B_j(A+1) of this step
+// is B_j(A) of the next one; BS [d] keeps it (owned by the thread of dimension j, so no
+// extra barrier).  first: build B_j(A) directly.
+__device__ __forceinline__ uint32_t sobol_base_step(const uint32_t* v, int p, uint64_t A1) {
+    const int c = __ffsll((long long)A1) - 1;  // A1 >= 1
+    uint32_t r = v[p - 1];
+    if (p + c < 32) r ^= v[p + c];
+    return r;
+}
+__device__ __forceinline__ void sobol_build_hw_inc(const uint32_t* vt, const uint32_t* sh, int d, int j0, int p, int nw,
+                                                   uint64_t A, bool first, uint32_t* BS, uint32_t* HW, int tid,
+                                                   int tpb) {
+    for (int j = tid; j < d; j += tpb) {
+        if (j < j0) continue;
+        const uint32_t* v = vt + j * 32;
+        uint32_t b0;
+        if (first) {
+            b0 = sh != nullptr ? sh[j] : 0u;
+            if (A & 1) b0 ^= v[p - 1];
+            uint32_t gA = (uint32_t)(A ^ (A >> 1)) & ((p >= 32) ? 0u : (0xFFFFFFFFu >> p));
+            while (gA) {
+                b0 ^= v[p + __ffs(gA) - 1];
+                gA &= gA - 1;
+            }
+        } else {
+            b0 = BS[j];
+        }
+        const uint32_t b1 = b0 ^ sobol_base_step(v, p, A + 1);
+        BS[j] = b1;
+        const uint32_t v4 = v[4], v5 = v[5], v6 = v[6];
+        for (int w = 0; w < nw; ++w) {
+            const int gw = w ^ (w >> 1);
+            const uint32_t wp = ((w & 1) ? v4 : 0u) ^ ((gw & 1) ? v5 : 0u) ^ ((gw & 2) ? v6 : 0u);
+            HW[w * d + j] = b0 ^ wp;
+            HW[(nw + w) * d + j] = b1 ^ wp;
+        }
+    }
+}
+
 __device__ __forceinline__ void sobol_build_hw(const uint32_t* vt, const uint32_t* sh, int d, int j0, int p, int nw,
                                                uint64_t A0, uint32_t* HW, int tid, int tpb) {
     const int n = 2 * nw * d;

@@ -55,6 +55,7 @@ __global__ void __launch_bounds__(128, paths_min_blocks<CONSTR, COND, METHOD>())
     HW += ((uintptr_t)HW & 7) ? 1 : 0;
     double* red = reinterpret_cast<double*>(HW);
     const int hw_size = 2 * nw * d;
+    uint32_t* BS = HW + 2 * hw_size;  // [d] incremental Gray bases (sobol_build_hw_inc)
 
     const uint64_t K0 = P.point_offset + i0;
     const uint64_t Ab = K0 >> tpb_log2;
@@ -84,7 +85,8 @@ __global__ void __launch_bounds__(128, paths_min_blocks<CONSTR, COND, METHOD>())
         if (i0 + ((uint64_t)a << tpb_log2) >= P.n_points) break;  // block-uniform: ragged last cell
         if (METHOD == kQmc) {
             uint32_t* HWb = HW + (a & 1) * hw_size;  // double-buffered: one barrier per iteration
-            sobol_build_hw(vt, OWEN ? nullptr : sh, d, P.dim_begin, tpb_log2, nw, Ab + (uint64_t)a, HWb, tid, tpb);
+            sobol_build_hw_inc(vt, OWEN ? nullptr : sh, d, P.dim_begin, tpb_log2, nw, Ab + (uint64_t)a, a == 0, BS, HWb, tid,
+                               tpb);
             __syncthreads();
             sob.HW = HWb;
         }
@@ -512,7 +514,7 @@ static size_t path_smem_bytes(const PathArgs& a, int constr, int cond, int metho
     size_t hw = 0;
     if (method == kQmc) {
         b += ((size_t)a.d * 32 * 2 + a.d) * sizeof(uint32_t) + 4;  // vt, sh, G, alignment pad
-        hw = 2 * 2 * nw * a.d * sizeof(uint32_t);
+        hw = (2 * 2 * nw * a.d + a.d) * sizeof(uint32_t);
     }
     const size_t red = 4 * 32 * sizeof(double);
     return b + (hw > red ? hw : red);

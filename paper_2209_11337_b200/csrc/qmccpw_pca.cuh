@@ -56,6 +56,7 @@ __global__ void __launch_bounds__(128, pca_min_blocks<COND, KF>()) pca_kernel(co
     HW += ((uintptr_t)HW & 7) ? 1 : 0;
     double* red = reinterpret_cast<double*>(HW);
     const int hw_size = 2 * nw * d;
+    uint32_t* BS = HW + 2 * hw_size;  // [d] incremental Gray bases (sobol_build_hw_inc)
     const uint64_t K0 = P.point_offset + i0;
     const uint64_t Ab = K0 >> tpb_log2;
     {
@@ -75,7 +76,7 @@ __global__ void __launch_bounds__(128, pca_min_blocks<COND, KF>()) pca_kernel(co
     for (int a = 0; a < ppt; ++a) {
         if (i0 + ((uint64_t)a << tpb_log2) >= P.n_points) break;  // block-uniform
         uint32_t* HWb = HW + (a & 1) * hw_size;
-        sobol_build_hw(vt, OWEN ? nullptr : sh, d, 0, tpb_log2, nw, Ab + (uint64_t)a, HWb, tid, tpb);
+        sobol_build_hw_inc(vt, OWEN ? nullptr : sh, d, 0, tpb_log2, nw, Ab + (uint64_t)a, a == 0, BS, HWb, tid, tpb);
         __syncthreads();
         // W1: statistics of this lane's own path, handed over by its quad after each row tile
         W1Acc w1own;
@@ -319,7 +320,7 @@ static size_t pca_smem_bytes(const PathArgs& a) {
     const size_t tpb = (size_t)1 << a.tpb_log2, nw = tpb / 32;
     size_t b = (size_t)a.n_opt * 8 * tpb * sizeof(double);
     b += ((size_t)a.d * 32 * 2 + a.d) * sizeof(uint32_t) + 4;
-    const size_t hw = 2 * 2 * nw * a.d * sizeof(uint32_t), red = 4 * 32 * sizeof(double);
+    const size_t hw = (2 * 2 * nw * a.d + a.d) * sizeof(uint32_t), red = 4 * 32 * sizeof(double);
     return b + (hw > red ? hw : red);
 }
 
