@@ -251,7 +251,8 @@ __global__ void sobol_hook_kernel(const uint32_t* __restrict__ vscr, const uint3
     for (int a = 0; a < kCellPoints / tpb; ++a) {
         if (K0 + ((uint64_t)a << tpb_log2) >= k_end) break;
         uint32_t* HWb = h.HW + (a & 1) * 2 * nw * d;
-        sobol_build_hw(h.vt, owen ? nullptr : h.sh, d, 0, tpb_log2, nw, Ab + (uint64_t)a, HWb, tid, tpb);
+        sobol_build_hw_inc(h.vt, owen ? nullptr : h.sh, d, 0, tpb_log2, nw, Ab + (uint64_t)a, a == 0,
+                           h.HW + 4 * nw * d, HWb, tid, tpb);  // the path kernels' incremental build
         __syncthreads();
         sob.HW = HWb;
         const uint64_t k = K0 + tid + ((uint64_t)a << tpb_log2);
@@ -288,7 +289,8 @@ __global__ void normals_hook_kernel(const uint32_t* __restrict__ vscr, const uin
     for (int a = 0; a < kCellPoints / tpb; ++a) {
         if (K0 + ((uint64_t)a << tpb_log2) >= k_end) break;
         uint32_t* HWb = h.HW + (a & 1) * 2 * nw * d;
-        sobol_build_hw(h.vt, owen ? nullptr : h.sh, d, 0, tpb_log2, nw, Ab + (uint64_t)a, HWb, tid, tpb);
+        sobol_build_hw_inc(h.vt, owen ? nullptr : h.sh, d, 0, tpb_log2, nw, Ab + (uint64_t)a, a == 0,
+                           h.HW + 4 * nw * d, HWb, tid, tpb);  // the path kernels' incremental build
         __syncthreads();
         sob.HW = HWb;
         const uint64_t k = K0 + tid + ((uint64_t)a << tpb_log2);
@@ -309,7 +311,7 @@ cudaError_t launch_sobol_hook(const uint32_t* d_vscr, const uint32_t* d_shift, i
                               cudaStream_t st) {
     const uint64_t nk = k_end - k_begin;
     const unsigned grid = (unsigned)((nk + kCellPoints - 1) / kCellPoints);
-    const size_t smem = ((size_t)d * 64 + d + 2 * 2 * 4 * d) * 4;
+    const size_t smem = ((size_t)d * 64 + d + 2 * 2 * 4 * d + d) * 4;
     cudaError_t e = cudaFuncSetAttribute(sobol_hook_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     sobol_hook_kernel<<<grid, 128, smem, st>>>(d_vscr, d_shift, d, dim_begin, dim_end, k_begin, k_end, owen, d_out);
@@ -322,7 +324,7 @@ cudaError_t launch_normals_hook(const uint32_t* d_vscr, const uint32_t* d_shift,
                                 cudaStream_t st) {
     const uint64_t nk = k_end - k_begin;
     const unsigned grid = (unsigned)((nk + kCellPoints - 1) / kCellPoints);
-    const size_t smem = method != kQmc ? 0 : ((size_t)d * 64 + d + 2 * 2 * 4 * d) * 4;
+    const size_t smem = method != kQmc ? 0 : ((size_t)d * 64 + d + 2 * 2 * 4 * d + d) * 4;
     cudaError_t e =
         cudaFuncSetAttribute(normals_hook_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
