@@ -11,11 +11,11 @@ namespace qmccpw {
 #define QMCCPW_BB_MINB 8
 #endif
 #ifndef QMCCPW_STD_MINB
-#define QMCCPW_STD_MINB 6
+#define QMCCPW_STD_MINB 7
 #endif
 // resident blocks per SM the register allocator must allow (128 threads each); 0 = ptxas'
 // own choice.  Measured on C4 (ms/step): BB-W1 34.3 (ptxas, 96 regs) / 33.8 (7) / 33.4
-// (8: 64 regs, a few spills to L1); STD-W1 33.1 (4) / 31.9 (5) / 31.2 (6)
+// (8: 64 regs, a few spills to L1); STD-W1 33.1 (4) / 31.9 (5) / 31.2 (6); v11: 27.20 (6) / 27.03 (7) / 27.4 (8)
 template <int CONSTR, int COND, int METHOD>
 constexpr int paths_min_blocks() {
     return (COND == kW1 && METHOD == kQmc) ? (CONSTR == kBB ? QMCCPW_BB_MINB : CONSTR == kStd ? QMCCPW_STD_MINB : 0) : 0;
