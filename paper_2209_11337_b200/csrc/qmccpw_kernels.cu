@@ -267,6 +267,8 @@ __global__ void normals_hook_kernel(const uint32_t* __restrict__ vscr, const uin
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const int tpb_log2 = 7, tpb = 128, tid = threadIdx.x, nw = 4;
     const uint64_t K0 = k_begin + (uint64_t)blockIdx.x * kCellPoints;
+    math_tables_load(tid, tpb);
+    __syncthreads();
     if (method != kQmc) {  // LR+MC, MC-CPW, MC+AV-CPW: the Philox stream
         for (int a = 0; a < kCellPoints / tpb; ++a) {
             const uint64_t k = K0 + tid + ((uint64_t)a << tpb_log2);

@@ -66,6 +66,8 @@ __global__ void __launch_bounds__(128, paths_min_blocks<CONSTR, COND, METHOD>())
     // Sobol' dimension bb_seq[i]), so the i-th normal reads row i: no per-normal
     // dimension lookup
     constexpr bool kPerm = (CONSTR == kBB && COND == kW1 && METHOD == kQmc);
+    math_tables_load(tid, tpb);
+    if (METHOD != kQmc) __syncthreads();  // QMC: the barrier below publishes the tables
     if (METHOD == kQmc) {
         const uint32_t* src = P.vscr + (size_t)rep_local * d * 32;
         for (int idx = tid; idx < d * 32; idx += tpb)

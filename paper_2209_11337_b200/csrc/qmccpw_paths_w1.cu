@@ -1,5 +1,6 @@
 // qmccpw_paths_w1.cu -- path kernels with W1 conditioning (all methods) and the
 // launch_paths dispatcher (X1 kernels: qmccpw_paths_x1.cu; PCA on DMMA: qmccpw_pca_*.cu).
+#define QMCCPW_SMEM_TABLES 1  // exp / log tables in shared memory (see qmccpw_math.cuh)
 #include "qmccpw_paths.cuh"
 
 namespace qmccpw {

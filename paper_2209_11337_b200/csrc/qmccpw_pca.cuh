@@ -60,6 +60,7 @@ __global__ void __launch_bounds__(128, pca_min_blocks<COND, KF>()) pca_kernel(co
     const uint64_t K0 = P.point_offset + i0;
     const uint64_t Ab = K0 >> tpb_log2;
     {
+        math_tables_load(tid, tpb);
         const uint32_t* src = P.vscr + (size_t)rep_local * d * 32;
         for (int idx = tid; idx < d * 32; idx += tpb) vt[idx] = src[idx];
         for (int idx = tid; idx < d; idx += tpb) sh[idx] = P.shift[(size_t)rep_local * d + idx];

@@ -1,4 +1,5 @@
 // qmccpw_pca_w1.cu -- PCA paths on DMMA tiles, W1 conditioning (d <= 128).
+#define QMCCPW_SMEM_TABLES 1  // exp / log tables in shared memory (see qmccpw_math.cuh)
 #include "qmccpw_pca.cuh"
 
 namespace qmccpw {
