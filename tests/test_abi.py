@@ -70,6 +70,14 @@ def test_validation_happens_before_device_access():
         q.qmccpw_price_greeks_batch([0] * 9, [q.params(sigma=0.1 + 0.01 * i, d=8) for i in range(9)], 1024, 2,
                                     q.config(construction=q.PCA))
     assert e.value.code == q.EUNSUPPORTED
+    with pytest.raises(q.QmcCpwError) as e:  # GPCA (row f3) is one market per call, not a portfolio
+        q.qmccpw_price_greeks_batch([0, 1, 2, 0], [q.params(K=90.0 + i, d=8) for i in range(4)], 1024, 2,
+                                    q.config(construction=q.GPCA))
+    assert e.value.code == q.EUNSUPPORTED
+    for cfg in (q.config(construction=5), q.config(randomization=5), q.config(method=q.MC_CPW, construction=q.GPCA)):
+        with pytest.raises(q.QmcCpwError) as e:
+            q.qmccpw_price_greeks(0, q.params(d=8), 1024, 2, cfg)
+        assert e.value.code in (q.EINVAL, q.EUNSUPPORTED)
     with pytest.raises(q.QmcCpwError) as e:  # different S0
         q.qmccpw_price_greeks_batch([0, 0], [q.params(S0=100.0, d=8), q.params(S0=90.0, d=8)], 1024, 2,
                                     q.config(construction=q.PCA))
