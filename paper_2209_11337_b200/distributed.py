@@ -1,14 +1,18 @@
 """Multi-GPU driver: one process per GPU, one NCCL all-reduce per run.
 
-SURVEY.md 8(e): the estimator shards with no data-path exchange -- each rank
-owns a contiguous range of replicates (every cell of a replicate, i.e. all of
-its Sobol' index blocks), runs the fused path kernel over its cells, reduces
-its own replicates to per-replicate sums on the device, and a single
-all_reduce(SUM) over NCCL (NVLink 5 / NVSwitch) combines the [L][stride]
-replicate-sum table.  Every row is nonzero on exactly one rank, so the sum is
-exact (x + 0 = x) and the result is bit-identical to a single-GPU run of the
-same workload.  torch is used only for device memory, streams and the process
-group; all arithmetic runs in libqmccpw.so.
+SURVEY.md 8(e): the estimator shards with no data-path exchange.  The work is
+the grid of cells (replicate, Sobol' index block of 4096 points), numbered
+replicate-major; each rank owns a contiguous range of cells -- a range of
+Sobol' indices within a range of replicates -- runs the fused path kernel over
+them, reduces the replicates it touches to per-replicate partial sums on the
+device, and a single all_reduce(SUM) over NCCL (NVLink 5 / NVSwitch) combines the
+[L][stride] replicate-sum table ("a few dozen partial sums" per replicate).
+When the world size divides L (the weak-scaling bench: 64 replicates per GPU)
+the cell ranges are whole replicates, every row is nonzero on exactly one rank,
+the sum is exact (x + 0 = x) and the result is bit-identical to one GPU; a
+replicate split between two ranks is the sum of their two partial sums
+(deterministic for a given world size).  torch is used only for device memory,
+streams and the process group; all arithmetic runs in libqmccpw.so.
 """
 import ctypes
 
@@ -20,6 +24,18 @@ from . import (Params, qmccpw_cell_count, qmccpw_finalize, qmccpw_partials, qmcc
 def replicate_range(n_replicates, world, rank):
     """Contiguous replicate block of `rank` (balanced to within one replicate)."""
     return n_replicates * rank // world, n_replicates * (rank + 1) // world
+
+
+def cell_range(n_cells, cells_per_rep, world, rank):
+    """Contiguous cell block of `rank` and the replicates it touches: cells are balanced to
+    within one cell; when `world` divides the replicate count the blocks are whole replicates
+    (the same partition as replicate_range)."""
+    n_reps = n_cells // cells_per_rep
+    if n_reps % world == 0:
+        rb, re = replicate_range(n_reps, world, rank)
+        return rb * cells_per_rep, re * cells_per_rep, rb, re
+    cb, ce = n_cells * rank // world, n_cells * (rank + 1) // world
+    return cb, ce, cb // cells_per_rep, (ce + cells_per_rep - 1) // cells_per_rep
 
 
 class DistributedPricer:
@@ -40,10 +56,11 @@ class DistributedPricer:
         self.cfg.device = self.device.index
         self.n_cells, self.per = qmccpw_cell_count(self.plist[0], len(self.options), n_points, n_replicates, cfg)
         self.cells_per_rep = self.n_cells // n_replicates
-        self.rep_begin, self.rep_end = replicate_range(n_replicates, world, rank)
-        self.cell_begin = self.rep_begin * self.cells_per_rep
-        self.cell_end = self.rep_end * self.cells_per_rep
-        self.partials = torch.empty(self.n_cells * self.per, dtype=torch.float64, device=self.device)
+        self.cell_begin, self.cell_end, self.rep_begin, self.rep_end = cell_range(self.n_cells, self.cells_per_rep,
+                                                                                  world, rank)
+        self.partials = torch.zeros(self.n_cells * self.per, dtype=torch.float64, device=self.device)
+        # cells of my boundary replicates that other ranks own stay zero (set once here: the
+        # path kernel only ever writes my cell rows)
         self.rep_sums = torch.zeros(n_replicates * self.per, dtype=torch.float64, device=self.device)
         self.h_rep_sums = torch.empty(n_replicates * self.per, dtype=torch.float64, pin_memory=True)
         self.d2h_bytes = self.h_rep_sums.numel() * 8

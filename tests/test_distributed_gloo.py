@@ -53,6 +53,43 @@ def test_replicate_partition():
             assert max(sizes) - min(sizes) <= 1
 
 
+def test_cell_partition_covers_the_grid_and_keeps_whole_replicates_when_it_can():
+    from paper_2209_11337_b200.distributed import cell_range
+    for L, cpr in ((64, 256), (13, 4), (3, 5), (1, 7), (8, 1)):
+        n = L * cpr
+        for G in range(1, 9):
+            parts = [cell_range(n, cpr, G, g) for g in range(G)]
+            assert parts[0][0] == 0 and parts[-1][1] == n
+            assert all(parts[g][1] == parts[g + 1][0] for g in range(G - 1))       # contiguous, disjoint
+            sizes = [ce - cb for cb, ce, _, _ in parts]
+            for cb, ce, rb, re in parts:
+                assert rb * cpr <= cb and ce <= re * cpr                          # replicates touched
+                if ce > cb:
+                    assert rb == cb // cpr and re == (ce - 1) // cpr + 1
+            if L % G == 0:
+                assert all(cb % cpr == 0 and ce % cpr == 0 for cb, ce, _, _ in parts)
+            else:
+                assert max(sizes) - min(sizes) <= 1
+
+
+def test_split_replicates_sum_to_the_single_process_table():
+    # synthetic per-cell partial rows; each rank sums the rows of its cells per replicate
+    # (other ranks' rows are zero in its buffer) and the all-reduce adds the rank tables
+    from paper_2209_11337_b200.distributed import cell_range
+    rng = np.random.default_rng(3)
+    L, cpr, per = 5, 7, 11
+    cells = rng.normal(size=(L * cpr, per))
+    ref = cells.reshape(L, cpr, per).sum(axis=1)
+    for G in (2, 3, 4):
+        total = np.zeros((L, per))
+        for g in range(G):
+            cb, ce, _, _ = cell_range(L * cpr, cpr, G, g)
+            mine = np.zeros_like(cells)
+            mine[cb:ce] = cells[cb:ce]
+            total += mine.reshape(L, cpr, per).sum(axis=1)
+        assert np.allclose(total, ref, rtol=1e-14, atol=1e-14)
+
+
 def _worker(rank, world, port, outdir):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     import torch
