@@ -746,7 +746,9 @@ static int estimate_impl(const or_option* opt, const or_market* mk, int method, 
         return opt->type == OR_LOOKBACK ? estimate_x1_lookback(&m, M, x, out) : estimate_x1(opt->type, &m, M, x, out);
     double* W = malloc(sizeof(double) * mk->d);
     int rc = 0;
-    if (construction == OR_GPCA) { /* W = M x with the market's GPCA matrix */
+    if (construction == OR_GPCA || (construction == OR_PCA && M != NULL)) {
+        /* W = M x with the call's path matrix (GPCA; PCA: the same pca_matrix that
+         * or_construct would rebuild for every path, built once per call) */
         for (int j = 0; j < mk->d; j++) {
             double acc = 0.0;
             for (int k = 0; k < mk->d; k++) acc += M[j * mk->d + k] * x[k];
@@ -783,7 +785,7 @@ int or_estimate(const or_option* opt, const or_market* mk, int32_t method, int32
     int rc = validate(opt, mk, method, construction, conditioning);
     if (rc) return rc;
     double* M = NULL;
-    if (method == OR_QMC_CPW && (conditioning == OR_COND_X1 || construction == OR_GPCA)) {
+    if (method == OR_QMC_CPW && (conditioning == OR_COND_X1 || construction >= OR_PCA)) {
         M = malloc(sizeof(double) * mk->d * mk->d);
         path_matrix_mk(construction, mk, M);
     }
@@ -800,7 +802,7 @@ int or_path_values(const or_option* opt, const or_market* mk, const or_config* c
     int d = mk->d;
     double* x = malloc(sizeof(double) * d);
     double* M = NULL;
-    if (cfg->method == OR_QMC_CPW && (cfg->conditioning == OR_COND_X1 || cfg->construction == OR_GPCA)) {
+    if (cfg->method == OR_QMC_CPW && (cfg->conditioning == OR_COND_X1 || cfg->construction >= OR_PCA)) {
         M = malloc(sizeof(double) * d * d);
         path_matrix_mk(cfg->construction, mk, M);
     }
@@ -946,7 +948,7 @@ int or_price_greeks(const or_option* opts, int32_t n_opt, const or_market* mk, u
     memset(&jb, 0, sizeof jb);
     jb.opts = opts; jb.n_opt = n_opt; jb.mk = mk; jb.cfg = cfg; jb.N = n_points; jb.L = n_replicates;
     double* M = NULL;
-    if (cfg->method == OR_QMC_CPW && (cfg->conditioning == OR_COND_X1 || cfg->construction == OR_GPCA)) {
+    if (cfg->method == OR_QMC_CPW && (cfg->conditioning == OR_COND_X1 || cfg->construction >= OR_PCA)) {
         M = malloc(sizeof(double) * d * d);
         path_matrix_mk(cfg->construction, mk, M);
     }

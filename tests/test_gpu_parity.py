@@ -314,6 +314,31 @@ def test_bench_launch_config_sampled_replicates(q, O):
                 assert abs(C_gpu - rm[rep, oi, qq]) <= 1e-9 * scale, (rep, oi, qq, C_gpu, rm[rep, oi, qq])
 
 
+@pytest.mark.parametrize("constr,cond", [(1, 0), (2, 0), (2, 1)])
+def test_c3_full_size_sampled_replicates(q, O, constr, cond):
+    """C3 at its full size (lookback, d = 64, 2^18 points x 32 replicates, one launch, incl.
+    the X1 envelope of row f1): replicates 0 and 1 against the oracle at full N."""
+    import torch
+    c = W.CONFIGS["C3"]
+    opts, d, N, L = c["options"], c["d"], c["n_points"], c["n_replicates"]
+    ps = [q.params(d=d)]
+    cfg = qcfg(q, constr, cond)
+    n_cells, per = q.qmccpw_cell_count(ps[0], 1, N, L, cfg)
+    buf = torch.zeros(n_cells * per, dtype=torch.float64, device="cuda:0")
+    q.qmccpw_partials(opts, ps, N, L, cfg, 0, n_cells, buf.data_ptr())
+    torch.cuda.synchronize()
+    part = buf.cpu().numpy().reshape(L, n_cells // L, per)
+    o, rm = O.price_greeks([(opts[0], 100.0)], O.market(d=d), N, 2, ocfg(O, constr, cond), want_rep_means=True)
+    piv = O.pivots(opts[0], 100.0, O.market(d=d))
+    for rep in (0, 1):
+        s1 = part[rep].sum(axis=0)
+        assert s1[8 + 2] == N                                   # every point of the replicate evaluated
+        for qq in range(4):
+            C_gpu = piv[qq] + s1[qq * 2] / N
+            scale = math.sqrt(max(o[0]["within_var"][qq], 0) + o[0]["mean"][qq] ** 2)
+            assert abs(C_gpu - rm[rep, 0, qq]) <= 1e-9 * scale, (rep, qq, C_gpu, rm[rep, 0, qq])
+
+
 # ------------------------------------------------------------------ C5 portfolio kernel
 def _c5_subset(q, d, picks):
     opts = W.c5_portfolio()
