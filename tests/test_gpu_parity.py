@@ -365,6 +365,33 @@ def test_portfolio_path_values(q, O, d, rand):
         assert np.all(err <= tol), (j, o, err.max(axis=0))
 
 
+def test_c5_bench_launch_sampled_options(q, O):
+    """The full C5 launch bench.py times (1024 options, d = 128, 2^18 points x 16 replicates):
+    replicates 0 and 1 of sampled options against the oracle at full N."""
+    import torch
+    d, N, L = 128, 1 << 18, 16
+    types, ps, sel = _c5_subset(q, d, list(range(1024)))
+    cfg = qcfg(q, 2, 0)
+    n_cells, per = q.qmccpw_cell_count(ps[0], 1024, N, L, cfg)
+    buf = torch.zeros(n_cells * per, dtype=torch.float64, device="cuda:0")
+    q.qmccpw_partials(types, ps, N, L, cfg, 0, n_cells, buf.data_ptr())
+    torch.cuda.synchronize()
+    part = buf.cpu().numpy().reshape(L, n_cells // L, per)
+    for i in (5, 389, 1023):  # three families, all three option types
+        o = sel[i]
+        mk = O.market(o["S0"], o["r"], o["sigma"], o["T"], d)
+        ref, rm = O.price_greeks([(o["type"], o["K"])], mk, N, 2, ocfg(O, 2, 0), want_rep_means=True)
+        piv = O.pivots(o["type"], o["K"], mk)
+        floor = np.abs(O.pivots(o["type"], o["S0"], mk))
+        for rep in (0, 1):
+            s1 = part[rep].sum(axis=0)
+            assert s1[1024 * 8 + 2] == N
+            for qq in range(4):
+                C_gpu = piv[qq] + s1[i * 8 + qq * 2] / N
+                scale = math.sqrt(max(ref[0]["within_var"][qq], 0) + ref[0]["mean"][qq] ** 2) + floor[qq]
+                assert abs(C_gpu - rm[rep, 0, qq]) <= 1e-9 * scale, (i, rep, qq, C_gpu, rm[rep, 0, qq])
+
+
 def test_portfolio_means_full_option_count(q, O):
     # all 1024 C5 options through one launch (ragged N, 2 replicates); a sample checked against the oracle
     d, N, L = 128, 4096 + 333, 2
