@@ -129,7 +129,7 @@ typedef struct {
  *   NULL p or out.
  * EUNSUPPORTED: BB with d != 2^m (Alg. 4 is defined for 2^m steps);
  *   LR_MC with a construction other than STD;
- *   MC_CPW / MC_AV_CPW with PCA or X1;
+ *   MC_CPW / MC_AV_CPW with PCA, GPCA or X1;
  *   d > 256 on the GPU. */
 int qmccpw_price_greeks(int32_t option, const qmccpw_params* p, uint64_t n_points, uint32_t n_replicates,
                         const qmccpw_config* cfg, qmccpw_result* out);
@@ -173,7 +173,9 @@ int qmccpw_partials(const int32_t* options, const qmccpw_params* p, int32_t n_op
  * sequential cell order) into rows rep of d_rep_sums (device, caller-owned,
  * n_replicates * partial_doubles_per_cell doubles); other rows untouched.
  * Enqueue only (cfg->stream).  Ranks owning disjoint replicate ranges can
- * all-reduce zero-initialised d_rep_sums exactly. */
+ * all-reduce zero-initialised d_rep_sums exactly; a replicate whose cells are
+ * split between ranks (each rank's other cells zero in its d_partials) sums to
+ * the two partial sums (deterministic, equal to rounding). */
 int qmccpw_replicate_sums(const double* d_partials, const qmccpw_params* p, int32_t n_options, uint64_t n_points,
                           uint32_t n_replicates, const qmccpw_config* cfg, uint32_t rep_begin, uint32_t rep_end,
                           double* d_rep_sums);
