@@ -117,7 +117,8 @@ typedef struct {
     double mean[4], se[4], sigma_run[4], within_var[4];
     uint64_t n_points;
     uint32_t n_replicates;
-    uint64_t newton_unconverged; /* X1 paths whose Newton step did not reach 1e-13 (expect 0) */
+    uint64_t newton_unconverged; /* X1 paths whose threshold iteration (Halley) had not converged
+                                    after 8 updates: last update > 1e-6 relative (expect 0) */
     uint64_t argmax_near_ties;   /* lookback paths with two S~(t_j) within 1e-12 in log (expect 0) */
 } qmccpw_result;
 

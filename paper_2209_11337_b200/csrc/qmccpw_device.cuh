@@ -298,6 +298,18 @@ struct X1Sums {
     double u, Dst, Qst, Vst, sumW, sumWv;
 };
 
+// X1 threshold step for f(u) = ln S(u) - ln(dK), S(u) = sum_j e^{c_j + sigma a_j u}:
+// f' = sigma m1, f'' = sigma^2 (m2 - m1^2), m1 = SA/S, m2 = SAA/S.  Halley's update
+// du = (f/f') / (1 - f f''/(2 f'^2)), the Newton step when the correction is large (far from
+// the root); f is convex-increasing in u for a_j > 0, so both steps move toward the root.
+__device__ __forceinline__ double halley_step(double h, double S, double SA, double SAA, double sg) {
+    const double invS = 1.0 / S;
+    const double m1 = SA * invS, m2 = SAA * invS;
+    const double newton = h / (sg * m1);
+    const double corr = 0.5 * h * (m2 - m1 * m1) / (m1 * m1);
+    return fabs(corr) < 0.5 ? newton / (1.0 - corr) : newton;
+}
+
 __device__ __forceinline__ X1Sums x1_solve(const PathArgs& P, int o, bool arith, const double* cb, int stride,
                                            unsigned& unconverged) {
     const int d = P.d;
@@ -313,7 +325,7 @@ __device__ __forceinline__ X1Sums x1_solve(const PathArgs& P, int o, bool arith,
     double u = fmin(u_hi, (lnK - sumc / d) / (sg * P.mean_a));
     bool conv = false;
     for (int it = 0; it < kNewtonMax; ++it) {
-        double S = 0.0, SA = 0.0;
+        double S = 0.0, SA = 0.0, SAA = 0.0;
         int j = 0;
 #pragma unroll 1
         for (; j + 1 < d; j += 2) {
@@ -322,18 +334,20 @@ __device__ __forceinline__ X1Sums x1_solve(const PathArgs& P, int o, bool arith,
             fast_exp_x2(fma(sg * aa, u, cb[j * stride]), fma(sg * ab, u, cb[(j + 1) * stride]), Ea, Eb);
             S += Ea;
             SA = fma(aa, Ea, SA);
+            SAA = fma(aa * aa, Ea, SAA);
             S += Eb;
             SA = fma(ab, Eb, SA);
+            SAA = fma(ab * ab, Eb, SAA);
         }
         if (j < d) {
             const double aj = P.a[j];
             const double E = fast_exp(fma(sg * aj, u, cb[j * stride]));
             S += E;
             SA = fma(aj, E, SA);
+            SAA = fma(aj * aj, E, SAA);
         }
-        const double h = fast_log(S) - lndK;
-        const double du = h * S / (sg * SA);
-        conv = fabs(du) <= 1e-13 * fmax(1.0, fabs(u));
+        const double du = halley_step(fast_log(S) - lndK, S, SA, SAA, sg);
+        conv = fabs(du) <= kHalleyTol * fmax(1.0, fabs(u));
         u = fmin(fmax(u - du, u_lo), u_hi);
         if (it + 1 >= kNewtonIt && __all_sync(__activemask(), conv)) break;
     }

@@ -9,8 +9,11 @@ namespace qmccpw {
 constexpr int kMaxOpt = 3;            // options fused on one path per launch
 constexpr int kCellPoints = 4096;     // points of one replicate per cell (block)
 constexpr int kMaxDimGpu = 256;       // largest d the kernels support
-constexpr int kNewtonIt = 4;          // fixed Newton updates (X1), then up to kNewtonMax
+constexpr int kNewtonIt = 2;          // X1 threshold: at least 2 Halley updates, then up to kNewtonMax
 constexpr int kNewtonMax = 8;
+// Halley's iteration converges cubically: once an update is below kHalleyTol (relative),
+// the error it leaves is ~C |du|^3 << 1e-16, so that update is the last (predictive stop)
+constexpr double kHalleyTol = 1e-6;
 
 enum Construction { kStd = 0, kBB = 1, kPca = 2 };
 enum Conditioning { kW1 = 0, kX1 = 1 };

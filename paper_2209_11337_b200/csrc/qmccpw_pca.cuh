@@ -211,7 +211,7 @@ __global__ void __launch_bounds__(128, pca_min_blocks<COND, KF>()) pca_kernel(co
                     bool conv = false;
 #pragma unroll 1
                     for (int it = 0; it < kNewtonMax; ++it) {
-                        double S = 0.0, SA = 0.0;
+                        double S = 0.0, SA = 0.0, SAA = 0.0;
 #pragma unroll
                         for (int jt = 0; jt < JT; ++jt) {
                             const int j0 = 8 * jt + 2 * r4;
@@ -223,14 +223,16 @@ __global__ void __launch_bounds__(128, pca_min_blocks<COND, KF>()) pca_kernel(co
                             Eb = (j0 + 1 < d) ? Eb : 0.0;
                             S += Ea;
                             SA = fma(aa, Ea, SA);
+                            SAA = fma(aa * aa, Ea, SAA);
                             S += Eb;
                             SA = fma(ab, Eb, SA);
+                            SAA = fma(ab * ab, Eb, SAA);
                         }
                         S = quad_sum(S);
                         SA = quad_sum(SA);
-                        const double h = fast_log(S) - lndK;
-                        const double du = h * S / (sg * SA);
-                        conv = !valid || fabs(du) <= 1e-13 * fmax(1.0, fabs(u));
+                        SAA = quad_sum(SAA);
+                        const double du = halley_step(fast_log(S) - lndK, S, SA, SAA, sg);
+                        conv = !valid || fabs(du) <= kHalleyTol * fmax(1.0, fabs(u));
                         u = fmin(fmax(u - du, ulo), uhi);
                         if (it + 1 >= kNewtonIt && __all_sync(0xffffffffu, conv)) break;
                     }
