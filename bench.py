@@ -327,9 +327,9 @@ def main():
                              "r=0.1, d=128, PCA-W1 (portfolio kernel)") if args.workload == "C5" else
                             ("C4: arithmetic+binary+lookback Asian calls fused on shared paths, S0=K=100, sigma=0.2, "
                              "r=0.1, T=1, d=64, " + {(1, 0): "BB-W1 (QMC+BB-CPW)", (0, 0): "STD-W1 (QMC-CPW)",
-                                                     (2, 0): "PCA-W1", (2, 1): "PCA-X1 (Newton)",
-                                                     (0, 1): "STD-X1 (Newton)", (1, 1): "BB-X1 (Newton)",
-                                                     (3, 0): "GPCA-W1 (f3)", (3, 1): "GPCA-X1 (Newton, f3)"}.get(
+                                                     (2, 0): "PCA-W1", (2, 1): "PCA-X1 (Halley threshold)",
+                                                     (0, 1): "STD-X1 (Halley threshold)", (1, 1): "BB-X1 (Halley threshold)",
+                                                     (3, 0): "GPCA-W1 (f3)", (3, 1): "GPCA-X1 (Halley threshold, f3)"}.get(
                                  (args.construction, args.conditioning), "custom"))
                             + {1: ", digital shift only", 3: ", plain Sobol'", 4: ", nested Owen scrambling (f4)"}.get(
                                 args.randomization, ""),
