@@ -181,6 +181,7 @@ def main():
                     help="0 LMS + digital shift (default), 1 shift, 3 none, 4 nested Owen scrambling (row f4)")
     ap.add_argument("--workload", default="C4", choices=["C4", "C5"],
                     help="C4: 3 exotics fused, d=64 (the BASELINE metric); C5: 1024-option portfolio, d=128")
+    ap.add_argument("--options", default=None, help="comma-separated option types (0 arith, 1 binary, 2 lookback)")
     ap.add_argument("--points", type=int, default=None)
     ap.add_argument("--reps-per-gpu", type=int, default=None)
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -215,7 +216,9 @@ def main():
         c = W.CONFIGS[W.HEADLINE]
         options, d = c["options"], c["d"]
         if args.conditioning == W.X1:
-            options = [W.ARITH, W.BINARY]
+            options = [W.ARITH, W.BINARY]  # the DMMA Newton-threshold kernel; --options 0,1,2 adds the lookback (f1)
+        if args.options:
+            options = [int(t) for t in args.options.split(",")]
         N = args.points or c["n_points"]
         L = (args.reps_per_gpu or c["n_replicates"]) * world
         plist = [q.params(S0=W.S0, K=100.0, r=W.R, sigma=W.SIGMA, T=W.T, d=d) for _ in options]
@@ -332,7 +335,8 @@ def main():
                                                      (3, 0): "GPCA-W1 (f3)", (3, 1): "GPCA-X1 (Halley threshold, f3)"}.get(
                                  (args.construction, args.conditioning), "custom"))
                             + {1: ", digital shift only", 3: ", plain Sobol'", 4: ", nested Owen scrambling (f4)"}.get(
-                                args.randomization, ""),
+                                args.randomization, "")
+                            + (f", options {args.options}" if args.options else ""),
                 "points_per_replicate": N, "replicates_per_gpu": L // world, "replicates_total": L,
                 "global_batch": N * L, "seq_len": d, "parallelism": f"dp{world} (replicate-partitioned)",
                 "option_paths_per_s": value * len(options), "greek_sets_per_s": value * len(options),

@@ -420,34 +420,54 @@ __device__ __forceinline__ void x1_lookback(const PathArgs& P, int o, const doub
             j0 = j;
         }
     }
-    // active line at u*: the maximum there; on ties the steeper one (it dominates just after)
-    int act = 0;
-    double best = -CUDART_INF, bact = 0.0;
+    // The upper envelope of the lines c_j + b_j u, b_j = sigma a_j, by the monotone
+    // convex-hull pass (O(d), no divisions): every construction has a_j nondecreasing in
+    // j (STD: equal; BB: t_j/sqrt(T); PCA / GPCA: positive increasing first column), so
+    // lines arrive by slope; a line is dropped when the next one overtakes it no later
+    // than it overtakes its predecessor.  Equal slopes keep the higher line.
+    uint8_t hull[kMaxDimGpu];  // line indices (d <= 256)
+    int top = 0;
+    if (__ldg(P.a) == __ldg(P.a + d - 1)) {  // STD: all slopes equal -> the single highest line (lowest j on ties)
+        int best = 0;
+        for (int j = 1; j < d; ++j) best = cb[j * stride] > cb[best * stride] ? j : best;
+        hull[top++] = (uint8_t)best;
+    } else
     for (int j = 0; j < d; ++j) {
-        const double bj = sg * __ldg(P.a + j);
-        const double v = fma(bj, ustar, cb[j * stride]);
-        if (v > best || (v == best && bj > bact)) {
-            best = v;
-            act = j;
-            bact = bj;
-        }
-    }
-    double J = 0.0, V = 0.0, lo = ustar;
-    for (int seg = 0; seg < d; ++seg) {
-        const double cact = cb[act * stride];
-        double hi = CUDART_INF, bn = 0.0;
-        int nxt = -1;
-        for (int i = 0; i < d; ++i) {
-            const double bi = sg * __ldg(P.a + i);
-            if (bi > bact) {
-                const double x = (cact - cb[i * stride]) / (bi - bact);
-                if (x < hi || (x == hi && bi > bn)) {
-                    hi = x;
-                    nxt = i;
-                    bn = bi;
-                }
+        const double b3 = sg * __ldg(P.a + j), c3 = cb[j * stride];
+        if (top > 0) {
+            const int l2 = hull[top - 1];
+            const double b2 = sg * __ldg(P.a + l2);
+            if (b2 == b3) {
+                if (c3 <= cb[l2 * stride]) continue;
+                --top;
             }
         }
+        while (top >= 2) {
+            const int l1 = hull[top - 2], l2 = hull[top - 1];
+            const double b1 = sg * __ldg(P.a + l1), b2 = sg * __ldg(P.a + l2);
+            const double c1 = cb[l1 * stride], c2 = cb[l2 * stride];
+            // l2 is never the maximum iff x(l1, l3) <= x(l1, l2), x(p, q) = (c_p - c_q) / (b_q - b_p)
+            if ((c1 - c3) * (b2 - b1) <= (c1 - c2) * (b3 - b1)) --top;
+            else break;
+        }
+        hull[top++] = (uint8_t)j;
+    }
+    // the envelope segment that contains u*: on a breakpoint tie the steeper line (it
+    // dominates just after)
+    int k = 0;
+    while (k + 1 < top) {
+        const int l1 = hull[k], l2 = hull[k + 1];
+        const double x = (cb[l1 * stride] - cb[l2 * stride]) / (sg * (__ldg(P.a + l2) - __ldg(P.a + l1)));
+        if (x > ustar) break;
+        ++k;
+    }
+    double J = 0.0, V = 0.0, lo = ustar;
+    for (; k < top; ++k) {
+        const int act = hull[k];
+        const double bact = sg * __ldg(P.a + act), cact = cb[act * stride];
+        const int nxt = (k + 1 < top) ? hull[k + 1] : -1;
+        double hi = CUDART_INF;
+        if (nxt >= 0) hi = (cact - cb[nxt * stride]) / (sg * __ldg(P.a + nxt) - bact);
         hi = fmax(hi, lo);
         const double aa = bact / sg;
         const double tj = (double)(act + 1) * P.t1;
@@ -461,10 +481,7 @@ __device__ __forceinline__ void x1_lookback(const PathArgs& P, int o, const doub
         }
         J = fma(w, Qlo - Qhi, J);
         V = fma(w, (Rj - sg * tj + sg * aa * aa) * (Qlo - Qhi) + aa * (plo - phi_hi), V);
-        if (nxt < 0) break;
         lo = hi;
-        act = nxt;
-        bact = bn;
     }
     const double D = P.Dfac, S0 = P.S0, K = P.K[o];
     double Qu, Q2, ph, ph2;
