@@ -187,7 +187,8 @@ int tpb_log2_for(const qmccpw_config& c, int d, int n_opt) {
     for (int lg = 7; lg >= 5; --lg) {
         size_t tpb = (size_t)1 << lg, nw = tpb / 32;
         size_t b = (size_t)n_opt * 8 * tpb * 8;
-        const bool mma = c.method == QMCCPW_QMC_CPW && c.construction == QMCCPW_PCA && c.conditioning == QMCCPW_COND_W1;
+        const bool mma = c.method == QMCCPW_QMC_CPW && c.construction == QMCCPW_PCA &&
+                         (c.conditioning == QMCCPW_COND_W1 || ((d + 7) & ~7) <= 128);  // X tile
         if (mma) b += (size_t)((d + 7) & ~7) * (tpb + 8) * 8;
         else if (need_buf) b += (size_t)d * tpb * 8;
         if (two_buf) b += (size_t)d * tpb * 8;

@@ -38,6 +38,9 @@ __global__ void __launch_bounds__(128, paths_min_blocks<CONSTR, COND, METHOD>())
     constexpr bool kNeedBuf = (METHOD == kQmc) && (CONSTR == kPca || COND == kX1);
     constexpr bool kTwoBuf = (METHOD == kQmc) && (CONSTR == kPca && COND == kX1);
     constexpr bool kWarpMma = (METHOD == kQmc) && (CONSTR == kPca && COND == kW1);
+    // X tile [M_ld][tpb + 8] in buf0 for the DMMA contraction: PCA-W1 always, PCA-X1 up to
+    // d = 128 (beyond, the X tile and the c_j columns do not both fit: per-thread matvec)
+    const bool kMmaX = (METHOD == kQmc) && CONSTR == kPca && (COND == kW1 || P.M_ld <= 128);
 
     // shared memory carve-up (8-byte aligned first):
     //   buf0, buf1 [d][tpb] | vt [d][32] | sh [d] | G [d][32] | pad | HW [2][2][nw][d] (>= 1 KB)
@@ -47,7 +50,7 @@ __global__ void __launch_bounds__(128, paths_min_blocks<CONSTR, COND, METHOD>())
     const int n_acc = P.n_opt * 8;
     const int lane = tid & 31;
     double* buf0 = reinterpret_cast<double*>(smem_raw);
-    double* buf1 = buf0 + (kWarpMma ? (size_t)P.M_ld * (tpb + 8) : (kNeedBuf ? (size_t)d * tpb : 0));
+    double* buf1 = buf0 + (kMmaX ? (size_t)P.M_ld * (tpb + 8) : (kNeedBuf ? (size_t)d * tpb : 0));
     uint32_t* vt = reinterpret_cast<uint32_t*>(buf1 + (kTwoBuf ? (size_t)d * tpb : 0));
     uint32_t* sh = vt + (METHOD == kQmc ? (size_t)d * 32 : 0);
     uint32_t* G = sh + (METHOD == kQmc ? d : 0);
@@ -79,8 +82,10 @@ __global__ void __launch_bounds__(128, paths_min_blocks<CONSTR, COND, METHOD>())
     __shared__ double wacc[4 * 32];  // per-warp centred sums (tpb <= 128)
     wacc[tid] = 0.0;
     __syncwarp();
-    if (kWarpMma)  // zero X rows d..dp-1 (the padded K of the mma tiles)
+    if (kMmaX) {  // zero X rows d..dp-1 (the padded K of the mma tiles); X1: also row 0 (x_1 := 0)
         for (int r = d; r < P.M_ld; ++r) buf0[(size_t)r * (tpb + 8) + tid] = 0.0;
+        if (COND == kX1) buf0[tid] = 0.0;
+    }
     unsigned unconverged = 0, ties = 0, npts = 0;
 
     for (int a = 0; a < ppt; ++a) {
@@ -451,7 +456,8 @@ __global__ void __launch_bounds__(128, paths_min_blocks<CONSTR, COND, METHOD>())
                     cb[(j - 1) * tpb] = P.lnS0 + P.omega * (double)j * P.t1 + P.sigma * Rj;
                     Wl = Rj;
                 }
-            } else {
+            } else if (!kMmaX) {
+                // PCA, d > 128: per-thread R = M x (x_1 := 0) from shared memory
                 double* xb = buf0 + tid;
                 int kk = 1;
 #pragma unroll 1
@@ -462,27 +468,60 @@ __global__ void __launch_bounds__(128, paths_min_blocks<CONSTR, COND, METHOD>())
                     xb[(kk + 1) * tpb] = xc;
                 }
                 if (kk < d) xb[kk * tpb] = normal_from_u32(sob.get(kk));
-                int j = 0;
 #pragma unroll 1
-                for (; j + 1 < d; j += 2) {
-                    const double* Ma = P.M + (size_t)j * P.M_ld;
-                    const double* Mb = Ma + P.M_ld;
-                    double Ra = 0.0, Rb = 0.0;
-#pragma unroll 4
-                    for (int q = 1; q < d; ++q) {
-                        const double xq = xb[q * tpb];
-                        Ra = fma(__ldg(Ma + q), xq, Ra);
-                        Rb = fma(__ldg(Mb + q), xq, Rb);
-                    }
-                    cb[j * tpb] = P.lnS0 + P.omega * (double)(j + 1) * P.t1 + P.sigma * Ra;
-                    cb[(j + 1) * tpb] = P.lnS0 + P.omega * (double)(j + 2) * P.t1 + P.sigma * Rb;
-                }
-                if (j < d) {
+                for (int j = 0; j < d; ++j) {
                     const double* Ma = P.M + (size_t)j * P.M_ld;
                     double Ra = 0.0;
-                    for (int q = 1; q < d; ++q) Ra = fma(__ldg(Ma + q), xb[q * tpb], Ra);
+#pragma unroll 4
+                    for (int q2 = 1; q2 < d; ++q2) Ra = fma(__ldg(Ma + q2), xb[q2 * tpb], Ra);
                     cb[j * tpb] = P.lnS0 + P.omega * (double)(j + 1) * P.t1 + P.sigma * Ra;
                 }
+            } else {
+                // PCA: R = X M^T (x_1 := 0) on the FP64 tensor cores, as in the W1 branch:
+                // X[k][path] in shared memory (row stride tpb + 8), mma.sync.m8n8k4.f64 over
+                // the warp's 32 paths, and each lane writes its tile's c_j into the owning
+                // threads' columns of cb
+                const int XS = tpb + 8, dp = P.M_ld;
+                double* xcol = buf0 + tid;
+                int kk = 1;
+#pragma unroll 1
+                for (; kk + 1 < d; kk += 2) {
+                    double xa, xc;
+                    normal_from_u32_x2(sob.get(kk), sob.get(kk + 1), xa, xc);
+                    xcol[kk * XS] = xa;
+                    xcol[(kk + 1) * XS] = xc;
+                }
+                if (kk < d) xcol[kk * XS] = normal_from_u32(sob.get(kk));
+                __syncwarp();
+                const int q = lane >> 2, r4 = lane & 3, wbase = tid & ~31;
+                const double* Xk = buf0 + wbase + (size_t)r4 * XS + q;
+#pragma unroll 1
+                for (int jt = 0; jt < dp; jt += 8) {
+                    double acc[4][2];
+#pragma unroll
+                    for (int rt = 0; rt < 4; ++rt) acc[rt][0] = acc[rt][1] = 0.0;
+                    const double* Mrow = P.M + (size_t)(jt + q) * dp + r4;
+#pragma unroll 2
+                    for (int kt = 0; kt < dp; kt += 4) {
+                        const double bfrag = __ldg(Mrow + kt);
+                        const double* Xr = Xk + (size_t)kt * XS;
+#pragma unroll
+                        for (int rt = 0; rt < 4; ++rt)
+                            asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+                                         : "+d"(acc[rt][0]), "+d"(acc[rt][1])
+                                         : "d"(Xr[8 * rt]), "d"(bfrag));
+                    }
+                    const int j0 = jt + 2 * r4;  // lane (q, r4) holds R at dates j0, j0 + 1 of paths 8 rt + q
+#pragma unroll
+                    for (int rt = 0; rt < 4; ++rt) {
+                        double* col = buf1 + wbase + 8 * rt + q;
+                        if (j0 < d) col[(size_t)j0 * tpb] = P.lnS0 + P.omega * (double)(j0 + 1) * P.t1 + P.sigma * acc[rt][0];
+                        if (j0 + 1 < d)
+                            col[(size_t)(j0 + 1) * tpb] = P.lnS0 + P.omega * (double)(j0 + 2) * P.t1 + P.sigma * acc[rt][1];
+                    }
+                }
+                __syncwarp();
+
             }
             tail_x1_all(P, cb, tpb, f, unconverged);
         }
@@ -510,7 +549,8 @@ static size_t path_smem_bytes(const PathArgs& a, int constr, int cond, int metho
     const bool need_buf = method == kQmc && (constr == kPca || cond == kX1);
     const bool two_buf = method == kQmc && constr == kPca && cond == kX1;
     size_t b = 0;
-    if (method == kQmc && constr == kPca && cond == kW1) b += (size_t)a.M_ld * (tpb + 8) * sizeof(double);
+    if (method == kQmc && constr == kPca && (cond == kW1 || a.M_ld <= 128))
+        b += (size_t)a.M_ld * (tpb + 8) * sizeof(double);  // X tile (DMMA)
     else if (need_buf) b += (size_t)a.d * tpb * sizeof(double);
     if (two_buf) b += (size_t)a.d * tpb * sizeof(double);
     size_t hw = 0;
