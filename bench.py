@@ -181,6 +181,8 @@ def main():
                     help="0 LMS + digital shift (default), 1 shift, 3 none, 4 nested Owen scrambling (row f4)")
     ap.add_argument("--workload", default="C4", choices=["C4", "C5"],
                     help="C4: 3 exotics fused, d=64 (the BASELINE metric); C5: 1024-option portfolio, d=128")
+    ap.add_argument("--method", type=int, default=0,
+                    help="0 QMC-CPW (default), 1 LR+MC (STD), 2 MC-CPW, 3 MC+AV-CPW (STD/BB, W1; row f2)")
     ap.add_argument("--options", default=None, help="comma-separated option types (0 arith, 1 binary, 2 lookback)")
     ap.add_argument("--points", type=int, default=None)
     ap.add_argument("--reps-per-gpu", type=int, default=None)
@@ -222,8 +224,8 @@ def main():
         N = args.points or c["n_points"]
         L = (args.reps_per_gpu or c["n_replicates"]) * world
         plist = [q.params(S0=W.S0, K=100.0, r=W.R, sigma=W.SIGMA, T=W.T, d=d) for _ in options]
-    ckw = dict(construction=args.construction, conditioning=args.conditioning, randomization=args.randomization,
-               seed=W.SEED, device=local)
+    ckw = dict(method=args.method, construction=args.construction, conditioning=args.conditioning,
+               randomization=args.randomization, seed=W.SEED, device=local)
     cfg = q.config(**ckw)
     pricer = DistributedPricer(options, plist, N, L, cfg, dev, rank, world)
 
@@ -302,6 +304,8 @@ def main():
     else:
         per_path = fp64_model_per_path(d, args.construction, args.conditioning, len(options),
                                        arith_x1=int(args.conditioning == W.X1))
+        if args.method == 3:  # MC+AV-CPW: the antithetic path's exps, accumulators and tails as well
+            per_path += d * (17 + 6) + len(options) * 160
     launch_paths = N * (L // world)
     achieved = 2.0 * per_path * launch_paths / (kernel_avg_ms / 1e3) / 1e12
     traffic = None
@@ -336,7 +340,9 @@ def main():
                                  (args.construction, args.conditioning), "custom"))
                             + {1: ", digital shift only", 3: ", plain Sobol'", 4: ", nested Owen scrambling (f4)"}.get(
                                 args.randomization, "")
-                            + (f", options {args.options}" if args.options else ""),
+                            + (f", options {args.options}" if args.options else "")
+                            + {1: ", LR+MC", 2: ", MC-CPW (Philox)", 3: ", MC+AV-CPW (Philox, antithetic)"}.get(
+                                args.method, ""),
                 "points_per_replicate": N, "replicates_per_gpu": L // world, "replicates_total": L,
                 "global_batch": N * L, "seq_len": d, "parallelism": f"dp{world} (replicate-partitioned)",
                 "option_paths_per_s": value * len(options), "greek_sets_per_s": value * len(options),
