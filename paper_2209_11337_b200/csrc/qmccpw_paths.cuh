@@ -37,7 +37,6 @@ __global__ void __launch_bounds__(128, paths_min_blocks<CONSTR, COND, METHOD>())
     const int ppt = kCellPoints >> tpb_log2;
     constexpr bool kNeedBuf = (METHOD == kQmc) && (CONSTR == kPca || COND == kX1);
     constexpr bool kTwoBuf = (METHOD == kQmc) && (CONSTR == kPca && COND == kX1);
-    constexpr bool kWarpMma = (METHOD == kQmc) && (CONSTR == kPca && COND == kW1);
     // X tile [M_ld][tpb + 8] in buf0 for the DMMA contraction: PCA-W1 always, PCA-X1 up to
     // d = 128 (beyond, the X tile and the c_j columns do not both fit: per-thread matvec)
     const bool kMmaX = (METHOD == kQmc) && CONSTR == kPca && (COND == kW1 || P.M_ld <= 128);
