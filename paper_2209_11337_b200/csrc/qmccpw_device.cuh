@@ -149,27 +149,8 @@ __device__ __forceinline__ void sobol_build_hw(const uint32_t* vt, const uint32_
 // (P:599 with the 1/d removed, reading 3).  Near-ties are tracked with the
 // runner-up exponent.
 // ---------------------------------------------------------------------------
-// MC-CPW / MC+AV-CPW / LR+MC normals: Philox4x32-10, counter (k_lo, k_hi, j/4,
-// (rep<<8)|0x02), word j%4 (the paper's PSEUDO generator).
-__device__ __forceinline__ uint32_t pick4(const uint32_t c[4], int w) {
-    return w == 0 ? c[0] : (w == 1 ? c[1] : (w == 2 ? c[2] : c[3]));
-}
-__device__ __forceinline__ void mc_normal_pair(const PathArgs& P, uint32_t rep, uint64_t k, int ja, int jb, double& xa,
-                                               double& xb) {
-    uint32_t ca[4] = {(uint32_t)k, (uint32_t)(k >> 32), (uint32_t)(ja >> 2), (rep << 8) | 0x02u};
-    philox4x32_10(ca, (uint32_t)P.seed, (uint32_t)(P.seed >> 32));
-    const uint32_t ya = pick4(ca, ja & 3);
-    uint32_t yb;
-    if ((jb >> 2) == (ja >> 2)) {
-        yb = pick4(ca, jb & 3);
-    } else {
-        uint32_t cb[4] = {(uint32_t)k, (uint32_t)(k >> 32), (uint32_t)(jb >> 2), (rep << 8) | 0x02u};
-        philox4x32_10(cb, (uint32_t)P.seed, (uint32_t)(P.seed >> 32));
-        yb = pick4(cb, jb & 3);
-    }
-    normal_from_u32_x2(ya, yb, xa, xb);
-}
-
+// (MC-CPW / MC+AV-CPW / LR+MC normals, drawn in paths_kernel and lr_path: Philox4x32-10,
+// counter (k_lo, k_hi, j/4, (rep<<8)|0x02), word j%4 -- the paper's PSEUDO generator.)
 struct W1Acc {
     double sumS, sumI, emax, esec, ymax;
     __device__ __forceinline__ void reset() {
@@ -226,17 +207,6 @@ struct NormalFifo {
     __device__ __forceinline__ double next(const SobolBlock& sob, DimAt dim_at) {
         if (have == 0) {
             normal_from_u32_x2(sob.get(dim_at(0)), sob.get(dim_at(1)), x0, x1);
-            have = 2;
-        }
-        const double r = (have == 2) ? x0 : x1;
-        --have;
-        return r;
-    }
-    // same, with an arbitrary pair drawer draw(dim_a, dim_b, x_a, x_b)
-    template <class Draw, class DimAt>
-    __device__ __forceinline__ double next_from(Draw draw, DimAt dim_at) {
-        if (have == 0) {
-            draw(dim_at(0), dim_at(1), x0, x1);
             have = 2;
         }
         const double r = (have == 2) ? x0 : x1;
