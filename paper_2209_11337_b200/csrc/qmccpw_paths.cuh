@@ -64,10 +64,10 @@ __global__ void __launch_bounds__(128, paths_min_blocks<CONSTR, COND, METHOD>())
     const uint64_t kt = K0 + (uint64_t)tid;
     SobolBlock sob{G, HW, d, nw, (int)(kt & 31), (int)((kt >> 5) & (uint64_t)(nw - 1)), (int)((kt >> tpb_log2) - Ab),
                    OWEN ? sh : nullptr};
-    // BB-W1 stages the replicate's tables in the bridge's consumption order (row i =
+    // BB stages the replicate's tables in the bridge's consumption order (row i =
     // Sobol' dimension bb_seq[i]), so the i-th normal reads row i: no per-normal
     // dimension lookup
-    constexpr bool kPerm = (CONSTR == kBB && COND == kW1 && METHOD == kQmc);
+    constexpr bool kPerm = (CONSTR == kBB && METHOD == kQmc);
     math_tables_load(tid, tpb);
     if (METHOD != kQmc) __syncthreads();  // QMC: the barrier below publishes the tables
     if (METHOD == kQmc) {
@@ -434,7 +434,7 @@ __global__ void __launch_bounds__(128, paths_min_blocks<CONSTR, COND, METHOD>())
                 NormalFifo fifo;
                 fifo.reset();
                 int pos = 1;
-                auto dim_at = [&](int o) { return (int)P.bb_seq[pos + o]; };
+                auto dim_at = [&](int o) { return pos + o; };  // tables in consumption order (kPerm)
                 double stW[12];
                 int sp = 0;
                 stW[0] = 0.0;
