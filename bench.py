@@ -40,18 +40,22 @@ FP64_LANES_PER_SM = 64          # FP64 FMA lanes per SM per clock (B200)
 SM_MAX_MHZ_FALLBACK = 1965.0    # B200_PROFILING.md / MEASURED_PEAKS.json sm_max_mhz
 
 
-def fp64_model_per_path(d, constr, cond, n_opt, arith_x1=0):
+def fp64_model_per_path(d, constr, cond, n_opt, arith_x1=0, n_lookback_x1=0):
     """Algorithmic FP64 lane-instructions per underlying path (SURVEY.md 8(d)
     planning model, fixed constants -- independent of how the kernel is written):
     c_icdf = 50 (branch-light FP64 inverse normal), c_exp = 17, c_tail = 160
-    per option (log + 2 erfc + exp + ~30 FMA), c_W = 1 (STD) / 2 (BB) / d (PCA)."""
+    per option (log + 2 erfc + exp + ~30 FMA), c_W = 1 (STD) / 2 (BB) / d (PCA).
+    X1: 4 Newton passes per arithmetic / binary option (SURVEY's count); a lookback under
+    X1 has a closed-form threshold and one envelope pass instead (row f1)."""
     c_icdf, c_exp, c_tail = 50, 17, 160
     c_w = {0: 1, 1: 2, 2: d, 3: d}[constr]  # GPCA: a rotated PCA matrix, same dense contraction
     d_icdf = d - 1 if (cond == 1 or constr == 0) else d
     if cond == 0:
         return d_icdf * c_icdf + d * (c_exp + c_w + 6) + n_opt * c_tail
     newton = 4 * d * (c_exp + 3)
-    return d_icdf * c_icdf + d * c_w + n_opt * (newton + d * (c_exp + 3) + c_tail) + arith_x1 * d * (c_exp + 60 + 4)
+    n_newton = n_opt - n_lookback_x1
+    return (d_icdf * c_icdf + d * c_w + n_newton * (newton + d * (c_exp + 3) + c_tail)
+            + n_lookback_x1 * (d * (c_exp + 3) + c_tail) + arith_x1 * d * (c_exp + 60 + 4))
 
 
 def measured_peaks():
@@ -303,7 +307,9 @@ def main():
         per_path = d * 50 + d * d + 8 * d * (17 + 6) + len(options) * 160
     else:
         per_path = fp64_model_per_path(d, args.construction, args.conditioning, len(options),
-                                       arith_x1=int(args.conditioning == W.X1))
+                                       arith_x1=int(args.conditioning == W.X1 and W.ARITH in options),
+                                       n_lookback_x1=sum(1 for t in options if t == W.LOOKBACK)
+                                       if args.conditioning == W.X1 else 0)
         if args.method == 3:  # MC+AV-CPW: the antithetic path's exps, accumulators and tails as well
             per_path += d * (17 + 6) + len(options) * 160
     launch_paths = N * (L // world)
