@@ -401,26 +401,39 @@ __device__ __forceinline__ void x1_lookback(const PathArgs& P, int o, const doub
         int best = 0;
         for (int j = 1; j < d; ++j) best = cb[j * stride] > cb[best * stride] ? j : best;
         hull[top++] = (uint8_t)best;
-    } else
-    for (int j = 0; j < d; ++j) {
-        const double b3 = sg * __ldg(P.a + j), c3 = cb[j * stride];
-        if (top > 0) {
-            const int l2 = hull[top - 1];
-            const double b2 = sg * __ldg(P.a + l2);
-            if (b2 == b3) {
-                if (c3 <= cb[l2 * stride]) continue;
-                --top;
+    } else {
+        // the top two hull lines (T = top, S = second) stay in registers; a pop reloads S
+        double bT = 0.0, cT = 0.0, bS = 0.0, cS = 0.0;
+        for (int j = 0; j < d; ++j) {
+            const double b3 = sg * __ldg(P.a + j), c3 = cb[j * stride];
+            if (top > 0 && bT == b3) {
+                if (c3 <= cT) continue;
+                --top;  // same slope, higher line: replaces the top
+                bT = bS;
+                cT = cS;
+                if (top >= 2) {
+                    const int l = hull[top - 2];
+                    bS = sg * __ldg(P.a + l);
+                    cS = cb[l * stride];
+                }
             }
+            // T is never the maximum iff x(S, new) <= x(S, T), x(p, q) = (c_p - c_q) / (b_q - b_p)
+            while (top >= 2 && (cS - c3) * (bT - bS) <= (cS - cT) * (b3 - bS)) {
+                --top;
+                bT = bS;
+                cT = cS;
+                if (top >= 2) {
+                    const int l = hull[top - 2];
+                    bS = sg * __ldg(P.a + l);
+                    cS = cb[l * stride];
+                }
+            }
+            hull[top++] = (uint8_t)j;
+            bS = bT;
+            cS = cT;
+            bT = b3;
+            cT = c3;
         }
-        while (top >= 2) {
-            const int l1 = hull[top - 2], l2 = hull[top - 1];
-            const double b1 = sg * __ldg(P.a + l1), b2 = sg * __ldg(P.a + l2);
-            const double c1 = cb[l1 * stride], c2 = cb[l2 * stride];
-            // l2 is never the maximum iff x(l1, l3) <= x(l1, l2), x(p, q) = (c_p - c_q) / (b_q - b_p)
-            if ((c1 - c3) * (b2 - b1) <= (c1 - c2) * (b3 - b1)) --top;
-            else break;
-        }
-        hull[top++] = (uint8_t)j;
     }
     // the envelope segment that contains u*: on a breakpoint tie the steeper line (it
     // dominates just after)
