@@ -256,6 +256,37 @@ __device__ __forceinline__ void phibar_phi_x2(double xa, double xb, double& Qa, 
     Qa = xa >= 0.0 ? qa : MC.one - qa;
     Qb = xb >= 0.0 ? qb : MC.one - qb;
 }
+// The same for four arguments (two options of the C5 portfolio's phase B): four
+// independent Horner chains per coefficient load.
+__device__ __forceinline__ void phibar_phi_x4(const double (&x)[4], double (&Q)[4], double (&ph)[4]) {
+    double a[4], r[4], t[4], h[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        a[i] = fabs(x[i]);
+        r[i] = rcp_newton(a[i] + MC.mills_c);
+        t[i] = fma(-MC.mills_2c, r[i], MC.one) - MILLS_H_CENTER;
+        h[i] = MILLS_H[27];
+    }
+#pragma unroll
+    for (int j = 26; j >= 0; --j)
+#pragma unroll
+        for (int i = 0; i < 4; ++i) h[i] = fma(h[i], t[i], MILLS_H[j]);
+    double sq[4], lo[4], e[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        sq[i] = a[i] * a[i];
+        lo[i] = fma(a[i], a[i], -sq[i]);
+    }
+    fast_exp_x2(MC.minus_half * sq[0], MC.minus_half * sq[1], e[0], e[1]);
+    fast_exp_x2(MC.minus_half * sq[2], MC.minus_half * sq[3], e[2], e[3]);
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        ph[i] = (sq[i] < MC.exp_floor * MC.two) ? MC.inv_sqrt_2pi * e[i] * fma(MC.minus_half, lo[i], MC.one) : 0.0;
+        const double q = ph[i] * (h[i] * r[i]);
+        Q[i] = x[i] >= 0.0 ? q : MC.one - q;
+    }
+}
+
 __device__ __forceinline__ double normal_sf(double x) {
     double Q, Q2, ph, ph2;
     phibar_phi_x2(x, x, Q, Q2, ph, ph2);

@@ -230,9 +230,10 @@ __global__ void __launch_bounds__(128, 3) portfolio_kernel(const PortfolioArgs P
                 if (two && B.lb && sb[7] != 0.0) ++ties;
                 const double psia = (A.c_lnK - (A.lb ? sa[5] : sa[1])) * A.inv_s;
                 const double psib = (B.c_lnK - (B.lb ? sb[5] : sb[1])) * B.inv_s;
-                double Q0a, Q1a, pha, phsa, Q0b, Q1b, phb, phsb;
-                phibar_phi_x2(psia, psia - A.c_s, Q0a, Q1a, pha, phsa);
-                phibar_phi_x2(psib, psib - B.c_s, Q0b, Q1b, phb, phsb);
+                const double xq[4] = {psia, psia - A.c_s, psib, psib - B.c_s};
+                double Qq[4], phq[4];
+                phibar_phi_x4(xq, Qq, phq);
+                const double Q0a = Qq[0], Q1a = Qq[1], pha = phq[0], Q0b = Qq[2], Q1b = Qq[3], phb = phq[2];
                 double fa[4], fb[4];
                 tail(A, sa, Q0a, Q1a, pha, psia, fa);
                 tail(B, sb, Q0b, Q1b, phb, psib, fb);
