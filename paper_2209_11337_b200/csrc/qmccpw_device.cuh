@@ -323,6 +323,13 @@ __device__ __forceinline__ X1Sums x1_solve(const PathArgs& P, int o, bool arith,
     }
     unconverged += conv ? 0u : 1u;
     double Dst = 0.0, Qst = 0.0, Vst = 0.0, sumW = 0.0, sumWv = 0.0;
+    // equal slopes (STD: a_j = sqrt(dt)): Phibar(u - sigma a_j) is one number for every date
+    const bool flat = arith && P.a[0] == P.a[d - 1];
+    double Pflat = 1.0;
+    if (flat) {
+        double Q2, p1, p2;
+        phibar_phi_x2(u - sg * P.a[0], u - sg * P.a[0], Pflat, Q2, p1, p2);
+    }
 #pragma unroll 1
     for (int j = 0; j < d; j += 2) {
         const int jb = (j + 1 < d) ? j + 1 : j;
@@ -340,15 +347,19 @@ __device__ __forceinline__ X1Sums x1_solve(const PathArgs& P, int o, bool arith,
         Qst = fma(ab * ab, Eb, Qst);
         Vst = fma(Eb, Rb - sg * tb + ab * u, Vst);
         if (arith) {
-            double wa, wb, Pa, Pb, pa, pb;
+            double wa, wb, Pa = 1.0, Pb = 1.0, pa, pb;
             fast_exp_x2(fma(0.5 * sg * sg * aa, aa, ca), fma(0.5 * sg * sg * ab, ab, cbb), wa, wb);
-            phibar_phi_x2(u - sg * aa, u - sg * ab, Pa, Pb, pa, pb);  // Phi(sigma a - u) = Phibar(u - sigma a)
+            if (!flat) phibar_phi_x2(u - sg * aa, u - sg * ab, Pa, Pb, pa, pb);  // Phi(sigma a - u) = Phibar(u - sigma a)
             wb *= wgt;
             sumW = fma(wa, Pa, sumW);
             sumWv = fma(wa * (Ra - sg * ta + sg * aa * aa), Pa, sumWv);
             sumW = fma(wb, Pb, sumW);
             sumWv = fma(wb * (Rb - sg * tb + sg * ab * ab), Pb, sumWv);
         }
+    }
+    if (flat) {
+        sumW *= Pflat;
+        sumWv *= Pflat;
     }
     return X1Sums{u, Dst, Qst, Vst, sumW, sumWv};
 }
