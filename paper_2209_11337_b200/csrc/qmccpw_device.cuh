@@ -294,6 +294,22 @@ __device__ __forceinline__ X1Sums x1_solve(const PathArgs& P, int o, bool arith,
     }
     double u = fmin(u_hi, (lnK - sumc / d) / (sg * P.mean_a));
     bool conv = false;
+    if (P.a[0] == P.a[d - 1]) {
+        // equal slopes (STD): S(u) = e^{sigma a u} sum_j e^{c_j}, so the threshold is closed-form,
+        // u* = (ln(d K) - ln sum_j e^{c_j}) / (sigma a) -- no iteration
+        double S = 0.0;
+        int j = 0;
+#pragma unroll 1
+        for (; j + 1 < d; j += 2) {
+            double Ea, Eb;
+            fast_exp_x2(cb[j * stride], cb[(j + 1) * stride], Ea, Eb);
+            S += Ea;
+            S += Eb;
+        }
+        if (j < d) S += fast_exp(cb[j * stride]);
+        u = fmin((lndK - fast_log(S)) / (sg * P.a[0]), u_hi);
+        conv = true;
+    } else
     for (int it = 0; it < kNewtonMax; ++it) {
         double S = 0.0, SA = 0.0, SAA = 0.0;
         int j = 0;
