@@ -45,14 +45,16 @@ def fp64_model_per_path(d, constr, cond, n_opt, arith_x1=0, n_lookback_x1=0):
     planning model, fixed constants -- independent of how the kernel is written):
     c_icdf = 50 (branch-light FP64 inverse normal), c_exp = 17, c_tail = 160
     per option (log + 2 erfc + exp + ~30 FMA), c_W = 1 (STD) / 2 (BB) / d (PCA).
-    X1: 4 Newton passes per arithmetic / binary option (SURVEY's count); a lookback under
-    X1 has a closed-form threshold and one envelope pass instead (row f1)."""
+    X1: 4 Newton passes per arithmetic / binary option (SURVEY's count); under STD all
+    dates share one slope, so the threshold is closed-form and one pass replaces the four
+    (reading 19); a lookback under X1 has a closed-form threshold and one
+    envelope pass instead (row f1)."""
     c_icdf, c_exp, c_tail = 50, 17, 160
     c_w = {0: 1, 1: 2, 2: d, 3: d}[constr]  # GPCA: a rotated PCA matrix, same dense contraction
     d_icdf = d - 1 if (cond == 1 or constr == 0) else d
     if cond == 0:
         return d_icdf * c_icdf + d * (c_exp + c_w + 6) + n_opt * c_tail
-    newton = 4 * d * (c_exp + 3)
+    newton = (1 if constr == 0 else 4) * d * (c_exp + 3)
     n_newton = n_opt - n_lookback_x1
     return (d_icdf * c_icdf + d * c_w + n_newton * (newton + d * (c_exp + 3) + c_tail)
             + n_lookback_x1 * (d * (c_exp + 3) + c_tail) + arith_x1 * d * (c_exp + 60 + 4))
@@ -341,7 +343,7 @@ def main():
                             ("C4: arithmetic+binary+lookback Asian calls fused on shared paths, S0=K=100, sigma=0.2, "
                              "r=0.1, T=1, d=64, " + {(1, 0): "BB-W1 (QMC+BB-CPW)", (0, 0): "STD-W1 (QMC-CPW)",
                                                      (2, 0): "PCA-W1", (2, 1): "PCA-X1 (Halley threshold)",
-                                                     (0, 1): "STD-X1 (Halley threshold)", (1, 1): "BB-X1 (Halley threshold)",
+                                                     (0, 1): "STD-X1 (closed-form threshold)", (1, 1): "BB-X1 (Halley threshold)",
                                                      (3, 0): "GPCA-W1 (f3)", (3, 1): "GPCA-X1 (Halley threshold, f3)"}.get(
                                  (args.construction, args.conditioning), "custom"))
                             + {1: ", digital shift only", 3: ", plain Sobol'", 4: ", nested Owen scrambling (f4)"}.get(

@@ -451,6 +451,7 @@ PathArgs make_args(const Plan& pl, const Scratch& s) {
     a.path_out = nullptr;
     a.hook_option = -1;
     a.owen = pl.cfg.randomization == QMCCPW_RAND_OWEN;
+    a.x1_lin = d >= 2 && (pl.cfg.construction == QMCCPW_STD || pl.cfg.construction == QMCCPW_BB);
     return a;
 }
 

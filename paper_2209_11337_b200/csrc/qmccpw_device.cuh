@@ -346,6 +346,17 @@ __device__ __forceinline__ X1Sums x1_solve(const PathArgs& P, int o, bool arith,
         double Q2, p1, p2;
         phibar_phi_x2(u - sg * P.a[0], u - sg * P.a[0], Pflat, Q2, p1, p2);
     }
+    // a_j linear in j (STD, BB): w_j = e^{c_j + sigma^2 a_j^2 / 2} = E_j q_j with
+    // q_j = e^{kappa_j}, kappa_j = sigma a_j (sigma a_j / 2 - u) quadratic in j, so q_j follows
+    // by two products per date (ratio rho_j = q_{j+1}/q_j, rho_{j+1} = rho_j e^{(sigma da)^2})
+    const bool lin = arith && P.x1_lin;
+    double qa = 0.0, rho = 0.0, g = 0.0;
+    if (lin) {
+        const double a0 = P.a[0], a1 = P.a[1], sda = sg * (a1 - a0);
+        const double k0 = sg * a0 * fma(0.5 * sg, a0, -u), k1 = sg * a1 * fma(0.5 * sg, a1, -u);
+        fast_exp_x2(k0, k1 - k0, qa, rho);
+        g = fast_exp(sda * sda);
+    }
 #pragma unroll 1
     for (int j = 0; j < d; j += 2) {
         const int jb = (j + 1 < d) ? j + 1 : j;
@@ -364,7 +375,16 @@ __device__ __forceinline__ X1Sums x1_solve(const PathArgs& P, int o, bool arith,
         Vst = fma(Eb, Rb - sg * tb + ab * u, Vst);
         if (arith) {
             double wa, wb, Pa = 1.0, Pb = 1.0, pa, pb;
-            fast_exp_x2(fma(0.5 * sg * sg * aa, aa, ca), fma(0.5 * sg * sg * ab, ab, cbb), wa, wb);
+            if (lin) {
+                const double qb = qa * rho;
+                wa = Ea * qa;
+                wb = Eb * qb;
+                rho *= g;
+                qa = qb * rho;
+                rho *= g;
+            } else {
+                fast_exp_x2(fma(0.5 * sg * sg * aa, aa, ca), fma(0.5 * sg * sg * ab, ab, cbb), wa, wb);
+            }
             if (!flat) phibar_phi_x2(u - sg * aa, u - sg * ab, Pa, Pb, pa, pb);  // Phi(sigma a - u) = Phibar(u - sigma a)
             wb *= wgt;
             sumW = fma(wa, Pa, sumW);

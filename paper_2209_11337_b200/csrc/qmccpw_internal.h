@@ -78,6 +78,7 @@ struct PathArgs {
     double* path_out;
     int hook_option;         // option index whose values go to path_out
     int owen;                // 1: nested (Owen) scrambling, shift[] holds the per-dimension seeds
+    int x1_lin;              // X1: a_j is linear in j (STD: constant, BB: t_j / sqrt(T)), d >= 2
 };
 
 // ---- portfolio (C5): up to kMaxPortfolio options in up to kMaxFamilies (sigma, T) families
