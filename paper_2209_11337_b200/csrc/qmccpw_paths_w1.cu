@@ -12,8 +12,8 @@ cudaError_t launch_paths(const PathArgs& args, int construction, int conditionin
                                                   : launch_paths_t<kStd, kW1, kMc, false>(args, st, smem_out);
     if (method == kMcAv) return construction == kBB ? launch_paths_t<kBB, kW1, kMcAv, false>(args, st, smem_out)
                                                     : launch_paths_t<kStd, kW1, kMcAv, false>(args, st, smem_out);
-    if (construction == kPca && method == kQmc && !(conditioning == kX1 && args.has_lookback)) {
-        // fragment-native tensor-core path for d <= 128 (the X1 lookback walks its envelope per thread)
+    if (construction == kPca && method == kQmc) {
+        // fragment-native tensor-core path for d <= 128
         bool handled = false;
         cudaError_t e = conditioning == kW1 ? launch_pca_w1(args, st, &handled) : launch_pca_x1(args, st, &handled);
         if (handled) return e;

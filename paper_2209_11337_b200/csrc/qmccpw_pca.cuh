@@ -32,6 +32,15 @@ template <int COND, int KF>
 constexpr int pca_min_blocks() {
     return KF > 16 ? 0 : (COND == kW1 ? QMCCPW_PCA_W1_MINB : QMCCPW_PCA_X1_MINB);
 }
+// byte offset of the X1 lookback staging: accs [n_acc][tpb] | vt, sh, G (+ pad) | HW / red
+__host__ __device__ __forceinline__ size_t pca_stage_offset(int n_acc, int d, int tpb) {
+    const size_t nw = (size_t)tpb / 32;
+    size_t b = (size_t)n_acc * tpb * sizeof(double);
+    b += ((size_t)d * 32 * 2 + d) * sizeof(uint32_t) + 4;
+    const size_t hw = (2 * 2 * nw * d + d) * sizeof(uint32_t), red = 4 * 32 * sizeof(double);
+    b += hw > red ? hw : red;
+    return (b + 7) & ~(size_t)7;
+}
 template <int COND, int KF, bool OWEN>
 __global__ void __launch_bounds__(128, pca_min_blocks<COND, KF>()) pca_kernel(const PathArgs P) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -57,6 +66,10 @@ __global__ void __launch_bounds__(128, pca_min_blocks<COND, KF>()) pca_kernel(co
     double* red = reinterpret_cast<double*>(HW);
     const int hw_size = 2 * nw * d;
     uint32_t* BS = HW + 2 * hw_size;  // [d] incremental Gray bases (sobol_build_hw_inc)
+    // X1 with a lookback: c_j of the warp's 32 paths staged [d][32] per warp, so that each lane
+    // walks the upper envelope of its own path (the quad layout holds a path over 4 lanes)
+    double* stage = reinterpret_cast<double*>(smem_raw + pca_stage_offset(n_acc, d, tpb)) +
+                    (size_t)(tid >> 5) * d * 32;
     const uint64_t K0 = P.point_offset + i0;
     const uint64_t Ab = K0 >> tpb_log2;
     {
@@ -183,6 +196,15 @@ __global__ void __launch_bounds__(128, pca_min_blocks<COND, KF>()) pca_kernel(co
                     cv[2 * jt] = fma(sg, cv[2 * jt], fma(P.omega, (double)(j0 + 1) * P.t1, P.lnS0));
                     cv[2 * jt + 1] = fma(sg, cv[2 * jt + 1], fma(P.omega, (double)(j0 + 2) * P.t1, P.lnS0));
                 }
+                if (P.has_lookback) {
+                    double* sw = stage + 8 * rt + q;
+#pragma unroll
+                    for (int jt = 0; jt < JT; ++jt) {
+                        const int j0 = 8 * jt + 2 * r4;
+                        if (j0 < d) sw[j0 * 32] = cv[2 * jt];
+                        if (j0 + 1 < d) sw[(j0 + 1) * 32] = cv[2 * jt + 1];
+                    }
+                }
                 double f[kMaxOpt][4];
                 // one Newton solve per strike group, not unrolled over the options: the
                 // body is large and the instruction cache is the limiter (ncu: 41 % of
@@ -190,7 +212,7 @@ __global__ void __launch_bounds__(128, pca_min_blocks<COND, KF>()) pca_kernel(co
 #pragma unroll 1
                 for (int o = 0; o < kMaxOpt; ++o) {
                     if (o >= P.n_opt) break;
-                    if (P.tail_leader[o] != o) continue;
+                    if (P.tail_leader[o] != o || P.type[o] == kLookback) continue;
                     const double lnK = P.lnK[o], lndK = P.lndK[o];
                     // bracket [min_j (lnK - c_j)/(sigma a_j), min_j (ln dK - c_j)/(sigma a_j)] and mean c
                     double ulo = CUDART_INF, uhi = CUDART_INF, sumc = 0.0;
@@ -280,12 +302,12 @@ __global__ void __launch_bounds__(128, pca_min_blocks<COND, KF>()) pca_kernel(co
                     if (P.path_out != nullptr) {
 #pragma unroll
                         for (int o = 0; o < kMaxOpt; ++o)
-                            if (o == P.hook_option)
+                            if (o == P.hook_option && P.type[o] != kLookback)
                                 for (int qq = 0; qq < 4; ++qq) P.path_out[ip * 4 + qq] = f[o][qq];
                     }
 #pragma unroll
                     for (int o = 0; o < kMaxOpt; ++o) {
-                        if (o < P.n_opt) {
+                        if (o < P.n_opt && P.type[o] != kLookback) {
 #pragma unroll
                             for (int qq = 0; qq < 4; ++qq) {
                                 const double y = f[o][qq] - P.piv[o][qq];
@@ -297,6 +319,31 @@ __global__ void __launch_bounds__(128, pca_min_blocks<COND, KF>()) pca_kernel(co
                     }
                 }
             }
+        }
+        if (COND == kX1 && P.has_lookback) {
+            // lookback options: lane L walks the envelope of path wbase + L from the staged c_j
+            __syncwarp();
+            const int tp = wbase + lane;
+            const uint64_t ip = i0 + (uint64_t)tp + ((uint64_t)a << tpb_log2);
+            const bool valid = ip < P.n_points;
+#pragma unroll 1
+            for (int o = 0; o < P.n_opt; ++o) {
+                if (P.type[o] != kLookback) continue;
+                double fl[4];
+                x1_lookback(P, o, stage + lane, 32, fl);
+                if (valid) {
+                    if (P.path_out != nullptr && o == P.hook_option)
+                        for (int qq = 0; qq < 4; ++qq) P.path_out[ip * 4 + qq] = fl[qq];
+#pragma unroll
+                    for (int qq = 0; qq < 4; ++qq) {
+                        const double y = fl[qq] - P.piv[o][qq];
+                        double* a1 = accs + (size_t)(o * 8 + qq * 2) * tpb + tp;
+                        a1[0] += y;
+                        a1[tpb] = fma(y, y, a1[tpb]);
+                    }
+                }
+            }
+            __syncwarp();  // the next batch overwrites the staging
         }
         if (COND == kW1) {
             const W1Acc& w1 = w1own;
@@ -319,12 +366,11 @@ __global__ void __launch_bounds__(128, pca_min_blocks<COND, KF>()) pca_kernel(co
     block_epilogue(P, COND == kX1 ? accs : nullptr, wacc, red, n_acc, tpb, tid, cell, unconverged, ties, npts);
 }
 
-static size_t pca_smem_bytes(const PathArgs& a) {
-    const size_t tpb = (size_t)1 << a.tpb_log2, nw = tpb / 32;
-    size_t b = (size_t)a.n_opt * 8 * tpb * sizeof(double);
-    b += ((size_t)a.d * 32 * 2 + a.d) * sizeof(uint32_t) + 4;
-    const size_t hw = (2 * 2 * nw * a.d + a.d) * sizeof(uint32_t), red = 4 * 32 * sizeof(double);
-    return b + (hw > red ? hw : red);
+static size_t pca_smem_bytes(const PathArgs& a, int cond) {
+    const size_t tpb = (size_t)1 << a.tpb_log2;
+    size_t b = pca_stage_offset(a.n_opt * 8, a.d, (int)tpb);
+    if (cond == kX1 && a.has_lookback) b += tpb * a.d * sizeof(double);  // [nw][d][32] staging
+    return b;
 }
 
 template <int K, int KF, bool OW>
@@ -341,7 +387,7 @@ static cudaError_t launch_pca_t(const PathArgs& args_in, cudaStream_t st) {
     int best_lg = -1, best_warps = -1;
     for (int lg = 7; lg >= 5; --lg) {
         args.tpb_log2 = lg;
-        const size_t smem = pca_smem_bytes(args);
+        const size_t smem = pca_smem_bytes(args, K);
         if (smem > 200 * 1024) continue;
         int nb = 0;
         if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, pca_kernel<K, KF, OW>, 1 << lg, smem) != cudaSuccess) continue;
@@ -354,7 +400,7 @@ static cudaError_t launch_pca_t(const PathArgs& args_in, cudaStream_t st) {
     args.tpb_log2 = best_lg;
     const uint64_t nblocks = args.cell_end - args.cell_begin;
     if (nblocks == 0) return cudaSuccess;
-    pca_kernel<K, KF, OW><<<(unsigned)nblocks, 1 << best_lg, pca_smem_bytes(args), st>>>(args);
+    pca_kernel<K, KF, OW><<<(unsigned)nblocks, 1 << best_lg, pca_smem_bytes(args, K), st>>>(args);
     ++launch_counter();
     return cudaGetLastError();
 }
