@@ -10,7 +10,7 @@ PKG = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 SOURCES = [os.path.join(CSRC, f) for f in (
-    "qmccpw_paths_w1.cu", "qmccpw_paths_x1.cu", "qmccpw_pca_w1.cu", "qmccpw_pca_x1.cu", "qmccpw_pca_x1_owen.cu",
+    "qmccpw_paths_w1.cu", "qmccpw_paths_x1.cu", "qmccpw_pca_w1.cu", "qmccpw_pca_x1.cu", "qmccpw_pca_x1_owen.cu", "qmccpw_pca_x1_lb.cu",
     "qmccpw_portfolio.cu",
     "qmccpw_kernels.cu", "qmccpw_api.cu", "qmccpw_microbench.cu")]
 HEADERS = [os.path.join(CSRC, f) for f in (

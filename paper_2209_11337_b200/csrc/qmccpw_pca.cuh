@@ -28,9 +28,10 @@ namespace qmccpw {
 #endif
 // d <= 64: shared memory allows 5 blocks/SM, so cap registers to match (measured on C4:
 // PCA-W1 72.4 -> 69.4 ms, PCA-X1 175 -> 165 ms); larger d is smem-limited anyway
-template <int COND, int KF>
+// (with a lookback the [d][32] per-warp staging allows 2 blocks/SM at d = 64: registers are free)
+template <int COND, int KF, bool LB>
 constexpr int pca_min_blocks() {
-    return KF > 16 ? 0 : (COND == kW1 ? QMCCPW_PCA_W1_MINB : QMCCPW_PCA_X1_MINB);
+    return KF > 16 ? 0 : (LB ? 2 : (COND == kW1 ? QMCCPW_PCA_W1_MINB : QMCCPW_PCA_X1_MINB));
 }
 // byte offset of the X1 lookback staging: accs [n_acc][tpb] | vt, sh, G (+ pad) | HW / red
 __host__ __device__ __forceinline__ size_t pca_stage_offset(int n_acc, int d, int tpb) {
@@ -41,8 +42,9 @@ __host__ __device__ __forceinline__ size_t pca_stage_offset(int n_acc, int d, in
     b += hw > red ? hw : red;
     return (b + 7) & ~(size_t)7;
 }
-template <int COND, int KF, bool OWEN>
-__global__ void __launch_bounds__(128, pca_min_blocks<COND, KF>()) pca_kernel(const PathArgs P) {
+// LB (X1 only): the launch has a lookback option (staging + per-lane envelope walk)
+template <int COND, int KF, bool OWEN, bool LB>
+__global__ void __launch_bounds__(128, pca_min_blocks<COND, KF, LB>()) pca_kernel(const PathArgs P) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     constexpr int DP = 4 * KF;  // padded dimension (multiple of 8)
     constexpr int JT = DP / 8;  // column tiles of 8 dates
@@ -196,7 +198,7 @@ __global__ void __launch_bounds__(128, pca_min_blocks<COND, KF>()) pca_kernel(co
                     cv[2 * jt] = fma(sg, cv[2 * jt], fma(P.omega, (double)(j0 + 1) * P.t1, P.lnS0));
                     cv[2 * jt + 1] = fma(sg, cv[2 * jt + 1], fma(P.omega, (double)(j0 + 2) * P.t1, P.lnS0));
                 }
-                if (P.has_lookback) {
+                if (LB) {
                     double* sw = stage + 8 * rt + q;
 #pragma unroll
                     for (int jt = 0; jt < JT; ++jt) {
@@ -320,7 +322,7 @@ __global__ void __launch_bounds__(128, pca_min_blocks<COND, KF>()) pca_kernel(co
                 }
             }
         }
-        if (COND == kX1 && P.has_lookback) {
+        if (COND == kX1 && LB) {
             // lookback options: lane L walks the envelope of path wbase + L from the staged c_j
             __syncwarp();
             const int tp = wbase + lane;
@@ -366,20 +368,20 @@ __global__ void __launch_bounds__(128, pca_min_blocks<COND, KF>()) pca_kernel(co
     block_epilogue(P, COND == kX1 ? accs : nullptr, wacc, red, n_acc, tpb, tid, cell, unconverged, ties, npts);
 }
 
-static size_t pca_smem_bytes(const PathArgs& a, int cond) {
+static size_t pca_smem_bytes(const PathArgs& a, bool lb) {
     const size_t tpb = (size_t)1 << a.tpb_log2;
     size_t b = pca_stage_offset(a.n_opt * 8, a.d, (int)tpb);
-    if (cond == kX1 && a.has_lookback) b += tpb * a.d * sizeof(double);  // [nw][d][32] staging
+    if (lb) b += tpb * a.d * sizeof(double);  // [nw][d][32] staging
     return b;
 }
 
-template <int K, int KF, bool OW>
+template <int K, int KF, bool OW, bool LB>
 static cudaError_t launch_pca_t(const PathArgs& args_in, cudaStream_t st) {
     static thread_local int set_for[64] = {0};
     int dev = 0;
     cudaGetDevice(&dev);
     if (set_for[dev & 63] == 0) {
-        cudaError_t e = cudaFuncSetAttribute(pca_kernel<K, KF, OW>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+        cudaError_t e = cudaFuncSetAttribute(pca_kernel<K, KF, OW, LB>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
         if (e != cudaSuccess) return e;
         set_for[dev & 63] = 1;
     }
@@ -387,10 +389,10 @@ static cudaError_t launch_pca_t(const PathArgs& args_in, cudaStream_t st) {
     int best_lg = -1, best_warps = -1;
     for (int lg = 7; lg >= 5; --lg) {
         args.tpb_log2 = lg;
-        const size_t smem = pca_smem_bytes(args, K);
+        const size_t smem = pca_smem_bytes(args, LB);
         if (smem > 200 * 1024) continue;
         int nb = 0;
-        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, pca_kernel<K, KF, OW>, 1 << lg, smem) != cudaSuccess) continue;
+        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, pca_kernel<K, KF, OW, LB>, 1 << lg, smem) != cudaSuccess) continue;
         if (nb * (1 << lg) / 32 > best_warps) {
             best_warps = nb * (1 << lg) / 32;
             best_lg = lg;
@@ -400,25 +402,25 @@ static cudaError_t launch_pca_t(const PathArgs& args_in, cudaStream_t st) {
     args.tpb_log2 = best_lg;
     const uint64_t nblocks = args.cell_end - args.cell_begin;
     if (nblocks == 0) return cudaSuccess;
-    pca_kernel<K, KF, OW><<<(unsigned)nblocks, 1 << best_lg, pca_smem_bytes(args, K), st>>>(args);
+    pca_kernel<K, KF, OW, LB><<<(unsigned)nblocks, 1 << best_lg, pca_smem_bytes(args, LB), st>>>(args);
     ++launch_counter();
     return cudaGetLastError();
 }
 
-template <int K, bool OW>
+template <int K, bool OW, bool LB = false>
 static cudaError_t launch_pca(const PathArgs& args, cudaStream_t st, bool* handled) {
     *handled = true;
     switch (args.M_ld) {
-    case 8: return launch_pca_t<K, 2, OW>(args, st);
-    case 16: return launch_pca_t<K, 4, OW>(args, st);
-    case 24: return launch_pca_t<K, 6, OW>(args, st);
-    case 32: return launch_pca_t<K, 8, OW>(args, st);
-    case 40: return launch_pca_t<K, 10, OW>(args, st);
-    case 48: return launch_pca_t<K, 12, OW>(args, st);
-    case 56: return launch_pca_t<K, 14, OW>(args, st);
-    case 64: return launch_pca_t<K, 16, OW>(args, st);
-    case 96: return launch_pca_t<K, 24, OW>(args, st);
-    case 128: return launch_pca_t<K, 32, OW>(args, st);
+    case 8: return launch_pca_t<K, 2, OW, LB>(args, st);
+    case 16: return launch_pca_t<K, 4, OW, LB>(args, st);
+    case 24: return launch_pca_t<K, 6, OW, LB>(args, st);
+    case 32: return launch_pca_t<K, 8, OW, LB>(args, st);
+    case 40: return launch_pca_t<K, 10, OW, LB>(args, st);
+    case 48: return launch_pca_t<K, 12, OW, LB>(args, st);
+    case 56: return launch_pca_t<K, 14, OW, LB>(args, st);
+    case 64: return launch_pca_t<K, 16, OW, LB>(args, st);
+    case 96: return launch_pca_t<K, 24, OW, LB>(args, st);
+    case 128: return launch_pca_t<K, 32, OW, LB>(args, st);
     default: *handled = false; return cudaSuccess;
     }
 }

@@ -1,12 +1,15 @@
 // qmccpw_pca_x1.cu -- PCA paths on DMMA tiles, X1 conditioning (d <= 128); the Owen
-// instantiations are in qmccpw_pca_x1_owen.cu (a separate unit: parallel build).
+// instantiations are in qmccpw_pca_x1_owen.cu, those with a lookback in qmccpw_pca_x1_lb.cu
+// (separate units: parallel build).
 #include "qmccpw_pca.cuh"
 
 namespace qmccpw {
 
 cudaError_t launch_pca_x1_owen(const PathArgs& args, cudaStream_t st, bool* handled);
+cudaError_t launch_pca_x1_lb(const PathArgs& args, cudaStream_t st, bool* handled);
 
 cudaError_t launch_pca_x1(const PathArgs& args, cudaStream_t st, bool* handled) {
+    if (args.has_lookback) return launch_pca_x1_lb(args, st, handled);
     return args.owen ? launch_pca_x1_owen(args, st, handled) : launch_pca<kX1, false>(args, st, handled);
 }
 

@@ -1,0 +1,11 @@
+// qmccpw_pca_x1_lb.cu -- PCA paths on DMMA tiles, X1 conditioning with a lookback option: the
+// warp's c_j are staged in shared memory and each lane walks its path's upper envelope.
+#include "qmccpw_pca.cuh"
+
+namespace qmccpw {
+
+cudaError_t launch_pca_x1_lb(const PathArgs& args, cudaStream_t st, bool* handled) {
+    return args.owen ? launch_pca<kX1, true, true>(args, st, handled) : launch_pca<kX1, false, true>(args, st, handled);
+}
+
+}  // namespace qmccpw
