@@ -441,7 +441,9 @@ __device__ __forceinline__ void x1_lookback(const PathArgs& P, int o, const doub
     // convex-hull pass (O(d), no divisions): every construction has a_j nondecreasing in
     // j (STD: equal; BB: t_j/sqrt(T); PCA / GPCA: positive increasing first column), so
     // lines arrive by slope; a line is dropped when the next one overtakes it no later
-    // than it overtakes its predecessor.  Equal slopes keep the higher line.
+    // than it overtakes its predecessor.  Equal slopes keep the higher line.  Only u >= u*
+    // matters: there line j0 is the highest (c_j + b_j u* <= c_j + b_j u_j = ln K), and a
+    // flatter line below it stays below, so the pass starts at j0.
     uint8_t hull[kMaxDimGpu];  // line indices (d <= 256)
     int top = 0;
     if (__ldg(P.a) == __ldg(P.a + d - 1)) {  // STD: all slopes equal -> the single highest line (lowest j on ties)
@@ -451,7 +453,7 @@ __device__ __forceinline__ void x1_lookback(const PathArgs& P, int o, const doub
     } else {
         // the top two hull lines (T = top, S = second) stay in registers; a pop reloads S
         double bT = 0.0, cT = 0.0, bS = 0.0, cS = 0.0;
-        for (int j = 0; j < d; ++j) {
+        for (int j = j0; j < d; ++j) {
             const double b3 = sg * __ldg(P.a + j), c3 = cb[j * stride];
             if (top > 0 && bT == b3) {
                 if (c3 <= cT) continue;
