@@ -140,6 +140,22 @@ __device__ __forceinline__ double fast_log(double t) {
     return fma(k, MC.ln2_hi, fma(k, MC.ln2_lo, fma(r * r, p, r) + c.y));
 }
 
+// degree of the central Phi^{-1} polynomial (fit_device_polys.py: max rel. error of the
+// double-rounded polynomial 4.3e-17 at 24, 1.7e-16 at 23, 3.3e-16 at 22)
+#ifndef QMCCPW_ICDF_DEG
+#define QMCCPW_ICDF_DEG 24
+#endif
+constexpr int kIcdfDeg = QMCCPW_ICDF_DEG;
+#if QMCCPW_ICDF_DEG == 24
+#define ICDF_C ICDF_CENTRAL
+#elif QMCCPW_ICDF_DEG == 23
+#define ICDF_C ICDF_CENTRAL_D23
+#elif QMCCPW_ICDF_DEG == 22
+#define ICDF_C ICDF_CENTRAL_D22
+#else
+#error "QMCCPW_ICDF_DEG must be 22, 23 or 24"
+#endif
+
 // (a3) lattice point -> standard normal, Phi^{-1}((y + 1/2) 2^-32).
 // Lower half (y < 2^31) evaluated, upper half mirrored (exact symmetry).
 // Giles' variable w = -ln(1 - z^2) = -ln(4u(1-u)), z = 2u - 1 (exact):
@@ -155,9 +171,9 @@ __device__ __forceinline__ double normal_from_u32(uint32_t y) {
     double p;
     if (w < MC.w_split) {
         const double v = w - ICDF_CENTRAL_CENTER;
-        p = ICDF_CENTRAL[24];
+        p = ICDF_C[kIcdfDeg];
 #pragma unroll
-        for (int j = 23; j >= 0; --j) p = fma(p, v, ICDF_CENTRAL[j]);
+        for (int j = kIcdfDeg - 1; j >= 0; --j) p = fma(p, v, ICDF_C[j]);
     } else {
         const double v = sqrt(w) - ICDF_TAIL_CENTER;
         p = ICDF_TAIL[24];
@@ -213,11 +229,11 @@ __device__ __forceinline__ void normal_from_u32_x2(uint32_t ya, uint32_t yb, dou
     wa = -wa;
     wb = -wb;
     const double va = wa - ICDF_CENTRAL_CENTER, vb = wb - ICDF_CENTRAL_CENTER;
-    double pa = ICDF_CENTRAL[24], pb = ICDF_CENTRAL[24];
+    double pa = ICDF_C[kIcdfDeg], pb = ICDF_C[kIcdfDeg];
 #pragma unroll
-    for (int j = 23; j >= 0; --j) {
-        pa = fma(pa, va, ICDF_CENTRAL[j]);
-        pb = fma(pb, vb, ICDF_CENTRAL[j]);
+    for (int j = kIcdfDeg - 1; j >= 0; --j) {
+        pa = fma(pa, va, ICDF_C[j]);
+        pb = fma(pb, vb, ICDF_C[j]);
     }
     if (wa >= MC.w_split) pa = icdf_tail_poly(wa);  // u < 4.8e-4: rare, divergent
     if (wb >= MC.w_split) pb = icdf_tail_poly(wb);
