@@ -143,7 +143,7 @@ __device__ __forceinline__ double fast_log(double t) {
 // degree of the central Phi^{-1} polynomial (fit_device_polys.py: max rel. error of the
 // double-rounded polynomial 4.3e-17 at 24, 1.7e-16 at 23, 3.3e-16 at 22)
 #ifndef QMCCPW_ICDF_DEG
-#define QMCCPW_ICDF_DEG 24
+#define QMCCPW_ICDF_DEG 22
 #endif
 constexpr int kIcdfDeg = QMCCPW_ICDF_DEG;
 #if QMCCPW_ICDF_DEG == 24
