@@ -31,6 +31,22 @@ __constant__ MathConst MC = {
 
 // Philox4x32-10 (Salmon et al., SC'11): 10 rounds of two 32x32->64 products,
 // Weyl key schedule.  c = counter in, output out (in place).
+// degrees of the exp and log1p kernels (fit_device_polys.py): exp(r), |r| <= ln2/128,
+// degree 6 (3.4e-21) or 5 (2.2e-18 relative); (log1p(r) - r)/r^2, |r| <= 2^-7, degree 5
+// or 4 (5.2e-13 relative, i.e. <= 1.6e-17 absolute in log1p(r))
+#ifndef QMCCPW_LOGEXP_LO
+#define QMCCPW_LOGEXP_LO 0
+#endif
+#if QMCCPW_LOGEXP_LO
+constexpr int kExpDeg = 5, kLogDeg = 4;
+#define EXP_P EXP64_POLY_D5
+#define LOG_P LOG1P_L_D4
+#else
+constexpr int kExpDeg = 6, kLogDeg = 5;
+#define EXP_P EXP64_POLY
+#define LOG_P LOG1P_L
+#endif
+
 __device__ __forceinline__ void philox4x32_10(uint32_t c[4], uint32_t k0, uint32_t k1) {
 #pragma unroll
     for (int r = 0; r < 10; ++r) {
@@ -88,9 +104,9 @@ __device__ __forceinline__ double fast_exp(double x) {
     double r = fma(n, -MC.e64_ln2_hi, x);
     r = fma(n, -MC.e64_ln2_lo, r);
     const double T = QMCCPW_EXP_TAB(ni & 63);
-    double p = EXP64_POLY[6];
+    double p = EXP_P[kExpDeg];
 #pragma unroll
-    for (int j = 5; j >= 0; --j) p = fma(p, r, EXP64_POLY[j]);
+    for (int j = kExpDeg - 1; j >= 0; --j) p = fma(p, r, EXP_P[j]);
     p *= T;
     return __hiloint2double(__double2hiint(p) + ((ni >> 6) << 20), __double2loint(p));
 }
@@ -117,11 +133,11 @@ __device__ __forceinline__ void fast_log_x2(double ta, double tb, double& la, do
     const double2 ca = QMCCPW_LOG_TAB((ha >> 14) & 63);
     const double2 cb = QMCCPW_LOG_TAB((hb >> 14) & 63);
     const double ra = fma(ma, ca.x, -MC.one), rb = fma(mb, cb.x, -MC.one);
-    double pa = LOG1P_L[5], pb = LOG1P_L[5];
+    double pa = LOG_P[kLogDeg], pb = LOG_P[kLogDeg];
 #pragma unroll
-    for (int j = 4; j >= 0; --j) {
-        pa = fma(pa, ra, LOG1P_L[j]);
-        pb = fma(pb, rb, LOG1P_L[j]);
+    for (int j = kLogDeg - 1; j >= 0; --j) {
+        pa = fma(pa, ra, LOG_P[j]);
+        pb = fma(pb, rb, LOG_P[j]);
     }
     const double sa = fma(ra * ra, pa, ra) + ca.y, sb = fma(rb * rb, pb, rb) + cb.y;
     la = fma(ka, MC.ln2_hi, fma(ka, MC.ln2_lo, sa));
@@ -134,9 +150,9 @@ __device__ __forceinline__ double fast_log(double t) {
     const double k = (double)((h >> 20) - 1023);
     const double2 c = QMCCPW_LOG_TAB((h >> 14) & 63);
     const double r = fma(m, c.x, -MC.one);
-    double p = LOG1P_L[5];
+    double p = LOG_P[kLogDeg];
 #pragma unroll
-    for (int j = 4; j >= 0; --j) p = fma(p, r, LOG1P_L[j]);
+    for (int j = kLogDeg - 1; j >= 0; --j) p = fma(p, r, LOG_P[j]);
     return fma(k, MC.ln2_hi, fma(k, MC.ln2_lo, fma(r * r, p, r) + c.y));
 }
 
@@ -197,11 +213,11 @@ __device__ __forceinline__ void fast_exp_x2(double xa, double xb, double& ra, do
     double qa = fma(fa, -MC.e64_ln2_hi, xa), qb = fma(fb, -MC.e64_ln2_hi, xb);
     qa = fma(fa, -MC.e64_ln2_lo, qa);
     qb = fma(fb, -MC.e64_ln2_lo, qb);
-    double pa = EXP64_POLY[6], pb = EXP64_POLY[6];
+    double pa = EXP_P[kExpDeg], pb = EXP_P[kExpDeg];
 #pragma unroll
-    for (int j = 5; j >= 0; --j) {
-        pa = fma(pa, qa, EXP64_POLY[j]);
-        pb = fma(pb, qb, EXP64_POLY[j]);
+    for (int j = kExpDeg - 1; j >= 0; --j) {
+        pa = fma(pa, qa, EXP_P[j]);
+        pb = fma(pb, qb, EXP_P[j]);
     }
     pa *= Ta;
     pb *= Tb;
