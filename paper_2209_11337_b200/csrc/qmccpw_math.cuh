@@ -35,7 +35,19 @@ __constant__ MathConst MC = {
 // degree 6 (3.4e-21) or 5 (2.2e-18 relative); (log1p(r) - r)/r^2, |r| <= 2^-7, degree 5
 // or 4 (5.2e-13 relative, i.e. <= 1.6e-17 absolute in log1p(r))
 #ifndef QMCCPW_LOGEXP_LO
-#define QMCCPW_LOGEXP_LO 0
+#define QMCCPW_LOGEXP_LO 1
+#endif
+// degree of the Mills-ratio polynomial: 27 (6.2e-17) or 23 (5.3e-17, the same rounding floor)
+#ifndef QMCCPW_MILLS_DEG
+#define QMCCPW_MILLS_DEG 23
+#endif
+constexpr int kMillsDeg = QMCCPW_MILLS_DEG;
+#if QMCCPW_MILLS_DEG == 27
+#define MILLS_P MILLS_H
+#elif QMCCPW_MILLS_DEG == 23
+#define MILLS_P MILLS_H_D23
+#else
+#error "QMCCPW_MILLS_DEG must be 23 or 27"
 #endif
 #if QMCCPW_LOGEXP_LO
 constexpr int kExpDeg = 5, kLogDeg = 4;
@@ -272,11 +284,11 @@ __device__ __forceinline__ void phibar_phi_x2(double xa, double xb, double& Qa, 
     const double aa = fabs(xa), ab = fabs(xb);
     const double ra = rcp_newton(aa + MC.mills_c), rb = rcp_newton(ab + MC.mills_c);
     const double ta = fma(-MC.mills_2c, ra, MC.one) - MILLS_H_CENTER, tb = fma(-MC.mills_2c, rb, MC.one) - MILLS_H_CENTER;
-    double ha = MILLS_H[27], hb = MILLS_H[27];
+    double ha = MILLS_P[kMillsDeg], hb = MILLS_P[kMillsDeg];
 #pragma unroll
-    for (int j = 26; j >= 0; --j) {
-        ha = fma(ha, ta, MILLS_H[j]);
-        hb = fma(hb, tb, MILLS_H[j]);
+    for (int j = kMillsDeg - 1; j >= 0; --j) {
+        ha = fma(ha, ta, MILLS_P[j]);
+        hb = fma(hb, tb, MILLS_P[j]);
     }
     const double sa = aa * aa, sb = ab * ab;
     const double la = fma(aa, aa, -sa), lb = fma(ab, ab, -sb);
@@ -297,12 +309,12 @@ __device__ __forceinline__ void phibar_phi_x4(const double (&x)[4], double (&Q)[
         a[i] = fabs(x[i]);
         r[i] = rcp_newton(a[i] + MC.mills_c);
         t[i] = fma(-MC.mills_2c, r[i], MC.one) - MILLS_H_CENTER;
-        h[i] = MILLS_H[27];
+        h[i] = MILLS_P[kMillsDeg];
     }
 #pragma unroll
-    for (int j = 26; j >= 0; --j)
+    for (int j = kMillsDeg - 1; j >= 0; --j)
 #pragma unroll
-        for (int i = 0; i < 4; ++i) h[i] = fma(h[i], t[i], MILLS_H[j]);
+        for (int i = 0; i < 4; ++i) h[i] = fma(h[i], t[i], MILLS_P[j]);
     double sq[4], lo[4], e[4];
 #pragma unroll
     for (int i = 0; i < 4; ++i) {
