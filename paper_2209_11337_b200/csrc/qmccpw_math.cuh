@@ -9,6 +9,17 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+// polynomial degrees of the function kernels (see the selections below); the generated
+// header keeps only the selected fits when QMCCPW_COEFF_GUARDS is defined
+#ifndef QMCCPW_ICDF_DEG
+#define QMCCPW_ICDF_DEG 22
+#endif
+#ifndef QMCCPW_MILLS_DEG
+#define QMCCPW_MILLS_DEG 23
+#endif
+#ifndef QMCCPW_LOGEXP_LO
+#define QMCCPW_LOGEXP_LO 1
+#endif
 #include "qmccpw_coeffs.cuh"
 
 namespace qmccpw {
@@ -29,18 +40,10 @@ __constant__ MathConst MC = {
     0x1p-32, 0x1p-33, 4.0, -700.0, 3.0, 6.0, 700.0,
     EXP64_INV_LN2, EXP64_LN2_HI, EXP64_LN2_LO};
 
-// Philox4x32-10 (Salmon et al., SC'11): 10 rounds of two 32x32->64 products,
-// Weyl key schedule.  c = counter in, output out (in place).
 // degrees of the exp and log1p kernels (fit_device_polys.py): exp(r), |r| <= ln2/128,
 // degree 6 (3.4e-21) or 5 (2.2e-18 relative); (log1p(r) - r)/r^2, |r| <= 2^-7, degree 5
 // or 4 (5.2e-13 relative, i.e. <= 1.6e-17 absolute in log1p(r))
-#ifndef QMCCPW_LOGEXP_LO
-#define QMCCPW_LOGEXP_LO 1
-#endif
 // degree of the Mills-ratio polynomial: 27 (6.2e-17) or 23 (5.3e-17, the same rounding floor)
-#ifndef QMCCPW_MILLS_DEG
-#define QMCCPW_MILLS_DEG 23
-#endif
 constexpr int kMillsDeg = QMCCPW_MILLS_DEG;
 #if QMCCPW_MILLS_DEG == 27
 #define MILLS_P MILLS_H
@@ -59,6 +62,8 @@ constexpr int kExpDeg = 6, kLogDeg = 5;
 #define LOG_P LOG1P_L
 #endif
 
+// Philox4x32-10 (Salmon et al., SC'11): 10 rounds of two 32x32->64 products,
+// Weyl key schedule.  c = counter in, output out (in place).
 __device__ __forceinline__ void philox4x32_10(uint32_t c[4], uint32_t k0, uint32_t k1) {
 #pragma unroll
     for (int r = 0; r < 10; ++r) {
@@ -170,9 +175,6 @@ __device__ __forceinline__ double fast_log(double t) {
 
 // degree of the central Phi^{-1} polynomial (fit_device_polys.py: max rel. error of the
 // double-rounded polynomial 4.3e-17 at 24, 1.7e-16 at 23, 3.3e-16 at 22)
-#ifndef QMCCPW_ICDF_DEG
-#define QMCCPW_ICDF_DEG 22
-#endif
 constexpr int kIcdfDeg = QMCCPW_ICDF_DEG;
 #if QMCCPW_ICDF_DEG == 24
 #define ICDF_C ICDF_CENTRAL
