@@ -16,9 +16,16 @@ namespace qmccpw {
 // resident blocks per SM the register allocator must allow (128 threads each); 0 = ptxas'
 // own choice.  Measured on C4 (ms/step): BB-W1 34.3 (ptxas, 96 regs) / 33.8 (7) / 33.4
 // (8: 64 regs, a few spills to L1); STD-W1 33.1 (4) / 31.9 (5) / 31.2 (6); v11: 27.20 (6) / 27.03 (7) / 27.4 (8)
+// MC+AV-CPW with the bridge: 140 registers uncapped at v18 (3 blocks/SM; 46.2 -> 51.5 ms
+// against v17), so it is capped at 4 blocks
+#ifndef QMCCPW_BBAV_MINB
+#define QMCCPW_BBAV_MINB 4
+#endif
 template <int CONSTR, int COND, int METHOD>
 constexpr int paths_min_blocks() {
-    return (COND == kW1 && METHOD == kQmc) ? (CONSTR == kBB ? QMCCPW_BB_MINB : CONSTR == kStd ? QMCCPW_STD_MINB : 0) : 0;
+    return (COND == kW1 && METHOD == kQmc) ? (CONSTR == kBB ? QMCCPW_BB_MINB : CONSTR == kStd ? QMCCPW_STD_MINB : 0)
+           : (COND == kW1 && METHOD == kMcAv && CONSTR == kBB) ? QMCCPW_BBAV_MINB
+                                                                : 0;
 }
 // OWEN: nested scrambling of the Sobol' coordinates (row f4) -- a template flag so
 // that the other randomisations pay nothing for it (measured 0.5-4 % as a runtime test)
