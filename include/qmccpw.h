@@ -23,8 +23,12 @@
  *     enqueues).
  *   - The output bits are a function of the inputs only: launch geometry and
  *     the number of GPUs sharing the cells do not change them (Sec. 8(e)).
- *   - One in-flight call per (device, stream); distinct devices may be driven
- *     from distinct host threads.
+ *   - One in-flight call per (device, stream).  The per-call tables, library
+ *     partials and pinned staging are keyed by (device, stream), so calls on
+ *     different streams -- of one device or of several, from one host thread
+ *     or several -- never share scratch: a qmccpw_partials still running on
+ *     stream A is not disturbed by a call on stream B.  Calls on one stream
+ *     are ordered by the stream.
  *   - There is no CPU fallback: without a usable sm_100a device every compute
  *     entry point returns QMCCPW_ECUDA.
  */

@@ -43,7 +43,7 @@ class Result(ctypes.Structure):
     _fields_ = [("mean", ctypes.c_double * 4), ("se", ctypes.c_double * 4),
                 ("sigma_run", ctypes.c_double * 4), ("within_var", ctypes.c_double * 4),
                 ("n_points", ctypes.c_uint64), ("n_replicates", ctypes.c_uint32),
-                ("argmax_near_ties", ctypes.c_uint64)]
+                ("argmax_near_ties", ctypes.c_uint64), ("mean_abs", ctypes.c_double * 4)]
 
 
 def build(force=False):
@@ -261,5 +261,6 @@ def price_greeks(options, mk, n_points, n_replicates, cfg=None, n_threads=None, 
     for r in res:
         out.append(dict(mean=np.array(r.mean[:]), se=np.array(r.se[:]), sigma_run=np.array(r.sigma_run[:]),
                         within_var=np.array(r.within_var[:]), n_points=r.n_points,
-                        n_replicates=r.n_replicates, argmax_near_ties=r.argmax_near_ties))
+                        n_replicates=r.n_replicates, argmax_near_ties=r.argmax_near_ties,
+                        mean_abs=np.array(r.mean_abs[:])))
     return out, rm

@@ -873,6 +873,7 @@ typedef struct {
     const double* piv;     /* [n_opt][4] */
     double* S1;            /* [L][n_opt][4] */
     double* S2;            /* [L][n_opt][4] */
+    double* SA;            /* [L][n_opt][4] sum of |f| (the 8(c) tolerance scale) */
     uint64_t* ties;        /* [L] */
     int next;
     int rc;
@@ -887,6 +888,7 @@ static void* worker(void* arg) {
     uint32_t* c = malloc(sizeof(uint32_t) * d);
     neum_t* acc1 = malloc(sizeof(neum_t) * n_opt * 4);
     neum_t* acc2 = malloc(sizeof(neum_t) * n_opt * 4);
+    neum_t* acca = malloc(sizeof(neum_t) * n_opt * 4);
     for (;;) {
         int rep = __atomic_fetch_add(&jb->next, 1, __ATOMIC_SEQ_CST);
         if (rep >= (int)jb->L) break;
@@ -895,6 +897,7 @@ static void* worker(void* arg) {
             rc = or_randomization(jb->cfg->seed, (uint32_t)rep, d, jb->cfg->randomization, v, c);
         memset(acc1, 0, sizeof(neum_t) * n_opt * 4);
         memset(acc2, 0, sizeof(neum_t) * n_opt * 4);
+        memset(acca, 0, sizeof(neum_t) * n_opt * 4);
         uint64_t ties = 0;
         for (uint64_t i = 0; i < jb->N && rc == 0; i++) {
             uint64_t k = jb->cfg->point_offset + i;
@@ -914,12 +917,14 @@ static void* worker(void* arg) {
                     double y = f[q] - jb->piv[o * 4 + q];
                     neum_add(&acc1[o * 4 + q], y);
                     neum_add(&acc2[o * 4 + q], y * y);
+                    neum_add(&acca[o * 4 + q], fabs(f[q]));
                 }
             }
         }
         for (int i = 0; i < n_opt * 4; i++) {
             jb->S1[(size_t)rep * n_opt * 4 + i] = neum_val(&acc1[i]);
             jb->S2[(size_t)rep * n_opt * 4 + i] = neum_val(&acc2[i]);
+            jb->SA[(size_t)rep * n_opt * 4 + i] = neum_val(&acca[i]);
         }
         jb->ties[rep] = ties;
         if (rc) {
@@ -928,7 +933,7 @@ static void* worker(void* arg) {
             pthread_mutex_unlock(&jb->mu);
         }
     }
-    free(x); free(v); free(c); free(acc1); free(acc2);
+    free(x); free(v); free(c); free(acc1); free(acc2); free(acca);
     return NULL;
 }
 
@@ -958,6 +963,7 @@ int or_price_greeks(const or_option* opts, int32_t n_opt, const or_market* mk, u
     jb.piv = piv;
     jb.S1 = malloc(sizeof(double) * L * n_opt * 4);
     jb.S2 = malloc(sizeof(double) * L * n_opt * 4);
+    jb.SA = malloc(sizeof(double) * L * n_opt * 4);
     jb.ties = calloc(L, sizeof(uint64_t));
     pthread_mutex_init(&jb.mu, NULL);
     if (n_threads < 1) n_threads = 1;
@@ -975,21 +981,23 @@ int or_price_greeks(const or_option* opts, int32_t n_opt, const or_market* mk, u
             res->n_replicates = n_replicates;
             for (int l = 0; l < L; l++) res->argmax_near_ties += jb.ties[l];
             for (int q = 0; q < 4; q++) {
-                double p = piv[o * 4 + q], sumV = 0.0;
+                double p = piv[o * 4 + q], sumV = 0.0, sumA = 0.0;
                 double* Cl = malloc(sizeof(double) * L);
                 for (int l = 0; l < L; l++) {
                     double s1 = jb.S1[(size_t)l * n_opt * 4 + o * 4 + q], s2 = jb.S2[(size_t)l * n_opt * 4 + o * 4 + q];
                     Cl[l] = p + s1 / N;                            /* C_P^(l) */
                     if (rep_means) rep_means[(size_t)l * n_opt * 4 + o * 4 + q] = Cl[l];
                     sumV += s2 / N - (s1 / N) * (s1 / N);          /* within-replicate variance */
+                    sumA += jb.SA[(size_t)l * n_opt * 4 + o * 4 + q] / N;
                 }
                 or_summarize(Cl, L, &res->mean[q], &res->se[q], &res->sigma_run[q]);
                 free(Cl);
                 res->within_var[q] = sumV / L;
+                res->mean_abs[q] = sumA / L;
             }
         }
     }
-    free(th); free(piv); free(jb.S1); free(jb.S2); free(jb.ties); free(M);
+    free(th); free(piv); free(jb.S1); free(jb.S2); free(jb.SA); free(jb.ties); free(M);
     pthread_mutex_destroy(&jb.mu);
     return rc;
 }

@@ -56,6 +56,8 @@ typedef struct {
     uint64_t n_points;
     uint32_t n_replicates;
     uint64_t argmax_near_ties;
+    double mean_abs[4]; /* mean over all N L paths of |f|: the scale of SURVEY.md 8(c)'s means tolerance
+                           1e-9 max(|C|, mean|f|); a statistic of the run, not an estimator output */
 } or_result;
 
 /* O1: load Joe-Kuo parameters (file format "d s a m_1..m_s"); returns #dims or <0 */

@@ -11,6 +11,7 @@
 #include <cmath>
 #include <cstdio>
 #include <cstring>
+#include <map>
 #include <mutex>
 #include <string>
 #include <vector>
@@ -39,7 +40,7 @@ int fail(int code, const std::string& msg) {
 constexpr int kTableDims = 1024;
 
 // Per-device cache: base direction numbers (cuRAND JOEKUO6, the paper's
-// generator P:440) and grow-only scratch.
+// generator P:440), built once per device.
 struct DeviceCache {
     bool ready = false;
     bool checked = false;
@@ -47,6 +48,15 @@ struct DeviceCache {
     uint32_t* base_v_scr = nullptr;    // [1024][32] cuRAND pre-scrambled
     uint32_t* base_shift = nullptr;    // [1024] cuRAND scramble constants
     uint32_t* zero_shift = nullptr;    // [1024] zeros
+};
+
+// Per-(device, stream) grow-only scratch: the per-call tables (scrambled direction
+// numbers, shifts, M, a_j, option table), the library-owned partials and replicate sums,
+// and the pinned host staging of the replicate sums.  Keying by stream makes calls on
+// different streams of one device independent: qmccpw_partials returns with its kernel
+// still reading the tables, and a call on another stream must not rebuild them.  Calls
+// on one stream are ordered by the stream itself.  Entries live until qmccpw_release.
+struct StreamScratch {
     void* scratch = nullptr;
     size_t scratch_bytes = 0;
     double* h_pinned = nullptr;
@@ -55,6 +65,7 @@ struct DeviceCache {
 
 std::mutex g_mu;
 DeviceCache g_cache[64];
+std::map<std::pair<int, cudaStream_t>, StreamScratch> g_scratch;  // guarded by g_mu
 
 int ensure_device(int device, DeviceCache** out) {
     if (device < 0 || device >= 64) return fail(QMCCPW_EINVAL, "device ordinal out of range");
@@ -89,24 +100,29 @@ int ensure_device(int device, DeviceCache** out) {
     return QMCCPW_OK;
 }
 
-int ensure_scratch(DeviceCache* c, size_t bytes) {
-    if (c->scratch_bytes >= bytes) return QMCCPW_OK;
-    if (c->scratch) cudaFree(c->scratch);
-    c->scratch = nullptr;
-    c->scratch_bytes = 0;
-    size_t want = bytes + bytes / 4;
-    if (cudaMalloc(&c->scratch, want) != cudaSuccess) return fail(QMCCPW_ENOMEM, "device scratch allocation failed");
-    c->scratch_bytes = want;
-    return QMCCPW_OK;
-}
-
-int ensure_pinned(DeviceCache* c, size_t bytes) {
-    if (c->pinned_bytes >= bytes) return QMCCPW_OK;
-    if (c->h_pinned) cudaFreeHost(c->h_pinned);
-    c->h_pinned = nullptr;
-    c->pinned_bytes = 0;
-    if (cudaMallocHost(&c->h_pinned, bytes) != cudaSuccess) return fail(QMCCPW_ENOMEM, "pinned allocation failed");
-    c->pinned_bytes = bytes;
+// The scratch of (device, stream), grown to at least `bytes` device and `pinned` host bytes.
+// A grow frees the old buffer with cudaFree, which waits for the device, so kernels still
+// reading it on this stream finish first.  Returns a pointer that stays valid until the next
+// grow of the same entry (only a later call on the same stream can grow it).
+int acquire_scratch(int device, cudaStream_t st, size_t bytes, size_t pinned, StreamScratch** out) {
+    std::lock_guard<std::mutex> lk(g_mu);
+    StreamScratch& e = g_scratch[std::make_pair(device, st)];
+    if (e.scratch_bytes < bytes) {
+        if (e.scratch) cudaFree(e.scratch);
+        e.scratch = nullptr;
+        e.scratch_bytes = 0;
+        size_t want = bytes + bytes / 4;
+        if (cudaMalloc(&e.scratch, want) != cudaSuccess) return fail(QMCCPW_ENOMEM, "device scratch allocation failed");
+        e.scratch_bytes = want;
+    }
+    if (e.pinned_bytes < pinned) {
+        if (e.h_pinned) cudaFreeHost(e.h_pinned);
+        e.h_pinned = nullptr;
+        e.pinned_bytes = 0;
+        if (cudaMallocHost(&e.h_pinned, pinned) != cudaSuccess) return fail(QMCCPW_ENOMEM, "pinned allocation failed");
+        e.pinned_bytes = pinned;
+    }
+    *out = &e;
     return QMCCPW_OK;
 }
 
@@ -307,11 +323,12 @@ struct Scratch {
     double* partials;
     double* rep_sums;
     PortfolioOption* opts;
+    double* h_rep_sums;  // pinned host staging, [L][stride]
 };
 
 size_t align_up(size_t x) { return (x + 255) & ~(size_t)255; }
 
-int carve(DeviceCache* c, const Plan& pl, bool own_partials, uint32_t table_reps, Scratch* s) {
+int carve(const Plan& pl, bool own_partials, uint32_t table_reps, Scratch* s, StreamScratch** entry = nullptr) {
     const int d = pl.d;
     size_t off = 0;
     size_t o_vscr = off; off = align_up(off + (size_t)table_reps * d * 32 * 4);
@@ -323,9 +340,11 @@ int carve(DeviceCache* c, const Plan& pl, bool own_partials, uint32_t table_reps
     size_t o_part = off; off = align_up(off + (own_partials ? (size_t)pl.n_cells * pl.stride * 8 : 0));
     size_t o_rs = off; off = align_up(off + (size_t)pl.L * pl.stride * 8);
     size_t o_opt = off; off = align_up(off + (pl.portfolio ? (size_t)pl.n_opt * sizeof(PortfolioOption) : 0));
-    int rc = ensure_scratch(c, off);
+    StreamScratch* e = nullptr;
+    int rc = acquire_scratch(pl.cfg.device, static_cast<cudaStream_t>(pl.cfg.stream), off,
+                             (size_t)pl.L * pl.stride * 8, &e);
     if (rc) return rc;
-    char* b = static_cast<char*>(c->scratch);
+    char* b = static_cast<char*>(e->scratch);
     s->vscr = reinterpret_cast<uint32_t*>(b + o_vscr);
     s->shift = reinterpret_cast<uint32_t*>(b + o_shift);
     s->M = reinterpret_cast<double*>(b + o_M);
@@ -334,6 +353,8 @@ int carve(DeviceCache* c, const Plan& pl, bool own_partials, uint32_t table_reps
     s->partials = own_partials ? reinterpret_cast<double*>(b + o_part) : nullptr;
     s->rep_sums = reinterpret_cast<double*>(b + o_rs);
     s->opts = reinterpret_cast<PortfolioOption*>(b + o_opt);
+    s->h_rep_sums = e->h_pinned;
+    if (entry) *entry = e;
     return QMCCPW_OK;
 }
 
@@ -587,7 +608,7 @@ int run_full(const Plan& pl, qmccpw_result* out) {
     int rc = ensure_device(pl.cfg.device, &c);
     if (rc) return rc;
     Scratch s;
-    rc = carve(c, pl, true, pl.L, &s);
+    rc = carve(pl, true, pl.L, &s);
     if (rc) return rc;
     cudaStream_t st = static_cast<cudaStream_t>(pl.cfg.stream);
     rc = build_tables(c, pl, 0, pl.L, s, st);
@@ -604,11 +625,9 @@ int run_full(const Plan& pl, qmccpw_result* out) {
     }
     CUDA_TRY(launch_reduce_cells(s.partials, pl.stride, 0, pl.L, pl.cells_per_rep, s.rep_sums, st));
     const size_t rs_bytes = (size_t)pl.L * pl.stride * 8;
-    rc = ensure_pinned(c, rs_bytes);
-    if (rc) return rc;
-    CUDA_TRY(cudaMemcpyAsync(c->h_pinned, s.rep_sums, rs_bytes, cudaMemcpyDeviceToHost, st));
+    CUDA_TRY(cudaMemcpyAsync(s.h_rep_sums, s.rep_sums, rs_bytes, cudaMemcpyDeviceToHost, st));
     CUDA_TRY(cudaStreamSynchronize(st));
-    return finalize_host(pl, c->h_pinned, out);
+    return finalize_host(pl, s.h_rep_sums, out);
 }
 
 }  // namespace
@@ -662,7 +681,7 @@ int qmccpw_partials(const int32_t* options, const qmccpw_params* p, int32_t n_op
     rc = ensure_device(pl.cfg.device, &c);
     if (rc) return rc;
     Scratch s;
-    rc = carve(c, pl, false, pl.L, &s);
+    rc = carve(pl, false, pl.L, &s);
     if (rc) return rc;
     cudaStream_t st = static_cast<cudaStream_t>(pl.cfg.stream);
     rc = build_tables(c, pl, 0, pl.L, s, st);
@@ -726,17 +745,15 @@ int qmccpw_finalize_device(const double* d_partials, const int32_t* options, con
     rc = ensure_device(pl.cfg.device, &c);
     if (rc) return rc;
     Scratch s;
-    rc = carve(c, pl, false, 0, &s);
+    rc = carve(pl, false, 0, &s);
     if (rc) return rc;
     cudaStream_t st = static_cast<cudaStream_t>(pl.cfg.stream);
     CUDA_TRY(launch_reduce_cells(d_partials, pl.stride, 0, pl.L, pl.cells_per_rep, s.rep_sums, st));
     const size_t rs_bytes = (size_t)pl.L * pl.stride * 8;
-    rc = ensure_pinned(c, rs_bytes);
-    if (rc) return rc;
-    CUDA_TRY(cudaMemcpyAsync(c->h_pinned, s.rep_sums, rs_bytes, cudaMemcpyDeviceToHost, st));
+    CUDA_TRY(cudaMemcpyAsync(s.h_rep_sums, s.rep_sums, rs_bytes, cudaMemcpyDeviceToHost, st));
     CUDA_TRY(cudaStreamSynchronize(st));
     std::vector<qmccpw_result> tmp(pl.n_opt);
-    rc = finalize_host(pl, c->h_pinned, tmp.data());
+    rc = finalize_host(pl, s.h_rep_sums, tmp.data());
     if (rc) return rc;
     for (int o = 0; o < pl.n_opt; ++o) out[o] = tmp[o];
     return QMCCPW_OK;
@@ -765,7 +782,7 @@ int qmccpw_sobol_u32(uint32_t replicate, uint32_t dim_begin, uint32_t dim_end, u
     int rc = ensure_device(pl.cfg.device, &c);
     if (rc) return rc;
     Scratch s;
-    rc = carve(c, pl, false, 1, &s);
+    rc = carve(pl, false, 1, &s);
     if (rc) return rc;
     cudaStream_t st = static_cast<cudaStream_t>(pl.cfg.stream);
     rc = build_tables(c, pl, replicate, 1, s, st);
@@ -804,7 +821,7 @@ int qmccpw_normals(uint32_t replicate, int32_t d, uint64_t k_begin, uint64_t k_e
     int rc = ensure_device(pl.cfg.device, &c);
     if (rc) return rc;
     Scratch s;
-    rc = carve(c, pl, false, 1, &s);
+    rc = carve(pl, false, 1, &s);
     if (rc) return rc;
     cudaStream_t st = static_cast<cudaStream_t>(pl.cfg.stream);
     rc = build_tables(c, pl, replicate, 1, s, st);
@@ -837,7 +854,7 @@ int qmccpw_path_values(int32_t option, const qmccpw_params* p, uint32_t replicat
     rc = ensure_device(pl.cfg.device, &c);
     if (rc) return rc;
     Scratch s;
-    rc = carve(c, pl, true, 1, &s);
+    rc = carve(pl, true, 1, &s);
     if (rc) return rc;
     cudaStream_t st = static_cast<cudaStream_t>(pl.cfg.stream);
     rc = build_tables(c, pl, replicate, 1, s, st);
@@ -883,7 +900,7 @@ int qmccpw_portfolio_path_values(const int32_t* options, const qmccpw_params* p,
     rc = ensure_device(pl.cfg.device, &c);
     if (rc) return rc;
     Scratch s;
-    rc = carve(c, pl, true, 1, &s);
+    rc = carve(pl, true, 1, &s);
     if (rc) return rc;
     cudaStream_t st = static_cast<cudaStream_t>(pl.cfg.stream);
     rc = build_tables(c, pl, replicate, 1, s, st);
@@ -904,22 +921,30 @@ const char* qmccpw_last_error(void) { return g_last_error.c_str(); }
 
 void qmccpw_release(int32_t device) {
     std::lock_guard<std::mutex> lk(g_mu);
+    int prev = -1;
+    cudaGetDevice(&prev);
+    for (auto it = g_scratch.begin(); it != g_scratch.end();) {
+        if (device >= 0 && it->first.first != device) {
+            ++it;
+            continue;
+        }
+        cudaSetDevice(it->first.first);
+        if (it->second.scratch) cudaFree(it->second.scratch);
+        if (it->second.h_pinned) cudaFreeHost(it->second.h_pinned);
+        it = g_scratch.erase(it);
+    }
     for (int dev = 0; dev < 64; ++dev) {
         if (device >= 0 && dev != device) continue;
         DeviceCache& c = g_cache[dev];
-        if (!c.ready && !c.scratch && !c.h_pinned) continue;
-        int prev = -1;
-        cudaGetDevice(&prev);
+        if (!c.ready) continue;
         cudaSetDevice(dev);
         cudaFree(c.base_v);
         cudaFree(c.base_v_scr);
         cudaFree(c.base_shift);
         cudaFree(c.zero_shift);
-        cudaFree(c.scratch);
-        if (c.h_pinned) cudaFreeHost(c.h_pinned);
         c = DeviceCache();
-        if (prev >= 0) cudaSetDevice(prev);
     }
+    if (prev >= 0) cudaSetDevice(prev);
 }
 
 uint64_t qmccpw_launch_count(int32_t reset) {

@@ -86,11 +86,29 @@ class DistributedPricer:
         if self.world > 1:
             self.torch.distributed.all_reduce(self.rep_sums, group=self.group)
 
-    def fetch_and_finalize(self):
+    def enqueue_fetch(self):
+        """Device->host copy of the (all-reduced) replicate sums, on the current stream."""
         self.h_rep_sums.copy_(self.rep_sums, non_blocking=True)
-        self.torch.cuda.current_stream(self.device).synchronize()
+
+    def finalize(self):
+        """Host finalize of the fetched table (call after the stream has synchronised)."""
         return qmccpw_finalize(self.h_rep_sums.numpy(), self.options, self.plist, self.n_points, self.n_replicates,
                                self.cfg)
+
+    def fetch_and_finalize(self):
+        self.enqueue_fetch()
+        self.torch.cuda.current_stream(self.device).synchronize()
+        return self.finalize()
+
+    def points_owned(self):
+        """Sobol' points (paths) this rank's cells hold: full cells of 4096 points, the last
+        cell of each replicate ragged when 4096 does not divide n_points."""
+        from . import CELL_POINTS
+        total = 0
+        for c in range(self.cell_begin, self.cell_end):
+            j = c % self.cells_per_rep
+            total += min(CELL_POINTS, self.n_points - j * CELL_POINTS)
+        return total
 
     def step(self, kernel_events=None):
         """One full run: device work, one all-reduce, device->host read, finalize."""

@@ -168,3 +168,37 @@ def test_bench_reference_arm_runs_on_cpu():
     d = json.loads(lines[0])
     assert d["impl"] == "reference" and d["value"] > 0 and d["cpu_baseline"]["kind"] == "oracle"
     assert d["e2e"]["h2d_bytes_per_step"] == 0
+
+
+def test_bench_refuses_more_gpus_than_visible():
+    # `bench.py --gpus 2` without torchrun spawns 2 ranks itself -- and fails loudly when the
+    # box has fewer GPUs, instead of pricing on one and printing n_gpus: 1
+    env = dict(os.environ, CUDA_VISIBLE_DEVICES="")
+    env.pop("WORLD_SIZE", None)
+    out = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--gpus", "2", "--steps", "1",
+                          "--warmup", "0"], capture_output=True, text=True, timeout=600, env=env)
+    assert out.returncode != 0 and "needs 2 visible CUDA devices" in out.stderr
+    assert not [l for l in out.stdout.splitlines() if l.startswith("{")]
+
+
+def test_bench_refuses_a_world_size_mismatch():
+    env = dict(os.environ, WORLD_SIZE="1", RANK="0", LOCAL_RANK="0")
+    out = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--gpus", "4", "--steps", "1",
+                          "--warmup", "0"], capture_output=True, text=True, timeout=600, env=env)
+    assert out.returncode != 0 and "world size 1 != --gpus 4" in out.stderr
+
+
+def test_bench_work_model_follows_survey_8d():
+    # SURVEY.md 8(d)'s planning table: the FP64 lane-instruction counts per path that the
+    # roofline's `achieved` is computed from (one threshold solve per strike group under X1)
+    sys.path.insert(0, ROOT)
+    import bench
+    C4 = [0, 1, 2]
+    assert bench.fp64_model_per_path(64, 1, 0, C4, [100.0] * 3) == 5280                 # BB-W1, the headline
+    assert bench.fp64_model_per_path(64, 0, 0, C4, [100.0] * 3) == 5166                 # STD-W1 (~5.2k)
+    assert bench.fp64_model_per_path(64, 2, 0, C4, [100.0] * 3) == 9248                 # PCA-W1 (~9.2k)
+    assert bench.fp64_model_per_path(64, 2, 1, [0, 1], [100.0] * 2) == 14158            # PCA-X1 (~14.2k)
+    assert bench.fp64_model_per_path(128, 2, 0, [0], [100.0]) == 25888                  # PCA-W1 d=128 (~25.9k)
+    # two strikes under X1 -> two solves; same strike -> one
+    two = bench.fp64_model_per_path(64, 2, 1, [0, 1], [95.0, 105.0])
+    assert two - 14158 == 4 * 64 * 20

@@ -2,20 +2,19 @@
 seeded points.  Tolerances:
   Sobol' integers        bit-exact
   normals                |dx| <= 2e-15 max(1, |x|)
-  per-path values        |df| <= 1e-12 (|f| + |pivot_K| + |pivot_ATM|); gamma x max(1, 0.03/(sigma^2 t_1))
-                         (pivot = the d = 1 Black-Scholes value of that output at the
-                         option's strike and at K = S0: the output's natural scale,
-                         so deep in/out-of-the-money Greeks near 0 keep a floor)
-                         (the threshold psi / u* carries an absolute rounding of
-                         ~c eps / (sigma sqrt t_1), c <~ 30 measured, and gamma
-                         differentiates it once more -> relative ~ c eps / s^2)
-  replicate / run means  |dC| <= 1e-9 sqrt(within_var + C^2)   (>= mean|f|; + |pivot_ATM| for the
-                         portfolio, whose deep in-the-money lookback gammas are ~1e-24)
+  per-path values        |df| <= 1e-12 (|f| + |pivot_K|)    (pivot_K = the d = 1
+                         Black-Scholes value of that output at the option's strike);
+                         gamma x max(1, 0.03/(sigma^2 t_1)): the threshold psi / u* carries
+                         an absolute rounding of ~c eps / (sigma sqrt t_1) and gamma
+                         differentiates it once more -> relative ~ c eps / s^2 (measured
+                         maximum in DESIGN.md 6 and tests/tools/parity_report.py)
+                         portfolio only: + |pivot_ATM| (deep in-the-money lookback gammas ~1e-24)
+  replicate / run means  |dC| <= 1e-9 max(|C|, mean|f|)   (SURVEY 8(c); mean|f| from the oracle;
+                         + |pivot_ATM| for the portfolio's ~1e-24 gammas)
   SE, sigma_run          <= 1e-6 relative (+ a 1e-12 x scale floor: at d = 1 the
                          estimator is exact per path and the spread is rounding)
   counters               equal
 """
-import math
 
 import numpy as np
 import pytest
@@ -91,7 +90,7 @@ def _pv_check(q, O, otype, K, d, constr, cond, method, rep, k0, k1, S0=W.S0, sig
     g = q.qmccpw_path_values(otype, p, rep, k0, k1, qcfg(q, constr, cond, method, rand=rand))
     mk = O.market(S0, r, sigma, T, d)
     o = O.path_values(otype, K, mk, ocfg(O, constr, cond, method, rand=rand), rep, k0, k1)
-    piv = np.abs(O.pivots(otype, K, mk)) + np.abs(O.pivots(otype, S0, mk))
+    piv = np.abs(O.pivots(otype, K, mk))
     err = np.abs(g - o) / (np.abs(o) + piv)
     s2 = sigma * sigma * T / d
     tol = np.array([1e-12, 1e-12, 1e-12, 1e-12 * max(1.0, 0.03 / s2)])
@@ -205,7 +204,7 @@ def _means_check(gres, ores, floor=0.0):
     """floor: the output's natural scale (|ATM Black-Scholes value|) where the mean itself can be ~0."""
     for gr, orr in zip(gres, ores):
         g = gr.as_dict() if hasattr(gr, "as_dict") else gr
-        scale = np.sqrt(np.maximum(orr["within_var"], 0) + orr["mean"] ** 2) + floor
+        scale = np.maximum(np.abs(orr["mean"]), orr["mean_abs"]) + floor
         assert np.all(np.abs(g["mean"] - orr["mean"]) <= 1e-9 * scale), (g["mean"], orr["mean"])
         if orr["n_replicates"] > 1:
             assert np.all(np.abs(g["se"] - orr["se"]) <= 1e-6 * orr["se"] + 1e-12 * scale), (g["se"], orr["se"])
@@ -310,7 +309,7 @@ def test_bench_launch_config_sampled_replicates(q, O):
             piv = O.pivots(opts[oi], 100.0, O.market(d=d))
             for qq in range(4):
                 C_gpu = piv[qq] + s1[oi * 8 + qq * 2] / N
-                scale = math.sqrt(max(o[oi]["within_var"][qq], 0) + o[oi]["mean"][qq] ** 2)
+                scale = max(abs(o[oi]["mean"][qq]), o[oi]["mean_abs"][qq])
                 assert abs(C_gpu - rm[rep, oi, qq]) <= 1e-9 * scale, (rep, oi, qq, C_gpu, rm[rep, oi, qq])
 
 
@@ -335,7 +334,7 @@ def test_c3_full_size_sampled_replicates(q, O, constr, cond):
         assert s1[8 + 2] == N                                   # every point of the replicate evaluated
         for qq in range(4):
             C_gpu = piv[qq] + s1[qq * 2] / N
-            scale = math.sqrt(max(o[0]["within_var"][qq], 0) + o[0]["mean"][qq] ** 2)
+            scale = max(abs(o[0]["mean"][qq]), o[0]["mean_abs"][qq])
             assert abs(C_gpu - rm[rep, 0, qq]) <= 1e-9 * scale, (rep, qq, C_gpu, rm[rep, 0, qq])
 
 
@@ -388,7 +387,7 @@ def test_c5_bench_launch_sampled_options(q, O):
             assert s1[1024 * 8 + 2] == N
             for qq in range(4):
                 C_gpu = piv[qq] + s1[i * 8 + qq * 2] / N
-                scale = math.sqrt(max(ref[0]["within_var"][qq], 0) + ref[0]["mean"][qq] ** 2) + floor[qq]
+                scale = max(abs(ref[0]["mean"][qq]), ref[0]["mean_abs"][qq]) + floor[qq]
                 assert abs(C_gpu - rm[rep, 0, qq]) <= 1e-9 * scale, (i, rep, qq, C_gpu, rm[rep, 0, qq])
 
 
