@@ -7,7 +7,13 @@
     and QMC+BB-CPW at the paper's P = 2^15, d = 64, K = 100.  The paper's
     randomisation and L = 500 runs are unknown (reading 10), so the pin is an
     order-of-magnitude band (x/20).  It catches the printed lookback-vega
-    1/d (reading 3), which moves that VRF by ~10^3.
+    1/d (reading 3), which moves that VRF by ~10^3;
+  * the comparison methods MC-CPW and MC+AV-CPW (reading 25):
+    unbiased against LR+MC and QMC+BB-CPW (4.5 SE), exact Black-Scholes at
+    d = 1 (a dropped 1/2 in the antithetic average doubles it), the antithetic
+    estimate even in the draw (a partner built from +x is not), and its
+    variance cut >= 3x for the arithmetic and lookback deltas (paper ~9x and
+    ~7.5x, P:675/682, P:747/754).
 """
 import math
 
@@ -59,6 +65,13 @@ def test_all_modes_estimate_the_same_greeks(O):
         runs[(constr, 0)] = O.price_greeks(opts, mk, N, L, O.config(construction=constr))[0]
     runs[(2, 1)] = O.price_greeks(opts, mk, N, L, O.config(construction=2, conditioning=1))[0]
     runs[(1, 1)] = O.price_greeks(opts, mk, N, L, O.config(construction=1, conditioning=1))[0]
+    # the paper's comparison methods: MC-CPW and MC+AV-CPW (Philox normals
+    # through the same CPW estimators; STD and the bridge) -- a dropped 1/2 in the antithetic
+    # average would double every MC+AV mean
+    for method in (2, 3):
+        for constr in (0, 1):
+            runs[("mc", method, constr)] = O.price_greeks(opts, mk, N, L, O.config(method=method,
+                                                                                   construction=constr))[0]
     for key, res in runs.items():
         for o in range(len(res)):
             _agree(res[o], lr[o])
@@ -93,3 +106,52 @@ def test_vrf_magnitudes_match_paper_tables(O):
                 vrf = (lr[o]["sigma_run"][q] / res[o]["sigma_run"][q]) ** 2
                 paper = PAPER_VRF_K100_D64[(o, name)][i]
                 assert paper / 20 <= vrf <= paper * 20, (o, name, q, vrf, paper)
+
+
+@pytest.mark.parametrize("method", [2, 3])
+@pytest.mark.parametrize("otype", [0, 1, 2])
+def test_mc_methods_at_d1_equal_black_scholes(O, method, otype):
+    # at d = 1 the CPW estimator is exact for every draw, so MC-CPW and the
+    # antithetic average of MC+AV-CPW both return the Black-Scholes values on every path
+    # (a dropped 1/2 in the average would return twice them)
+    from tests.test_oracle_estimators import bs
+    for K in (90.0, 100.0, 110.0):
+        mk = O.market(d=1)
+        pv = O.path_values(otype, K, mk, O.config(method=method), 2, 0, 64)
+        ref = bs(otype, 100.0, K, 0.1, 0.2, 1.0)
+        assert np.allclose(pv, ref[None, :], rtol=1e-13, atol=1e-15), (method, otype, K)
+
+
+def test_antithetic_estimate_is_even_in_the_draw(O):
+    # MC+AV-CPW averages the estimator over the pair (x, -x): as a function of the
+    # draw it is therefore EVEN -- f_AV(x) = f_AV(-x) for every x, in every construction and
+    # option -- while the plain estimator is not.  Building the partner from +x breaks this.
+    rng = np.random.default_rng(11)
+    mk = O.market(d=64)
+    for constr in (0, 1):
+        for otype in (0, 1, 2):
+            odd_seen = False
+            for _ in range(8):
+                x = rng.standard_normal(64)
+                a = O.estimate(otype, 100.0, mk, x, method=3, construction=constr)
+                b = O.estimate(otype, 100.0, mk, -x, method=3, construction=constr)
+                assert np.array_equal(a, b), (constr, otype)
+                p = O.estimate(otype, 100.0, mk, x, method=2, construction=constr)
+                m = O.estimate(otype, 100.0, mk, -x, method=2, construction=constr)
+                odd_seen |= not np.allclose(p, m)
+            assert odd_seen
+
+
+@pytest.mark.slow
+def test_antithetic_pairing_reduces_the_variance(O):
+    # P:682 / P:675 (Table 1): VRF of the arithmetic delta 963 (MC+AV-CPW) against 106 (MC-CPW),
+    # i.e. the antithetic average cuts the per-path variance ~9x at d = 64, K = 100.  A pairing
+    # with +x (AV == MC) gives 1x; the pin asks for >= 3x on the within-replicate variance, and
+    # the same direction for the arithmetic vega and the lookback delta (Tables 1 and 3).
+    mk = O.market(d=64)
+    opts = [(0, 100.0), (2, 100.0)]
+    mc, _ = O.price_greeks(opts, mk, 1 << 13, 8, O.config(method=2, construction=0))
+    av, _ = O.price_greeks(opts, mk, 1 << 13, 8, O.config(method=3, construction=0))
+    assert mc[0]["within_var"][1] / av[0]["within_var"][1] >= 3.0      # arithmetic delta
+    assert mc[0]["within_var"][2] / av[0]["within_var"][2] >= 1.5      # arithmetic vega (paper: 2.6x)
+    assert mc[1]["within_var"][1] / av[1]["within_var"][1] >= 3.0      # lookback delta (paper: 7.5x)
