@@ -440,8 +440,17 @@ def main():
                 "note": f"FP64 pipe: {SM_COUNT} SMs x {FP64_LANES_PER_SM} FMA lanes x 2 x {sm_max:.0f} MHz "
                         f"(spec at sm_max_mhz; DESIGN.md 5); algorithmic work {per_path} FP64 lane-instr/path "
                         f"(SURVEY 8(d) model) x {launch_paths} paths per launch / kernel time (CUDA events)"}
+        try:  # the FP64 roof measured on this GPU now (context; the denominator stays the spec figure)
+            mb = q.qmccpw_fp64_roof(local)
+            roof["measured_roof"] = {k: mb[k] for k in ("dfma_tflops", "dmma_tflops", "sm_clock_mhz",
+                                                        "dfma_latency_cycles")}
+            roof["measured_roof"]["dfma_frac_of_spec_at_run_clock"] = mb["dfma_tflops"] / (
+                SM_COUNT * FP64_LANES_PER_SM * 2 * mb["sm_clock_mhz"] * 1e6 / 1e12)
+        except Exception as e:  # noqa: BLE001 -- context only
+            roof["measured_roof"] = {"error": str(e)}
         if ncu:
-            roof["ncu"] = {k: ncu[k] for k in ("fp64_pipe_pct", "issue_active_pct", "xu_pipe_pct", "warps_active",
+            roof["ncu"] = {k: ncu[k] for k in ("fp64_pipe_pct", "dmma_pipe_pct", "fp64_plus_dmma_pct",
+                                               "issue_active_pct", "xu_pipe_pct", "warps_active",
                                                "registers", "build", "source") if k in ncu}
         line = {
             "metric": metric, "value": value, "unit": unit, "n_gpus": world, "steps": args.steps,

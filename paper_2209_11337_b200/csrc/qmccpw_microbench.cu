@@ -12,19 +12,26 @@
 
 namespace qmccpw {
 
+// ILP independent chains per thread, the iteration loop unrolled 4x so that loop overhead is
+// ~1 instruction per 32 DFMAs; block 0 / thread 0 records clock64() at both ends, so the
+// caller gets the SM clock the run actually saw (cycles / event time) and the per-clock rate
 template <int ILP>
-__global__ void dfma_throughput_kernel(double* out, int iters, double a, double b) {
+__global__ void dfma_throughput_kernel(double* out, int iters, double a, double b, long long* cycles) {
     double x[ILP];
 #pragma unroll
     for (int i = 0; i < ILP; ++i) x[i] = (double)(threadIdx.x + i) * 1e-3;
+    const long long t0 = clock64();
+#pragma unroll 4
     for (int it = 0; it < iters; ++it) {
 #pragma unroll
         for (int i = 0; i < ILP; ++i) x[i] = fma(x[i], a, b);
     }
+    const long long t1 = clock64();
     double s = 0.0;
 #pragma unroll
     for (int i = 0; i < ILP; ++i) s += x[i];
     if (s == 12345.678) out[blockIdx.x] = s;  // keep the chains alive
+    if (blockIdx.x == 0 && threadIdx.x == 0 && cycles) *cycles = t1 - t0;
 }
 
 __global__ void dfma_latency_kernel(double* out, int iters, double a, double b, long long* cycles) {
@@ -76,15 +83,19 @@ extern "C" int qmccpw_fp64_roof(int32_t device, double* dfma_tflops, double* dfm
     cudaEventCreate(&e0);
     cudaEventCreate(&e1);
     float ms = 0.f;
-    // DFMA: 8 independent chains per thread, 8 blocks x 256 threads per SM
-    const int iters = 4096, blocks = sms * 8, tpb = 256;
-    dfma_throughput_kernel<8><<<blocks, tpb>>>(d_out, 16, 0.999999, 1e-7);  // warm-up
+    // DFMA: 8 independent chains per thread, 4 blocks x 256 threads per SM (32 warps), long
+    // enough (~0.2 s) that launch and tail effects are < 0.1 %
+    const int iters = 1 << 16, blocks = sms * 4, tpb = 256;
+    dfma_throughput_kernel<8><<<blocks, tpb>>>(d_out, 1024, 0.999999, 1e-7, nullptr);  // warm-up
     cudaEventRecord(e0);
-    dfma_throughput_kernel<8><<<blocks, tpb>>>(d_out, iters, 0.999999, 1e-7);
+    dfma_throughput_kernel<8><<<blocks, tpb>>>(d_out, iters, 0.999999, 1e-7, d_cyc);
     cudaEventRecord(e1);
     cudaEventSynchronize(e1);
     cudaEventElapsedTime(&ms, e0, e1);
     *dfma_tflops = 2.0 * 8.0 * iters * (double)blocks * tpb / (ms * 1e-3) / 1e12;
+    long long run_cyc = 0;
+    cudaMemcpy(&run_cyc, d_cyc, sizeof run_cyc, cudaMemcpyDeviceToHost);
+    *sm_clock_mhz = (double)run_cyc / (ms * 1e-3) / 1e6;  // block 0's span ~ the whole run (one wave)
     launch_counter() += 2;
     // latency: one warp, one dependent chain
     dfma_latency_kernel<<<1, 32>>>(d_out, 4096, 0.999999, 1e-7, d_cyc);
@@ -103,9 +114,6 @@ extern "C" int qmccpw_fp64_roof(int32_t device, double* dfma_tflops, double* dfm
     cudaEventElapsedTime(&ms, e0, e1);
     *dmma_tflops = 512.0 * 4.0 * diters * (double)dblocks * (dtpb / 32) / (ms * 1e-3) / 1e12;
     launch_counter() += 2;
-    int clk_khz = 0;
-    cudaDeviceGetAttribute(&clk_khz, cudaDevAttrClockRate, device);
-    *sm_clock_mhz = clk_khz / 1000.0;
     cudaEventDestroy(e0);
     cudaEventDestroy(e1);
     cudaFree(d_out);

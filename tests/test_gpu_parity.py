@@ -200,11 +200,17 @@ def test_path_values_d256_and_other_markets(q, O, constr, cond):
 
 
 # ------------------------------------------------------------------ (a8) full runs
-def _means_check(gres, ores, floor=0.0):
-    """floor: the output's natural scale (|ATM Black-Scholes value|) where the mean itself can be ~0."""
-    for gr, orr in zip(gres, ores):
+def _means_check(gres, ores, floor=0.0, piv=None):
+    """|dC| <= 1e-9 max(|C|, mean|f|).  floor: the output's natural scale (|ATM
+    Black-Scholes value|, portfolio only).  piv: the pivots p (8(a8)); both sides form
+    C = p + S1/N from S1 = sum (f - p), summed in different orders, so C carries an absolute
+    rounding ~ log2(N) eps |p| that no algorithm on either side can remove when |C| << |p|
+    (deep in-the-money lookback gammas under X1: C ~ 1e-9, p ~ 1e-2; reading 30):
+    1e-14 |p| is added to the bound."""
+    for i, (gr, orr) in enumerate(zip(gres, ores)):
         g = gr.as_dict() if hasattr(gr, "as_dict") else gr
-        scale = np.maximum(np.abs(orr["mean"]), orr["mean_abs"]) + floor
+        pfloor = 1e-14 * np.abs(piv[i]) if piv is not None else 0.0
+        scale = np.maximum(np.abs(orr["mean"]), orr["mean_abs"]) + floor + pfloor * 1e9
         assert np.all(np.abs(g["mean"] - orr["mean"]) <= 1e-9 * scale), (g["mean"], orr["mean"])
         if orr["n_replicates"] > 1:
             assert np.all(np.abs(g["se"] - orr["se"]) <= 1e-6 * orr["se"] + 1e-12 * scale), (g["se"], orr["se"])
@@ -250,6 +256,18 @@ def test_c4_fused_three_options_and_lr(q, O):
     g = q.qmccpw_price_greeks_batch([0, 1, 2], [q.params(K=95.0, d=64)] * 3, N, L, qcfg(q, 2, 1))
     o, _ = O.price_greeks([(0, 95.0), (1, 95.0), (2, 95.0)], O.market(d=64), N, L, ocfg(O, 2, 1))
     _means_check(g, o)
+
+
+@pytest.mark.parametrize("constr", [1, 2])
+def test_x1_deep_in_the_money_means(q, O, constr):
+    # X1 at K = 90, all three options: the lookback gamma's mean (~1e-9) sits ~1e7 below its
+    # pivot (the d = 1 Black-Scholes gamma ~1e-2), so the pivot-centred sums carry an absolute
+    # rounding ~eps |p| (reading 30) -- the bound adds 1e-14 |p|
+    N, L, K = 2 * 4096 + 77, 4, 90.0
+    g = q.qmccpw_price_greeks_batch([0, 1, 2], [q.params(K=K, d=64)] * 3, N, L, qcfg(q, constr, 1))
+    o, _ = O.price_greeks([(t, K) for t in (0, 1, 2)], O.market(d=64), N, L, ocfg(O, constr, 1))
+    piv = [O.pivots(t, K, O.market(d=64)) for t in (0, 1, 2)]
+    _means_check(g, o, piv=piv)
 
 
 def test_edge_cases(q, O):
