@@ -35,7 +35,8 @@ def build(force=False, verbose=False, defines=(), out=None):
     if out is None and not force and not stale():
         return LIB
     target = out or LIB
-    objdir = os.path.join(PKG, "build", os.path.basename(target) + ".o.d")
+    # object files outside the repo: they are large and must not travel to the GPU box
+    objdir = os.path.join(os.environ.get("QMCCPW_OBJDIR", "/tmp/qmccpw_obj"), os.path.basename(target) + ".o.d")
     os.makedirs(objdir, exist_ok=True)
     procs = []
     for src in SOURCES:
@@ -61,6 +62,18 @@ def build(force=False, verbose=False, defines=(), out=None):
     if verbose:
         print("\n".join(logs))
     return target
+
+
+CHECKED_LIB = os.path.join(PKG, "libqmccpw_checked.so")
+
+
+def build_checked(force=False):
+    """The QMCCPW_CHECKED variant (device-side bounds asserts, tests/test_memory_safety.py),
+    built next to the production library; rebuilt when a source is newer."""
+    if not force and os.path.exists(CHECKED_LIB) and all(
+            os.path.getmtime(f) <= os.path.getmtime(CHECKED_LIB) for f in SOURCES + HEADERS):
+        return CHECKED_LIB
+    return build(defines=("QMCCPW_CHECKED=1",), out=CHECKED_LIB)
 
 
 if __name__ == "__main__":

@@ -10,6 +10,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <mutex>
@@ -122,6 +123,15 @@ int acquire_scratch(int device, cudaStream_t st, size_t bytes, size_t pinned, St
         if (cudaMallocHost(&e.h_pinned, pinned) != cudaSuccess) return fail(QMCCPW_ENOMEM, "pinned allocation failed");
         e.pinned_bytes = pinned;
     }
+    // QMCCPW_POISON=1 (tests/test_memory_safety.py, an initcheck substitute): fill the scratch with
+    // 0xFF bytes -- NaN as doubles, 0xFFFFFFFF as table words -- on every call, so a kernel that
+    // read a table entry, partial or replicate sum before writing it would change the results
+    static const bool poison = [] {
+        const char* v = std::getenv("QMCCPW_POISON");
+        return v != nullptr && v[0] == '1';
+    }();
+    if (poison && cudaMemsetAsync(e.scratch, 0xFF, e.scratch_bytes, st) != cudaSuccess)
+        return fail(QMCCPW_ECUDA, "poison memset failed");
     *out = &e;
     return QMCCPW_OK;
 }

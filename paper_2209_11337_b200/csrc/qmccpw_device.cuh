@@ -57,6 +57,9 @@ struct SobolBlock {
     int lane_t, w_t, f_t;
     const uint32_t* os = nullptr;  // Owen seeds [d] (smem) or nullptr (LMS / shift / plain: folded into HW)
     __device__ __forceinline__ uint32_t get(int j) const {
+        QMCCPW_CHECK(j >= 0 && j < d && f_t >= 0 && f_t < 2 && w_t >= 0 && w_t < nw && lane_t >= 0 && lane_t < 32);
+        QMCCPW_CHK_SMEM(&HW[(f_t * nw + w_t) * d + j]);
+        QMCCPW_CHK_SMEM(&G[j * 32 + lane_t]);
         const uint32_t y = HW[(f_t * nw + w_t) * d + j] ^ G[j * 32 + lane_t];
         return os != nullptr ? owen_scramble(y, os[j]) : y;
     }
@@ -70,6 +73,7 @@ __device__ __forceinline__ void sobol_build_g(const uint32_t* vt, int d, uint32_
 #pragma unroll
         for (int b = 0; b < 5; ++b)
             if ((g >> b) & 1) y ^= vt[j * 32 + b];
+        QMCCPW_CHK_SMEM(&G[idx]);
         G[idx] = y;
     }
 }
@@ -106,11 +110,14 @@ __device__ __forceinline__ void sobol_build_hw_inc(const uint32_t* vt, const uin
             b0 = BS[j];
         }
         const uint32_t b1 = b0 ^ sobol_base_step(v, p, A + 1);
+        QMCCPW_CHK_SMEM(&BS[j]);
+        QMCCPW_CHK_SMEM(&v[31]);
         BS[j] = b1;
         const uint32_t v4 = v[4], v5 = v[5], v6 = v[6];
         for (int w = 0; w < nw; ++w) {
             const int gw = w ^ (w >> 1);
             const uint32_t wp = ((w & 1) ? v4 : 0u) ^ ((gw & 1) ? v5 : 0u) ^ ((gw & 2) ? v6 : 0u);
+            QMCCPW_CHK_SMEM(&HW[(nw + w) * d + j]);
             HW[w * d + j] = b0 ^ wp;
             HW[(nw + w) * d + j] = b1 ^ wp;
         }
@@ -206,7 +213,11 @@ struct NormalFifo {
     template <class DimAt>
     __device__ __forceinline__ double next(const SobolBlock& sob, DimAt dim_at) {
         if (have == 0) {
-            normal_from_u32_x2(sob.get(dim_at(0)), sob.get(dim_at(1)), x0, x1);
+            // the partner of the last normal of an odd count (BB-X1: d - 1 normals; d = 1) would be
+            // table row d, past the [d] rows: clamp it (its value is never consumed).  Found by the
+            // QMCCPW_CHECKED build (tests/test_memory_safety.py)
+            const int j1 = dim_at(1);
+            normal_from_u32_x2(sob.get(dim_at(0)), sob.get(j1 < sob.d ? j1 : sob.d - 1), x0, x1);
             have = 2;
         }
         const double r = (have == 2) ? x0 : x1;
@@ -477,6 +488,7 @@ __device__ __forceinline__ void x1_lookback(const PathArgs& P, int o, const doub
                     cS = cb[l * stride];
                 }
             }
+            QMCCPW_CHECK(top < kMaxDimGpu);
             hull[top++] = (uint8_t)j;
             bS = bT;
             cS = cT;
@@ -621,6 +633,7 @@ __device__ __forceinline__ void warp_slot_sums(const double (&f)[kMaxOpt][4], co
         }
         v[0] += __shfl_xor_sync(0xffffffffu, v[0], 2);
         v[0] += __shfl_xor_sync(0xffffffffu, v[0], 1);
+        QMCCPW_CHECK(o * 8 + (lane >> 2) < 32);
         if ((lane & 3) == 0) wacc[o * 8 + (lane >> 2)] += v[0];
     }
 }
@@ -638,6 +651,7 @@ __device__ __forceinline__ void thread_acc2(const double (&f)[kMaxOpt][4], const
         for (int q = 0; q < 4; ++q) {
             const double y = f[o][q] - P.piv[o][q];
             double2* a = acc2 + (size_t)(o * 4 + q) * tpb + tid;
+            QMCCPW_CHK_SMEM(a);
             double2 t = *a;
             t.x += y;
             t.y = fma(y, y, t.y);
@@ -665,6 +679,7 @@ __device__ __forceinline__ void block_epilogue(const PathArgs& P, const double* 
     const int n_out = P.partial_stride;
     __syncthreads();  // red aliases the Sobol' tables
     if (accs == nullptr) {  // per-warp sums (warp_slot_sums)
+        QMCCPW_CHECK(n_acc + 3 <= 32 && warp < 4);
         if (lane < n_acc) red[warp * 32 + lane] = wacc[warp * 32 + lane];
     } else {
         for (int v = 0; v < n_acc; ++v) {
@@ -682,6 +697,7 @@ __device__ __forceinline__ void block_epilogue(const PathArgs& P, const double* 
         nc += __shfl_xor_sync(0xffffffffu, nc, off);
     }
     if (lane == 0) {
+        QMCCPW_CHK_SMEM(&red[warp * 32 + P.n_opt * 8 + 2]);
         red[warp * 32 + P.n_opt * 8 + 0] = (double)uc;
         red[warp * 32 + P.n_opt * 8 + 1] = (double)tc;
         red[warp * 32 + P.n_opt * 8 + 2] = (double)nc;  // points this cell evaluated (completeness check)
@@ -690,6 +706,7 @@ __device__ __forceinline__ void block_epilogue(const PathArgs& P, const double* 
     if (tid < n_out) {
         double s = 0.0;
         for (int w = 0; w < nwarps; ++w) s += red[w * 32 + tid];
+        QMCCPW_CHECK(cell >= P.cell_begin && cell < P.cell_end);
         P.partials[(size_t)cell * n_out + tid] = s;
     }
 }

@@ -15,6 +15,37 @@ constexpr int kNewtonMax = 8;
 // the error it leaves is ~C |du|^3 << 1e-16, so that update is the last (predictive stop)
 constexpr double kHalleyTol = 1e-6;
 
+// ---- QMCCPW_CHECKED builds (scripts/checked_build.py -> libqmccpw_checked.so): device-side
+// bounds asserts at the computed shared- and global-memory indices of the hot path, a memcheck
+// substitute (compute-sanitizer is closed on the GPU pool).  A failed check executes __trap(),
+// so the launch fails with cudaErrorLaunchFailure and the call returns QMCCPW_ECUDA.  In the
+// production build the macros expand to nothing.
+#ifndef QMCCPW_CHECKED
+#define QMCCPW_CHECKED 0
+#endif
+#if QMCCPW_CHECKED && defined(__CUDA_ARCH__)
+// [p, p + n) must lie inside the block's dynamic shared memory window
+__device__ __forceinline__ void qmccpw_chk_dsmem(const void* p, size_t n) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    uint32_t dyn;
+    asm volatile("mov.u32 %0, %%dynamic_smem_size;" : "=r"(dyn));
+    const unsigned char* c = static_cast<const unsigned char*>(p);
+    if (c < smem_raw || c + n > smem_raw + dyn) __trap();
+}
+#define QMCCPW_CHECK(cond) \
+    do {                   \
+        if (!(cond)) __trap(); \
+    } while (0)
+#define QMCCPW_CHK_SMEM(ptr) qmccpw_chk_dsmem((ptr), sizeof(*(ptr)))
+#else
+#define QMCCPW_CHECK(cond) \
+    do {                   \
+    } while (0)
+#define QMCCPW_CHK_SMEM(ptr) \
+    do {                     \
+    } while (0)
+#endif
+
 enum Construction { kStd = 0, kBB = 1, kPca = 2 };
 enum Conditioning { kW1 = 0, kX1 = 1 };
 enum Method { kQmc = 0, kLr = 1, kMc = 2, kMcAv = 3 };

@@ -277,6 +277,40 @@ __device__ __forceinline__ void normal_from_u32_x2(uint32_t ya, uint32_t yb, dou
     xb = upb ? -rb : rb;
 }
 
+// four lattice points -> four standard normals (same arithmetic as normal_from_u32): four
+// interleaved Horner chains, so each coefficient loaded into a uniform register feeds four
+// DFMAs (half the constant-load instructions per normal of the paired form)
+__device__ __forceinline__ void normal_from_u32_x4(const uint32_t (&y)[4], double (&x)[4]) {
+    bool up[4];
+    double u[4], z[4], t[4], w[4], v[4], p[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        up[i] = (y[i] >> 31) != 0u;
+        const uint32_t l = up[i] ? ~y[i] : y[i];
+        u[i] = fma((double)l, MC.p32, MC.p33);
+        z[i] = fma(MC.two, u[i], -MC.one);
+        t[i] = (MC.four * u[i]) * (MC.one - u[i]);
+    }
+    fast_log_x2(t[0], t[1], w[0], w[1]);
+    fast_log_x2(t[2], t[3], w[2], w[3]);
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        w[i] = -w[i];
+        v[i] = w[i] - ICDF_CENTRAL_CENTER;
+        p[i] = ICDF_C[kIcdfDeg];
+    }
+#pragma unroll
+    for (int j = kIcdfDeg - 1; j >= 0; --j)
+#pragma unroll
+        for (int i = 0; i < 4; ++i) p[i] = fma(p[i], v[i], ICDF_C[j]);
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        if (w[i] >= MC.w_split) p[i] = icdf_tail_poly(w[i]);  // u < 4.8e-4: rare, divergent
+        const double r = z[i] * p[i];
+        x[i] = up[i] ? -r : r;
+    }
+}
+
 __device__ __forceinline__ double normal_pdf(double x) {
     const double a = MC.minus_half * x * x;
     return a > MC.pdf_floor ? MC.inv_sqrt_2pi * fast_exp(a) : 0.0;

@@ -18,6 +18,11 @@ namespace qmccpw {
 // (8: 64 regs, a few spills to L1); STD-W1 33.1 (4) / 31.9 (5) / 31.2 (6); v11: 27.20 (6) / 27.03 (7) / 27.4 (8)
 // MC+AV-CPW with the bridge: 140 registers uncapped at v18 (3 blocks/SM; 46.2 -> 51.5 ms
 // against v17), so it is capped at 4 blocks
+// BB-W1 (QMC) at d >= 8: the eight-dates-per-group bridge (static expression tree for the last
+// seven normals of each group, four-way normals); 0: the pairwise bridge with the normal FIFO
+#ifndef QMCCPW_BB_GROUPED
+#define QMCCPW_BB_GROUPED 1
+#endif
 #ifndef QMCCPW_BBAV_MINB
 #define QMCCPW_BBAV_MINB 4
 #endif
@@ -79,9 +84,16 @@ __global__ void __launch_bounds__(128, paths_min_blocks<CONSTR, COND, METHOD>())
     if (METHOD != kQmc) __syncthreads();  // QMC: the barrier below publishes the tables
     if (METHOD == kQmc) {
         const uint32_t* src = P.vscr + (size_t)rep_local * d * 32;
-        for (int idx = tid; idx < d * 32; idx += tpb)
+        QMCCPW_CHECK(rep_local < P.n_reps && cell < P.cell_end);
+        for (int idx = tid; idx < d * 32; idx += tpb) {
+            QMCCPW_CHK_SMEM(&vt[idx]);
+            QMCCPW_CHECK(!kPerm || P.bb_seq[idx >> 5] < d);
             vt[idx] = src[kPerm ? (int)P.bb_seq[idx >> 5] * 32 + (idx & 31) : idx];
-        for (int idx = tid; idx < d; idx += tpb) sh[idx] = P.shift[(size_t)rep_local * d + (kPerm ? P.bb_seq[idx] : idx)];
+        }
+        for (int idx = tid; idx < d; idx += tpb) {
+            QMCCPW_CHK_SMEM(&sh[idx]);
+            sh[idx] = P.shift[(size_t)rep_local * d + (kPerm ? P.bb_seq[idx] : idx)];
+        }
         __syncthreads();
         sobol_build_g(vt, d, G, tid, tpb);
     }
@@ -230,6 +242,62 @@ __global__ void __launch_bounds__(128, paths_min_blocks<CONSTR, COND, METHOD>())
                     Wt = fma(P.sqrt_t1, normal_from_u32(sob.get(j)), Wt);
                     w1.push(P, j, Wt);
                 }
+            } else if (CONSTR == kBB && QMCCPW_BB_GROUPED && d >= 8) {
+                // Alg. 4 in time order, eight dates per group g (pairs 4g..4g+3 of the
+                // pairwise form below).  Pair 4g descends e0 = 3 + ctz(g) levels (e0 = m at
+                // g = 0); pairs 4g+1, 4g+2, 4g+3 descend 1, 2, 1.  So only levels c >= 3 of the
+                // first descent are data-dependent: they go through the stack (pushed for c > 3;
+                // the c = 3 midpoint is the group's right end R = W(8g+8), or R is popped when
+                // e0 = 3), and the last seven normals of the group -- levels 2, 1, 0 of pair 4g,
+                // then 1, 2, 1 normals -- are consecutive in Alg. 4's order and feed a fixed
+                // expression tree with no stack traffic, no FIFO and no branches.  Every W is
+                // the same fma / 0.5 (l + r) expression as in the pairwise form (same bits).
+                const int m = P.bb_m;
+                const double b0 = P.bb_b[m], b1 = P.bb_b[m - 1], b2 = P.bb_b[m - 2];
+                double stW[12];
+                int sp = 0;
+                int pos = 0;
+                stW[0] = P.sqrtT * normal_from_u32(sob.get(pos++));  // terminal: W(T) = sqrt(T) x_0
+                double Wl = 0.0, W1 = 0.0;
+#pragma unroll 1
+                for (int g = 0; g < (d >> 3); ++g) {
+                    const int e0 = (g == 0) ? m : 2 + __ffs(g);
+                    double R;
+                    if (e0 == 3) {
+                        R = stW[sp];
+                        --sp;
+                    } else {
+                        double Wr = stW[sp];
+#pragma unroll 1
+                        for (int c = e0 - 1; c >= 3; --c) {
+                            const double Wm = fma(P.bb_b[m - c], normal_from_u32(sob.get(pos++)), 0.5 * (Wl + Wr));
+                            if (c > 3) stW[++sp] = Wm;
+                            Wr = Wm;
+                        }
+                        R = Wr;
+                    }
+                    QMCCPW_CHECK(sp >= -1 && sp < 12 && pos + 7 <= d);
+                    uint32_t y4[4] = {sob.get(pos), sob.get(pos + 1), sob.get(pos + 2), sob.get(pos + 3)};
+                    double x[7];
+                    double x4[4];
+                    normal_from_u32_x4(y4, x4);
+                    normal_from_u32_x2(sob.get(pos + 4), sob.get(pos + 5), x[4], x[5]);
+                    x[6] = normal_from_u32(sob.get(pos + 6));
+                    pos += 7;
+                    const double M4 = fma(b2, x4[0], 0.5 * (Wl + R));   // W(8g+4)
+                    const double M2 = fma(b1, x4[1], 0.5 * (Wl + M4));  // W(8g+2)
+                    const double Wa = fma(b0, x4[2], 0.5 * (Wl + M2));  // W(8g+1)
+                    if (g == 0) W1 = Wa;
+                    const double W3 = fma(b0, x4[3], 0.5 * (M2 + M4));
+                    const double W6 = fma(b1, x[4], 0.5 * (M4 + R));
+                    const double W5 = fma(b0, x[5], 0.5 * (M4 + W6));
+                    const double W7 = fma(b0, x[6], 0.5 * (W6 + R));
+                    w1.push2(P, 8 * g, Wa - W1, M2 - W1);
+                    w1.push2(P, 8 * g + 2, W3 - W1, M4 - W1);
+                    w1.push2(P, 8 * g + 4, W5 - W1, W6 - W1);
+                    w1.push2(P, 8 * g + 6, W7 - W1, R - W1);
+                    Wl = R;
+                }
             } else if (CONSTR == kBB) {
                 // Alg. 4 generated in time order, two dates per step.  At odd
                 // j = 2p+1 the bridge descends e = 1 + ctz(p) levels (e = m at p = 0) from the
@@ -284,6 +352,7 @@ __global__ void __launch_bounds__(128, paths_min_blocks<CONSTR, COND, METHOD>())
                             --sp;
                         }
                         if (pp == 0) W1 = Wodd;
+                        QMCCPW_CHECK(sp >= -1 && sp < 12 && pos <= d + 2);
                         w1.push2(P, 2 * pp, Wodd - W1, Weven - W1);
                         Wl = Weven;
                     }
@@ -306,6 +375,7 @@ __global__ void __launch_bounds__(128, paths_min_blocks<CONSTR, COND, METHOD>())
                 for (; kk + 1 < d; kk += 2) {
                     double xa, xc2;
                     normal_from_u32_x2(sob.get(kk), sob.get(kk + 1), xa, xc2);
+                    QMCCPW_CHK_SMEM(&xc[(kk + 1) * XS]);
                     xc[kk * XS] = xa;
                     xc[(kk + 1) * XS] = xc2;
                 }
@@ -427,6 +497,7 @@ __global__ void __launch_bounds__(128, paths_min_blocks<CONSTR, COND, METHOD>())
                     double xa, xb2;
                     normal_from_u32_x2(sob.get(j), sob.get(j + 1), xa, xb2);
                     R = fma(P.sqrt_t1, xa, R);
+                    QMCCPW_CHK_SMEM(&cb[(j + 1) * tpb]);
                     cb[j * tpb] = P.lnS0 + P.omega * (double)(j + 1) * P.t1 + P.sigma * R;
                     R = fma(P.sqrt_t1, xb2, R);
                     cb[(j + 1) * tpb] = P.lnS0 + P.omega * (double)(j + 2) * P.t1 + P.sigma * R;
@@ -467,6 +538,8 @@ __global__ void __launch_bounds__(128, paths_min_blocks<CONSTR, COND, METHOD>())
                         }
                         Rj = Wr;
                     }
+                    QMCCPW_CHK_SMEM(&cb[(j - 1) * tpb]);
+                    QMCCPW_CHECK(sp >= -1 && sp < 12 && pos <= d + 1);  // the last date pops the bottom
                     cb[(j - 1) * tpb] = P.lnS0 + P.omega * (double)j * P.t1 + P.sigma * Rj;
                     Wl = Rj;
                 }
@@ -478,6 +551,7 @@ __global__ void __launch_bounds__(128, paths_min_blocks<CONSTR, COND, METHOD>())
                 for (; kk + 1 < d; kk += 2) {
                     double xa, xc;
                     normal_from_u32_x2(sob.get(kk), sob.get(kk + 1), xa, xc);
+                    QMCCPW_CHK_SMEM(&xb[(kk + 1) * tpb]);
                     xb[kk * tpb] = xa;
                     xb[(kk + 1) * tpb] = xc;
                 }
@@ -488,6 +562,7 @@ __global__ void __launch_bounds__(128, paths_min_blocks<CONSTR, COND, METHOD>())
                     double Ra = 0.0;
 #pragma unroll 4
                     for (int q2 = 1; q2 < d; ++q2) Ra = fma(__ldg(Ma + q2), xb[q2 * tpb], Ra);
+                    QMCCPW_CHK_SMEM(&cb[j * tpb]);
                     cb[j * tpb] = P.lnS0 + P.omega * (double)(j + 1) * P.t1 + P.sigma * Ra;
                 }
             } else {
@@ -529,6 +604,7 @@ __global__ void __launch_bounds__(128, paths_min_blocks<CONSTR, COND, METHOD>())
 #pragma unroll
                     for (int rt = 0; rt < 4; ++rt) {
                         double* col = buf1 + wbase + 8 * rt + q;
+                        if (j0 < d) QMCCPW_CHK_SMEM(&col[(size_t)j0 * tpb]);
                         if (j0 < d) col[(size_t)j0 * tpb] = P.lnS0 + P.omega * (double)(j0 + 1) * P.t1 + P.sigma * acc[rt][0];
                         if (j0 + 1 < d)
                             col[(size_t)(j0 + 1) * tpb] = P.lnS0 + P.omega * (double)(j0 + 2) * P.t1 + P.sigma * acc[rt][1];
@@ -548,7 +624,11 @@ __global__ void __launch_bounds__(128, paths_min_blocks<CONSTR, COND, METHOD>())
 #pragma unroll
             for (int o = 0; o < kMaxOpt; ++o)
                 if (o == P.hook_option)
-                    for (int q = 0; q < 4; ++q) P.path_out[i * 4 + q] = f[o][q];
+#pragma unroll
+                    for (int q = 0; q < 4; ++q) {
+                        QMCCPW_CHECK(i < P.n_points);
+                        P.path_out[i * 4 + q] = f[o][q];
+                    }
         }
         warp_slot_sums(f, P, valid, lane, wacc + (tid >> 5) * 32);
         (void)k;

@@ -23,6 +23,12 @@ namespace qmccpw {
 #ifndef QMCCPW_PCA_W1_MINB
 #define QMCCPW_PCA_W1_MINB 4
 #endif
+// W1: per-warp reduce-scatter of the centred sums (warp_slot_sums, no per-thread smem
+// accumulators: 24.6 KB less shared memory per block at 3 options) instead of the per-thread
+// (S1, S2) pairs; lets more blocks fit when the register cap allows them
+#ifndef QMCCPW_PCA_WARPSUM
+#define QMCCPW_PCA_WARPSUM 0
+#endif
 #ifndef QMCCPW_PCA_X1_MINB
 #define QMCCPW_PCA_X1_MINB 5
 #endif
@@ -57,10 +63,12 @@ __global__ void __launch_bounds__(128, pca_min_blocks<COND, KF, LB>()) pca_kerne
     const int ppt = kCellPoints >> tpb_log2;
     const int nw = tpb >> 5;
     const int n_acc = P.n_opt * 8;
+    constexpr bool kWarpSum = COND == kW1 && QMCCPW_PCA_WARPSUM;
+    const int n_acc_smem = kWarpSum ? 0 : n_acc;  // smem accumulator rows
     // per-path accumulators in smem: X1 as scalars (one quad lane per path), W1 as (S1, S2) pairs
     double* accs = reinterpret_cast<double*>(smem_raw);
     double2* acc2 = reinterpret_cast<double2*>(smem_raw);
-    uint32_t* vt = reinterpret_cast<uint32_t*>(accs + (size_t)n_acc * tpb);
+    uint32_t* vt = reinterpret_cast<uint32_t*>(accs + (size_t)n_acc_smem * tpb);
     uint32_t* sh = vt + (size_t)d * 32;
     uint32_t* G = sh + d;
     uint32_t* HW = G + (size_t)d * 32;
@@ -70,19 +78,29 @@ __global__ void __launch_bounds__(128, pca_min_blocks<COND, KF, LB>()) pca_kerne
     uint32_t* BS = HW + 2 * hw_size;  // [d] incremental Gray bases (sobol_build_hw_inc)
     // X1 with a lookback: c_j of the warp's 32 paths staged [d][32] per warp, so that each lane
     // walks the upper envelope of its own path (the quad layout holds a path over 4 lanes)
-    double* stage = reinterpret_cast<double*>(smem_raw + pca_stage_offset(n_acc, d, tpb)) +
+    double* stage = reinterpret_cast<double*>(smem_raw + pca_stage_offset(n_acc_smem, d, tpb)) +
                     (size_t)(tid >> 5) * d * 32;
     const uint64_t K0 = P.point_offset + i0;
     const uint64_t Ab = K0 >> tpb_log2;
     {
         math_tables_load(tid, tpb);
         const uint32_t* src = P.vscr + (size_t)rep_local * d * 32;
-        for (int idx = tid; idx < d * 32; idx += tpb) vt[idx] = src[idx];
-        for (int idx = tid; idx < d; idx += tpb) sh[idx] = P.shift[(size_t)rep_local * d + idx];
+        QMCCPW_CHECK(rep_local < P.n_reps && cell < P.cell_end);
+        for (int idx = tid; idx < d * 32; idx += tpb) {
+            QMCCPW_CHK_SMEM(&vt[idx]);
+            vt[idx] = src[idx];
+        }
+        for (int idx = tid; idx < d; idx += tpb) {
+            QMCCPW_CHK_SMEM(&sh[idx]);
+            sh[idx] = P.shift[(size_t)rep_local * d + idx];
+        }
         __syncthreads();
         sobol_build_g(vt, d, G, tid, tpb);
     }
-    for (int v = 0; v < n_acc; ++v) accs[v * tpb + tid] = 0.0;
+    for (int v = 0; v < n_acc_smem; ++v) {
+        QMCCPW_CHK_SMEM(&accs[v * tpb + tid]);
+        accs[v * tpb + tid] = 0.0;
+    }
     __shared__ double wacc[4 * 32];  // per-warp centred sums (tpb <= 128)
     wacc[tid] = 0.0;
     __syncwarp();
@@ -203,6 +221,7 @@ __global__ void __launch_bounds__(128, pca_min_blocks<COND, KF, LB>()) pca_kerne
 #pragma unroll
                     for (int jt = 0; jt < JT; ++jt) {
                         const int j0 = 8 * jt + 2 * r4;
+                        if (j0 < d) QMCCPW_CHK_SMEM(&sw[j0 * 32]);
                         if (j0 < d) sw[j0 * 32] = cv[2 * jt];
                         if (j0 + 1 < d) sw[(j0 + 1) * 32] = cv[2 * jt + 1];
                     }
@@ -314,6 +333,7 @@ __global__ void __launch_bounds__(128, pca_min_blocks<COND, KF, LB>()) pca_kerne
                             for (int qq = 0; qq < 4; ++qq) {
                                 const double y = f[o][qq] - P.piv[o][qq];
                                 double* a1 = accs + (size_t)(o * 8 + qq * 2) * tpb + tp;
+                                QMCCPW_CHK_SMEM(&a1[tpb]);
                                 a1[0] += y;
                                 a1[tpb] = fma(y, y, a1[tpb]);
                             }
@@ -361,16 +381,18 @@ __global__ void __launch_bounds__(128, pca_min_blocks<COND, KF, LB>()) pca_kerne
                     if (o == P.hook_option)
                         for (int qq = 0; qq < 4; ++qq) P.path_out[i * 4 + qq] = f[o][qq];
             }
-            thread_acc2(f, P, valid, acc2, tpb, tid);
+            if (kWarpSum) warp_slot_sums(f, P, valid, lane, wacc + (tid >> 5) * 32);
+            else thread_acc2(f, P, valid, acc2, tpb, tid);
         }
     }
-    if (COND == kW1) acc2_to_wacc(P, acc2, wacc, tpb, tid);
+    if (COND == kW1 && !kWarpSum) acc2_to_wacc(P, acc2, wacc, tpb, tid);
     block_epilogue(P, COND == kX1 ? accs : nullptr, wacc, red, n_acc, tpb, tid, cell, unconverged, ties, npts);
 }
 
-static size_t pca_smem_bytes(const PathArgs& a, bool lb) {
+static size_t pca_smem_bytes(const PathArgs& a, bool lb, int cond) {
     const size_t tpb = (size_t)1 << a.tpb_log2;
-    size_t b = pca_stage_offset(a.n_opt * 8, a.d, (int)tpb);
+    const bool warpsum = cond == kW1 && QMCCPW_PCA_WARPSUM;
+    size_t b = pca_stage_offset(warpsum ? 0 : a.n_opt * 8, a.d, (int)tpb);
     if (lb) b += tpb * a.d * sizeof(double);  // [nw][d][32] staging
     return b;
 }
@@ -389,7 +411,7 @@ static cudaError_t launch_pca_t(const PathArgs& args_in, cudaStream_t st) {
     int best_lg = -1, best_warps = -1;
     for (int lg = 7; lg >= 5; --lg) {
         args.tpb_log2 = lg;
-        const size_t smem = pca_smem_bytes(args, LB);
+        const size_t smem = pca_smem_bytes(args, LB, K);
         if (smem > 200 * 1024) continue;
         int nb = 0;
         if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, pca_kernel<K, KF, OW, LB>, 1 << lg, smem) != cudaSuccess) continue;
@@ -402,7 +424,7 @@ static cudaError_t launch_pca_t(const PathArgs& args_in, cudaStream_t st) {
     args.tpb_log2 = best_lg;
     const uint64_t nblocks = args.cell_end - args.cell_begin;
     if (nblocks == 0) return cudaSuccess;
-    pca_kernel<K, KF, OW, LB><<<(unsigned)nblocks, 1 << best_lg, pca_smem_bytes(args, LB), st>>>(args);
+    pca_kernel<K, KF, OW, LB><<<(unsigned)nblocks, 1 << best_lg, pca_smem_bytes(args, LB, K), st>>>(args);
     ++launch_counter();
     return cudaGetLastError();
 }

@@ -50,8 +50,15 @@ __global__ void __launch_bounds__(128, 3) portfolio_kernel(const PortfolioArgs P
     {
         math_tables_load(tid, tpb);
         const uint32_t* src = P.vscr + (size_t)rep_local * d * 32;
-        for (int idx = tid; idx < d * 32; idx += tpb) vt[idx] = src[idx];
-        for (int idx = tid; idx < d; idx += tpb) sh[idx] = P.shift[(size_t)rep_local * d + idx];
+        QMCCPW_CHECK(rep_local < P.n_reps && cell < P.cell_end);
+        for (int idx = tid; idx < d * 32; idx += tpb) {
+            QMCCPW_CHK_SMEM(&vt[idx]);
+            vt[idx] = src[idx];
+        }
+        for (int idx = tid; idx < d; idx += tpb) {
+            QMCCPW_CHK_SMEM(&sh[idx]);
+            sh[idx] = P.shift[(size_t)rep_local * d + idx];
+        }
         for (int o = tid; o < nopt; o += tpb)  // zeroed by the thread that will own the option
 #pragma unroll
             for (int v = 0; v < 8; ++v) prow[o * 8 + v] = 0.0;
@@ -157,6 +164,7 @@ __global__ void __launch_bounds__(128, 3) portfolio_kernel(const PortfolioArgs P
                     double lnSA, lnSmax;
                     fast_log_x2(SA, Smax, lnSA, lnSmax);
                     double* st = stats + ((size_t)slot * nfam + fi) * kStatW;
+                    QMCCPW_CHK_SMEM(&st[7]);
                     st[0] = SA;
                     st[1] = lnSA;
                     st[2] = sI * inv_d;

@@ -217,7 +217,9 @@ def _means_check(gres, ores, floor=0.0, piv=None):
             assert np.all(np.abs(g["sigma_run"] - orr["sigma_run"]) <= 1e-6 * orr["sigma_run"] + 1e-12 * scale)
         else:
             assert np.all(np.isnan(g["se"]))
-        assert np.allclose(g["within_var"], orr["within_var"], rtol=1e-7, atol=1e-12 * scale ** 2)
+        # within_var = S2/N - (S1/N)^2 of pivot-centred sums: the same eps |p|^2 floor (reading 30)
+        pvar = 1e-13 * np.asarray(piv[i]) ** 2 if piv is not None else 0.0
+        assert np.allclose(g["within_var"], orr["within_var"], rtol=1e-7, atol=1e-12 * scale ** 2 + pvar)
         assert g["argmax_near_ties"] == orr["argmax_near_ties"]
 
 
