@@ -217,7 +217,7 @@ int qmccpw_path_values(int32_t option, const qmccpw_params* p, uint32_t replicat
 /* FP64 roof microbenchmarks on `device`: DFMA TFLOP/s at
  * full occupancy (independent chains), dependent-DFMA latency in SM cycles,
  * FP64 tensor-core (mma.sync m8n8k4, SASS DMMA) TFLOP/s, and the SM clock in
- * MHz measured during the DFMA run (clock64 cycles of block 0 / event time), so
+ * MHz measured during the DFMA run (clock64 cycles / %globaltimer ns of one block's span), so
  * that dfma_tflops / (2 x 148 x 64 x clock) is the per-clock fraction of the
  * FP64 pipe's peak.  Outputs are host pointers. */
 int qmccpw_fp64_roof(int32_t device, double* dfma_tflops, double* dfma_latency_cycles, double* dmma_tflops,

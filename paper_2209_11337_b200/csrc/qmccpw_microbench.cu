@@ -13,13 +13,15 @@
 namespace qmccpw {
 
 // ILP independent chains per thread, the iteration loop unrolled 4x so that loop overhead is
-// ~1 instruction per 32 DFMAs; block 0 / thread 0 records clock64() at both ends, so the
-// caller gets the SM clock the run actually saw (cycles / event time) and the per-clock rate
+// ~1 instruction per 32 DFMAs; block 0 / thread 0 records clock64() and %globaltimer at both
+// ends, so the caller gets the SM clock the run actually saw (cycles / ns of the same span)
 template <int ILP>
 __global__ void dfma_throughput_kernel(double* out, int iters, double a, double b, long long* cycles) {
     double x[ILP];
 #pragma unroll
     for (int i = 0; i < ILP; ++i) x[i] = (double)(threadIdx.x + i) * 1e-3;
+    long long g0;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g0));
     const long long t0 = clock64();
 #pragma unroll 4
     for (int it = 0; it < iters; ++it) {
@@ -27,11 +29,16 @@ __global__ void dfma_throughput_kernel(double* out, int iters, double a, double 
         for (int i = 0; i < ILP; ++i) x[i] = fma(x[i], a, b);
     }
     const long long t1 = clock64();
+    long long g1;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g1));
     double s = 0.0;
 #pragma unroll
     for (int i = 0; i < ILP; ++i) s += x[i];
     if (s == 12345.678) out[blockIdx.x] = s;  // keep the chains alive
-    if (blockIdx.x == 0 && threadIdx.x == 0 && cycles) *cycles = t1 - t0;
+    if (blockIdx.x == 0 && threadIdx.x == 0 && cycles) {
+        cycles[0] = t1 - t0;  // SM cycles and nanoseconds of the same span: the clock it ran at
+        cycles[1] = g1 - g0;
+    }
 }
 
 __global__ void dfma_latency_kernel(double* out, int iters, double a, double b, long long* cycles) {
@@ -78,7 +85,7 @@ extern "C" int qmccpw_fp64_roof(int32_t device, double* dfma_tflops, double* dfm
     double* d_out = nullptr;
     long long* d_cyc = nullptr;
     if (cudaMalloc(&d_out, 1 << 20) != cudaSuccess) return QMCCPW_ENOMEM;
-    cudaMalloc(&d_cyc, sizeof(long long));
+    cudaMalloc(&d_cyc, 2 * sizeof(long long));
     cudaEvent_t e0, e1;
     cudaEventCreate(&e0);
     cudaEventCreate(&e1);
@@ -93,9 +100,9 @@ extern "C" int qmccpw_fp64_roof(int32_t device, double* dfma_tflops, double* dfm
     cudaEventSynchronize(e1);
     cudaEventElapsedTime(&ms, e0, e1);
     *dfma_tflops = 2.0 * 8.0 * iters * (double)blocks * tpb / (ms * 1e-3) / 1e12;
-    long long run_cyc = 0;
-    cudaMemcpy(&run_cyc, d_cyc, sizeof run_cyc, cudaMemcpyDeviceToHost);
-    *sm_clock_mhz = (double)run_cyc / (ms * 1e-3) / 1e6;  // block 0's span ~ the whole run (one wave)
+    long long span[2] = {0, 1};
+    cudaMemcpy(span, d_cyc, sizeof span, cudaMemcpyDeviceToHost);
+    *sm_clock_mhz = span[1] > 0 ? (double)span[0] / (double)span[1] * 1e3 : 0.0;  // cycles per ns -> MHz
     launch_counter() += 2;
     // latency: one warp, one dependent chain
     dfma_latency_kernel<<<1, 32>>>(d_out, 4096, 0.999999, 1e-7, d_cyc);

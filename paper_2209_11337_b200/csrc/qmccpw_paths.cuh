@@ -19,7 +19,9 @@ namespace qmccpw {
 // MC+AV-CPW with the bridge: 140 registers uncapped at v18 (3 blocks/SM; 46.2 -> 51.5 ms
 // against v17), so it is capped at 4 blocks
 // BB-W1 (QMC) at d >= 8: the eight-dates-per-group bridge (static expression tree for the last
-// seven normals of each group, four-way normals); 0: the pairwise bridge with the normal FIFO
+// seven normals of each group, four-way normals); 0: the pairwise bridge with the normal FIFO.
+// A/B on one B200, C4 BB-W1 (ms/step): pairwise 27.94; grouped at 8 / 7 / 6 blocks/SM
+// 26.33 / 26.57 / 26.66
 #ifndef QMCCPW_BB_GROUPED
 #define QMCCPW_BB_GROUPED 1
 #endif

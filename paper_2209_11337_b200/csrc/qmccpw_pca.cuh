@@ -21,13 +21,15 @@ namespace qmccpw {
 //    quad-reduced, so the threshold is solved by the 4 lanes together.
 // ---------------------------------------------------------------------------
 #ifndef QMCCPW_PCA_W1_MINB
-#define QMCCPW_PCA_W1_MINB 4
+#define QMCCPW_PCA_W1_MINB 8
 #endif
 // W1: per-warp reduce-scatter of the centred sums (warp_slot_sums, no per-thread smem
 // accumulators: 24.6 KB less shared memory per block at 3 options) instead of the per-thread
-// (S1, S2) pairs; lets more blocks fit when the register cap allows them
+// (S1, S2) pairs, so more blocks fit.  A/B on one B200, C4 PCA-W1 (ms/step): per-thread pairs
+// at 4 blocks/SM 50.63; warp sums at 4 / 5 / 6 / 7 / 8 blocks/SM 50.50 / 47.34 / 46.87 / 46.63
+// / 46.54 (8: 64 registers, 344 B of spills to L1) -- profiles/r02/ab_*
 #ifndef QMCCPW_PCA_WARPSUM
-#define QMCCPW_PCA_WARPSUM 0
+#define QMCCPW_PCA_WARPSUM 1
 #endif
 #ifndef QMCCPW_PCA_X1_MINB
 #define QMCCPW_PCA_X1_MINB 5
