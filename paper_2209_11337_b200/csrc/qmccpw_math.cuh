@@ -244,6 +244,34 @@ __device__ __forceinline__ void fast_exp_x2(double xa, double xb, double& ra, do
     rb = __hiloint2double(__double2hiint(pb) + ((nb >> 6) << 20), __double2loint(pb));
 }
 
+// four exponentials with interleaved Horner chains (one coefficient load per four DFMAs)
+__device__ __forceinline__ void fast_exp_x4(const double (&x)[4], double (&r)[4]) {
+    double t[4], f[4], q[4], T[4], p[4];
+    int n[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        t[i] = fma(x[i], MC.e64_inv_ln2, MC.shift);
+        n[i] = __double2loint(t[i]);
+        T[i] = QMCCPW_EXP_TAB(n[i] & 63);
+        f[i] = t[i] - MC.shift;
+        q[i] = fma(f[i], -MC.e64_ln2_hi, x[i]);
+    }
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        q[i] = fma(f[i], -MC.e64_ln2_lo, q[i]);
+        p[i] = EXP_P[kExpDeg];
+    }
+#pragma unroll
+    for (int j = kExpDeg - 1; j >= 0; --j)
+#pragma unroll
+        for (int i = 0; i < 4; ++i) p[i] = fma(p[i], q[i], EXP_P[j]);
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        p[i] *= T[i];
+        r[i] = __hiloint2double(__double2hiint(p[i]) + ((n[i] >> 6) << 20), __double2loint(p[i]));
+    }
+}
+
 static __device__ __noinline__ double icdf_tail_poly(double w) {
     const double v = sqrt(w) - ICDF_TAIL_CENTER;
     double p = ICDF_TAIL[24];
@@ -276,6 +304,11 @@ __device__ __forceinline__ void normal_from_u32_x2(uint32_t ya, uint32_t yb, dou
     xa = upa ? -ra : ra;
     xb = upb ? -rb : rb;
 }
+
+// one lattice point -> one normal, out of line: for the bridge's rare data-dependent levels
+// (the terminal and the levels c >= 3 of each group's first descent), so that their copies
+// of the polynomial do not sit in the hot loop's instruction stream
+static __device__ __noinline__ double normal_from_u32_call(uint32_t y) { return normal_from_u32(y); }
 
 // four lattice points -> four standard normals (same arithmetic as normal_from_u32): four
 // interleaved Horner chains, so each coefficient loaded into a uniform register feeds four

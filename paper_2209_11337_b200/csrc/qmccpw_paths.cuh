@@ -25,6 +25,20 @@ namespace qmccpw {
 #ifndef QMCCPW_BB_GROUPED
 #define QMCCPW_BB_GROUPED 1
 #endif
+// grouped bridge: exps of four dates at once (push4) and the rare single normals out of line
+// A/B on one B200, C4 BB-W1 (ms/step): neither 26.43, push4 26.90, out-of-line single normals
+// 26.07, both 26.40
+#ifndef QMCCPW_BB_PUSH4
+#define QMCCPW_BB_PUSH4 0
+#endif
+#ifndef QMCCPW_BB_N1CALL
+#define QMCCPW_BB_N1CALL 1
+#endif
+#if QMCCPW_BB_N1CALL
+#define NORMAL1 normal_from_u32_call
+#else
+#define NORMAL1 normal_from_u32
+#endif
 #ifndef QMCCPW_BBAV_MINB
 #define QMCCPW_BBAV_MINB 4
 #endif
@@ -33,6 +47,18 @@ constexpr int paths_min_blocks() {
     return (COND == kW1 && METHOD == kQmc) ? (CONSTR == kBB ? QMCCPW_BB_MINB : CONSTR == kStd ? QMCCPW_STD_MINB : 0)
            : (COND == kW1 && METHOD == kMcAv && CONSTR == kBB) ? QMCCPW_BBAV_MINB
                                                                 : 0;
+}
+// X1 lookback envelope staging (QMCCPW_LB_SMEM, see qmccpw_pca.cuh): defined here for both
+// kernels of this header
+#ifndef QMCCPW_LB_SMEM
+#define QMCCPW_LB_SMEM 0
+#endif
+#ifndef QMCCPW_LB_HULL
+#define QMCCPW_LB_HULL 0
+#endif
+static __host__ __device__ size_t path_smem_base_bytes(const PathArgs& a, int constr, int cond, int method);
+__host__ __device__ __forceinline__ size_t path_lb_offset(const PathArgs& a, int constr, int cond, int method) {
+    return (path_smem_base_bytes(a, constr, cond, method) + 7) & ~(size_t)7;
 }
 // OWEN: nested scrambling of the Sobol' coordinates (row f4) -- a template flag so
 // that the other randomisations pay nothing for it (measured 0.5-4 % as a runtime test)
@@ -72,6 +98,12 @@ __global__ void __launch_bounds__(128, paths_min_blocks<CONSTR, COND, METHOD>())
     double* red = reinterpret_cast<double*>(HW);
     const int hw_size = 2 * nw * d;
     uint32_t* BS = HW + 2 * hw_size;  // [d] incremental Gray bases (sobol_build_hw_inc)
+    // X1 with a lookback (QMCCPW_LB_SMEM): the slopes sigma a_j, 1/(sigma a_j) [d] and each
+    // thread's envelope hull [d][tpb] bytes after the HW / reduction region
+    constexpr bool kLbSmem = (COND == kX1) && (METHOD == kQmc) && QMCCPW_LB_SMEM;
+    double* sl_b = reinterpret_cast<double*>(smem_raw + path_lb_offset(P, CONSTR, COND, METHOD));
+    double* sl_isa = sl_b + d;
+    uint8_t* hull_t = reinterpret_cast<uint8_t*>(sl_isa + d) + tid;
 
     const uint64_t K0 = P.point_offset + i0;
     const uint64_t Ab = K0 >> tpb_log2;
@@ -83,6 +115,7 @@ __global__ void __launch_bounds__(128, paths_min_blocks<CONSTR, COND, METHOD>())
     // dimension lookup
     constexpr bool kPerm = (CONSTR == kBB && METHOD == kQmc);
     math_tables_load(tid, tpb);
+    if (kLbSmem && P.has_lookback) x1_stage_slopes(P, sl_b, sl_isa, tid, tpb);
     if (METHOD != kQmc) __syncthreads();  // QMC: the barrier below publishes the tables
     if (METHOD == kQmc) {
         const uint32_t* src = P.vscr + (size_t)rep_local * d * 32;
@@ -259,7 +292,7 @@ __global__ void __launch_bounds__(128, paths_min_blocks<CONSTR, COND, METHOD>())
                 double stW[12];
                 int sp = 0;
                 int pos = 0;
-                stW[0] = P.sqrtT * normal_from_u32(sob.get(pos++));  // terminal: W(T) = sqrt(T) x_0
+                stW[0] = P.sqrtT * NORMAL1(sob.get(pos++));  // terminal: W(T) = sqrt(T) x_0
                 double Wl = 0.0, W1 = 0.0;
 #pragma unroll 1
                 for (int g = 0; g < (d >> 3); ++g) {
@@ -272,7 +305,7 @@ __global__ void __launch_bounds__(128, paths_min_blocks<CONSTR, COND, METHOD>())
                         double Wr = stW[sp];
 #pragma unroll 1
                         for (int c = e0 - 1; c >= 3; --c) {
-                            const double Wm = fma(P.bb_b[m - c], normal_from_u32(sob.get(pos++)), 0.5 * (Wl + Wr));
+                            const double Wm = fma(P.bb_b[m - c], NORMAL1(sob.get(pos++)), 0.5 * (Wl + Wr));
                             if (c > 3) stW[++sp] = Wm;
                             Wr = Wm;
                         }
@@ -294,10 +327,15 @@ __global__ void __launch_bounds__(128, paths_min_blocks<CONSTR, COND, METHOD>())
                     const double W6 = fma(b1, x[4], 0.5 * (M4 + R));
                     const double W5 = fma(b0, x[5], 0.5 * (M4 + W6));
                     const double W7 = fma(b0, x[6], 0.5 * (W6 + R));
+#if QMCCPW_BB_PUSH4
+                    w1.push4(P, 8 * g, Wa - W1, M2 - W1, W3 - W1, M4 - W1);
+                    w1.push4(P, 8 * g + 4, W5 - W1, W6 - W1, W7 - W1, R - W1);
+#else
                     w1.push2(P, 8 * g, Wa - W1, M2 - W1);
                     w1.push2(P, 8 * g + 2, W3 - W1, M4 - W1);
                     w1.push2(P, 8 * g + 4, W5 - W1, W6 - W1);
                     w1.push2(P, 8 * g + 6, W7 - W1, R - W1);
+#endif
                     Wl = R;
                 }
             } else if (CONSTR == kBB) {
@@ -615,7 +653,10 @@ __global__ void __launch_bounds__(128, paths_min_blocks<CONSTR, COND, METHOD>())
                 __syncwarp();
 
             }
-            tail_x1_all(P, cb, tpb, f, unconverged);
+            if (kLbSmem && P.has_lookback)
+                tail_x1_all(P, cb, tpb, f, unconverged, X1Slopes{sl_b, sl_isa}, QMCCPW_LB_HULL ? hull_t : nullptr, tpb);
+            else
+                tail_x1_all(P, cb, tpb, f, unconverged);
         }
 
         if (!valid) {
@@ -641,6 +682,14 @@ __global__ void __launch_bounds__(128, paths_min_blocks<CONSTR, COND, METHOD>())
 
 
 static size_t path_smem_bytes(const PathArgs& a, int constr, int cond, int method) {
+    size_t b = path_smem_base_bytes(a, constr, cond, method);
+    if (QMCCPW_LB_SMEM && cond == kX1 && method == kQmc && a.has_lookback)
+        b = path_lb_offset(a, constr, cond, method) + 2 * (size_t)a.d * sizeof(double) +
+            (QMCCPW_LB_HULL ? ((size_t)1 << a.tpb_log2) * (size_t)a.d : 0);  // slopes, hulls
+    return b;
+}
+
+static __host__ __device__ size_t path_smem_base_bytes(const PathArgs& a, int constr, int cond, int method) {
     const size_t tpb = (size_t)1 << a.tpb_log2, nw = tpb / 32;
     const bool need_buf = method == kQmc && (constr == kPca || cond == kX1);
     const bool two_buf = method == kQmc && constr == kPca && cond == kX1;

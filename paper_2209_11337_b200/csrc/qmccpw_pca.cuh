@@ -50,6 +50,19 @@ __host__ __device__ __forceinline__ size_t pca_stage_offset(int n_acc, int d, in
     b += hw > red ? hw : red;
     return (b + 7) & ~(size_t)7;
 }
+// X1 lookback: the envelope walk reads the slopes from shared memory (QMCCPW_LB_SMEM, one LDS
+// per reload instead of an L1 load of P.a) and, with QMCCPW_LB_HULL, keeps each lane's hull in
+// shared memory instead of a per-thread local array.  A/B on one B200, C4 PCA-X1 with the
+// lookback (ms/step): global slopes + local hull 215.5; shared slopes 234.1; shared slopes and
+// hull 300.3 (the extra 9 KB per block drop the kernel from 2 blocks/SM to 1).  BB-X1 with the
+// lookback (paths kernel): 164.9 / 188.5 / 187.2.  Divergent per-lane slope reads conflict in
+// the shared-memory banks; through L1 they cost less -- both options stay off.
+#ifndef QMCCPW_LB_SMEM
+#define QMCCPW_LB_SMEM 0
+#endif
+#ifndef QMCCPW_LB_HULL
+#define QMCCPW_LB_HULL 0
+#endif
 // LB (X1 only): the launch has a lookback option (staging + per-lane envelope walk)
 template <int COND, int KF, bool OWEN, bool LB>
 __global__ void __launch_bounds__(128, pca_min_blocks<COND, KF, LB>()) pca_kernel(const PathArgs P) {
@@ -80,8 +93,12 @@ __global__ void __launch_bounds__(128, pca_min_blocks<COND, KF, LB>()) pca_kerne
     uint32_t* BS = HW + 2 * hw_size;  // [d] incremental Gray bases (sobol_build_hw_inc)
     // X1 with a lookback: c_j of the warp's 32 paths staged [d][32] per warp, so that each lane
     // walks the upper envelope of its own path (the quad layout holds a path over 4 lanes)
-    double* stage = reinterpret_cast<double*>(smem_raw + pca_stage_offset(n_acc_smem, d, tpb)) +
-                    (size_t)(tid >> 5) * d * 32;
+    double* stage_base = reinterpret_cast<double*>(smem_raw + pca_stage_offset(n_acc_smem, d, tpb));
+    double* stage = stage_base + (size_t)(tid >> 5) * d * 32;
+    // ... then the slopes sigma a_j, 1/(sigma a_j) [d] each and the lanes' hulls [nw][d][32] bytes
+    double* sl_b = stage_base + (size_t)tpb * d;
+    double* sl_isa = sl_b + d;
+    uint8_t* hull_w = reinterpret_cast<uint8_t*>(sl_isa + d) + (size_t)(tid >> 5) * d * 32;
     const uint64_t K0 = P.point_offset + i0;
     const uint64_t Ab = K0 >> tpb_log2;
     {
@@ -96,6 +113,7 @@ __global__ void __launch_bounds__(128, pca_min_blocks<COND, KF, LB>()) pca_kerne
             QMCCPW_CHK_SMEM(&sh[idx]);
             sh[idx] = P.shift[(size_t)rep_local * d + idx];
         }
+        if (COND == kX1 && LB && QMCCPW_LB_SMEM) x1_stage_slopes(P, sl_b, sl_isa, tid, tpb);
         __syncthreads();
         sobol_build_g(vt, d, G, tid, tpb);
     }
@@ -354,7 +372,11 @@ __global__ void __launch_bounds__(128, pca_min_blocks<COND, KF, LB>()) pca_kerne
             for (int o = 0; o < P.n_opt; ++o) {
                 if (P.type[o] != kLookback) continue;
                 double fl[4];
-                x1_lookback(P, o, stage + lane, 32, fl);
+                if (QMCCPW_LB_SMEM)
+                    x1_lookback(P, o, stage + lane, 32, fl, X1Slopes{sl_b, sl_isa},
+                                QMCCPW_LB_HULL ? hull_w + lane : nullptr, 32);
+                else
+                    x1_lookback(P, o, stage + lane, 32, fl);
                 if (valid) {
                     if (P.path_out != nullptr && o == P.hook_option)
                         for (int qq = 0; qq < 4; ++qq) P.path_out[ip * 4 + qq] = fl[qq];
@@ -396,6 +418,7 @@ static size_t pca_smem_bytes(const PathArgs& a, bool lb, int cond) {
     const bool warpsum = cond == kW1 && QMCCPW_PCA_WARPSUM;
     size_t b = pca_stage_offset(warpsum ? 0 : a.n_opt * 8, a.d, (int)tpb);
     if (lb) b += tpb * a.d * sizeof(double);  // [nw][d][32] staging
+    if (lb && QMCCPW_LB_SMEM) b += 2 * a.d * sizeof(double) + (QMCCPW_LB_HULL ? tpb * a.d : 0);  // slopes, hulls
     return b;
 }
 

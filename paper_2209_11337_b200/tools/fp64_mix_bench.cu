@@ -51,6 +51,39 @@ void run(const char* name, int sms) {
     cudaFree(d);
 }
 
+// DFMA-only variants: chain count, operands from registers (b loaded per thread) or constants
+template <int ILP, bool REG>
+__global__ void dfma_only(double* out, int iters, double a, double b) {
+    double x[ILP];
+    for (int i = 0; i < ILP; ++i) x[i] = threadIdx.x * 1e-3 + i;
+    double ra = a + threadIdx.x * 1e-12, rb = b + threadIdx.x * 1e-15;
+#pragma unroll 2
+    for (int it = 0; it < iters; ++it)
+#pragma unroll
+        for (int i = 0; i < ILP; ++i) x[i] = REG ? fma(x[i], ra, rb) : fma(x[i], a, b);
+    double s = 0;
+    for (int i = 0; i < ILP; ++i) s += x[i];
+    if (s == 1234.5) out[0] = s;
+}
+template <int ILP, bool REG>
+void run_only(const char* name, int sms, int bps, int tpb) {
+    double* d;
+    cudaMalloc(&d, 8);
+    const int blocks = sms * bps, iters = (1 << 17) / ILP;
+    dfma_only<ILP, REG><<<blocks, tpb>>>(d, 64, 0.999, 1e-7);
+    cudaEvent_t e0, e1;
+    cudaEventCreate(&e0);
+    cudaEventCreate(&e1);
+    cudaEventRecord(e0);
+    dfma_only<ILP, REG><<<blocks, tpb>>>(d, iters, 0.999, 1e-7);
+    cudaEventRecord(e1);
+    cudaEventSynchronize(e1);
+    float ms;
+    cudaEventElapsedTime(&ms, e0, e1);
+    printf("%-40s %8.3f ms  DFMA %6.2f TFLOP/s\n", name, ms, 2.0 * blocks * tpb * (double)iters * ILP / ms / 1e9);
+    cudaFree(d);
+}
+
 int main() {
     int sms;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
@@ -59,5 +92,11 @@ int main() {
     run<4, 1>("DFMA 32 + DMMA 4 per iter", sms);
     run<2, 1>("DFMA 16 + DMMA 4 per iter", sms);
     run<4, 2>("DFMA 32 + DMMA 8 per iter", sms);
+    run_only<8, false>("DFMA ILP8 const operands 4x256", sms, 4, 256);
+    run_only<8, true>("DFMA ILP8 register operands 4x256", sms, 4, 256);
+    run_only<16, true>("DFMA ILP16 register operands 4x256", sms, 4, 256);
+    run_only<4, true>("DFMA ILP4 register operands 8x256", sms, 8, 256);
+    run_only<8, true>("DFMA ILP8 register operands 2x512", sms, 2, 512);
+    run_only<8, true>("DFMA ILP8 register operands 8x128", sms, 8, 128);
     return 0;
 }
