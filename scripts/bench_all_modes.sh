@@ -8,3 +8,5 @@ done
 for c in "2 1" "1 1" "0 1"; do set -- $c; run --construction $1 --conditioning $2 --options 0,1,2; done   # f1
 for c in "1 0" "2 0" "2 1" "3 0" "3 1"; do set -- $c; run --method $1 --construction $2; done                 # f2
 timeout 600 python bench.py --workload C5 --steps 3 --warmup 3 --no-cpu-baseline 2>/dev/null | grep '^{' >> $out
+timeout 600 python bench.py --points 8388608 --steps 3 --warmup 3 --no-cpu-baseline 2>/dev/null | grep '^{' >> $out   # x8 variant of C4
+timeout 600 python bench.py --scaling weak --steps 5 --warmup 3 --no-cpu-baseline 2>/dev/null | grep '^{' >> $out
