@@ -555,14 +555,23 @@ struct DeviceGuard {
 int launch_portfolio_plan(DeviceCache* c, const Plan& pl, const Scratch& s, uint64_t cell_begin, uint64_t cell_end,
                           double* d_partials, double* d_path_out, uint32_t rep_base, cudaStream_t st) {
     const size_t ob = (size_t)pl.n_opt * sizeof(PortfolioOption);
+    // ordered by option type (stable): the kernel gives each thread two options of the table,
+    // so a warp then runs one type's tail (the binary call needs one Phibar, the others two)
+    // without divergence; each entry keeps its slot in the call's partial row
     std::vector<PortfolioOption> host(pl.n_opt);
-    for (int o = 0; o < pl.n_opt; ++o) {
-        host[o].type = pl.types[o];
-        host[o].family = pl.fam_of[o];
-        host[o].K = pl.p[o].K;
-        host[o].lnK = std::log(pl.p[o].K);
-        bs_pivots(pl.types[o], pl.p[o], host[o].piv);
-    }
+    int n = 0;
+    for (int t = 0; t < 3; ++t)
+        for (int o = 0; o < pl.n_opt; ++o) {
+            if (pl.types[o] != t) continue;
+            PortfolioOption& h = host[n++];
+            h.type = pl.types[o];
+            h.family = pl.fam_of[o];
+            h.slot = o;
+            h.pad = 0;
+            h.K = pl.p[o].K;
+            h.lnK = std::log(pl.p[o].K);
+            bs_pivots(pl.types[o], pl.p[o], h.piv);
+        }
     CUDA_TRY(cudaMemcpyAsync(s.opts, host.data(), ob, cudaMemcpyHostToDevice, st));
     CUDA_TRY(cudaStreamSynchronize(st));  // the host staging vector dies with this scope
     PortfolioArgs a;

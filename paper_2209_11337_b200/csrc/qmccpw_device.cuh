@@ -382,6 +382,13 @@ __device__ __forceinline__ X1Sums x1_solve(const PathArgs& P, int o, bool arith,
     // q_j = e^{kappa_j}, kappa_j = sigma a_j (sigma a_j / 2 - u) quadratic in j, so q_j follows
     // by two products per date (ratio rho_j = q_{j+1}/q_j, rho_{j+1} = rho_j e^{(sigma da)^2})
     const bool lin = arith && P.x1_lin;
+    // w_j Phibar(x_j), x_j = u - sigma a_j, without a per-date phi: w_j phi(x_j) = phi(u) E_j, so it
+    // is phi(u) E_j R(x_j) for x_j >= 0 and w_j - phi(u) E_j R(-x_j) below (R the Mills ratio)
+    double phu = 0.0;
+    if (arith && !flat) {
+        double Qu_, Q2_, ph2_;
+        phibar_phi_x2(u, u, Qu_, Q2_, phu, ph2_);
+    }
     double qa = 0.0, rho = 0.0, g = 0.0;
     if (lin) {
         const double a0 = P.a[0], a1 = P.a[1], sda = sg * (a1 - a0);
@@ -406,7 +413,7 @@ __device__ __forceinline__ X1Sums x1_solve(const PathArgs& P, int o, bool arith,
         Qst = fma(ab * ab, Eb, Qst);
         Vst = fma(Eb, Rb - sg * tb + ab * u, Vst);
         if (arith) {
-            double wa, wb, Pa = 1.0, Pb = 1.0, pa, pb;
+            double wa, wb;
             if (lin) {
                 const double qb = qa * rho;
                 wa = Ea * qa;
@@ -417,12 +424,20 @@ __device__ __forceinline__ X1Sums x1_solve(const PathArgs& P, int o, bool arith,
             } else {
                 fast_exp_x2(fma(0.5 * sg * sg * aa, aa, ca), fma(0.5 * sg * sg * ab, ab, cbb), wa, wb);
             }
-            if (!flat) phibar_phi_x2(u - sg * aa, u - sg * ab, Pa, Pb, pa, pb);  // Phi(sigma a - u) = Phibar(u - sigma a)
             wb *= wgt;
-            sumW = fma(wa, Pa, sumW);
-            sumWv = fma(wa * (Ra - sg * ta + sg * aa * aa), Pa, sumWv);
-            sumW = fma(wb, Pb, sumW);
-            sumWv = fma(wb * (Rb - sg * tb + sg * ab * ab), Pb, sumWv);
+            double WPa = wa, WPb = wb;  // flat: the common Phibar(u - sigma a) is applied after the loop
+            if (!flat) {  // Phi(sigma a - u) = Phibar(u - sigma a)
+                const double xa = u - sg * aa, xb = u - sg * ab;
+                double Ma, Mb;
+                mills_x2(xa, xb, Ma, Mb);
+                const double ga = phu * Ea * Ma, gb = phu * Eb * Mb;  // Eb, wb carry the odd-d weight
+                WPa = xa >= 0.0 ? ga : wa - ga;
+                WPb = xb >= 0.0 ? gb : wb - gb;
+            }
+            sumW += WPa;
+            sumWv = fma(Ra - sg * ta + sg * aa * aa, WPa, sumWv);
+            sumW += WPb;
+            sumWv = fma(Rb - sg * tb + sg * ab * ab, WPb, sumWv);
         }
     }
     if (flat) {

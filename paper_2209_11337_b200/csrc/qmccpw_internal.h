@@ -117,9 +117,11 @@ struct PathArgs {
 constexpr int kMaxPortfolio = 1024;
 constexpr int kMaxFamilies = 8;
 
-struct PortfolioOption {  // device table, one per option
+struct PortfolioOption {  // device table, one per option, ordered by type (see launch_portfolio_plan)
     int type;
     int family;
+    int slot;      // the option's index in the call (its partial-row slot)
+    int pad;
     double K, lnK;
     double piv[4];
 };

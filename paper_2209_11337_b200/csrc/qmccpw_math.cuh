@@ -374,6 +374,23 @@ __device__ __forceinline__ void phibar_phi_x2(double xa, double xb, double& Qa, 
     Qa = xa >= 0.0 ? qa : MC.one - qa;
     Qb = xb >= 0.0 ? qb : MC.one - qb;
 }
+// The Mills ratio R(|x|) = Phibar(|x|) / phi(|x|) alone, for two arguments: the polynomial
+// part of phibar_phi_x2, same arithmetic (Phibar(|x|) = phi(|x|) R(|x|) there).  The X1
+// arithmetic sums use it with w_j phi(u - sigma a_j) = phi(u) E_j (qmccpw_device.cuh x1_solve).
+__device__ __forceinline__ void mills_x2(double xa, double xb, double& Ra, double& Rb) {
+    const double aa = fabs(xa), ab = fabs(xb);
+    const double ra = rcp_newton(aa + MC.mills_c), rb = rcp_newton(ab + MC.mills_c);
+    const double ta = fma(-MC.mills_2c, ra, MC.one) - MILLS_H_CENTER, tb = fma(-MC.mills_2c, rb, MC.one) - MILLS_H_CENTER;
+    double ha = MILLS_P[kMillsDeg], hb = MILLS_P[kMillsDeg];
+#pragma unroll
+    for (int j = kMillsDeg - 1; j >= 0; --j) {
+        ha = fma(ha, ta, MILLS_P[j]);
+        hb = fma(hb, tb, MILLS_P[j]);
+    }
+    Ra = ha * ra;
+    Rb = hb * rb;
+}
+
 // The same for four arguments (two options of the C5 portfolio's phase B): four
 // independent Horner chains per coefficient load.
 __device__ __forceinline__ void phibar_phi_x4(const double (&x)[4], double (&Q)[4], double (&ph)[4]) {
@@ -403,6 +420,35 @@ __device__ __forceinline__ void phibar_phi_x4(const double (&x)[4], double (&Q)[
         const double q = ph[i] * (h[i] * r[i]);
         Q[i] = x[i] >= 0.0 ? q : MC.one - q;
     }
+}
+
+// The Mills ratio R(|x|) for four arguments (four Horner chains per coefficient load), and
+// phi for two: the two halves of phibar_phi_x4, same arithmetic.  The C5 portfolio's phase B
+// combines them with A S~ phi(psi - s) = D K phi(psi), so one phi serves both Phibar's.
+__device__ __forceinline__ void mills_x4(const double (&x)[4], double (&R)[4]) {
+    double a[4], r[4], t[4], h[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        a[i] = fabs(x[i]);
+        r[i] = rcp_newton(a[i] + MC.mills_c);
+        t[i] = fma(-MC.mills_2c, r[i], MC.one) - MILLS_H_CENTER;
+        h[i] = MILLS_P[kMillsDeg];
+    }
+#pragma unroll
+    for (int j = kMillsDeg - 1; j >= 0; --j)
+#pragma unroll
+        for (int i = 0; i < 4; ++i) h[i] = fma(h[i], t[i], MILLS_P[j]);
+#pragma unroll
+    for (int i = 0; i < 4; ++i) R[i] = h[i] * r[i];
+}
+__device__ __forceinline__ void phi_x2(double xa, double xb, double& pa, double& pb) {
+    const double aa = fabs(xa), ab = fabs(xb);
+    const double sa = aa * aa, sb = ab * ab;
+    const double la = fma(aa, aa, -sa), lb = fma(ab, ab, -sb);
+    double ea, eb;
+    fast_exp_x2(MC.minus_half * sa, MC.minus_half * sb, ea, eb);
+    pa = (sa < MC.exp_floor * MC.two) ? MC.inv_sqrt_2pi * ea * fma(MC.minus_half, la, MC.one) : 0.0;
+    pb = (sb < MC.exp_floor * MC.two) ? MC.inv_sqrt_2pi * eb * fma(MC.minus_half, lb, MC.one) : 0.0;
 }
 
 __device__ __forceinline__ double normal_sf(double x) {

@@ -302,6 +302,14 @@ __global__ void __launch_bounds__(128, pca_min_blocks<COND, KF, LB>()) pca_kerne
                     if (r4 == 0 && valid && !conv) ++unconverged;
                     double Dst = 0.0, Qst = 0.0, Vst = 0.0, sumW = 0.0, sumWv = 0.0;
                     const bool need_arith = P.x1_need_arith[o] != 0;
+                    // arithmetic sums: w_j Phibar(x_j), x_j = u - sigma a_j, without a per-date phi:
+                    // w_j phi(x_j) = phi(u) E_j, so it is phi(u) E_j R(x_j) for x_j >= 0 and
+                    // w_j - phi(u) E_j R(-x_j) below (R the Mills ratio)
+                    double phu = 0.0;
+                    if (need_arith) {
+                        double Qu_, Q2_, ph2_;
+                        phibar_phi_x2(u, u, Qu_, Q2_, phu, ph2_);
+                    }
 #pragma unroll
                     for (int jt = 0; jt < JT; ++jt) {
                         const int j0 = 8 * jt + 2 * r4;
@@ -322,15 +330,17 @@ __global__ void __launch_bounds__(128, pca_min_blocks<COND, KF, LB>()) pca_kerne
                         Qst = fma(ab * ab, Eb, Qst);
                         Vst = fma(Eb, Rb - sg * tb + ab * u, Vst);
                         if (need_arith) {
-                            double wa, wb, Pa, Pb, pa, pb;
+                            double wa, wb, Ma, Mb;
                             fast_exp_x2(fma(0.5 * sg * sg * aa, aa, ca), fma(0.5 * sg * sg * ab, ab, cb2), wa, wb);
-                            phibar_phi_x2(u - sg * aa, u - sg * ab, Pa, Pb, pa, pb);
-                            wa = (j0 < d) ? wa : 0.0;
-                            wb = (j0 + 1 < d) ? wb : 0.0;
-                            sumW = fma(wa, Pa, sumW);
-                            sumWv = fma(wa * (Ra - sg * ta + sg * aa * aa), Pa, sumWv);
-                            sumW = fma(wb, Pb, sumW);
-                            sumWv = fma(wb * (Rb - sg * tb + sg * ab * ab), Pb, sumWv);
+                            const double xa = u - sg * aa, xb = u - sg * ab;
+                            mills_x2(xa, xb, Ma, Mb);
+                            const double ga = phu * Ea * Ma, gb = phu * Eb * Mb;  // Ea, Eb are 0 past d
+                            const double WPa = (j0 < d) ? (xa >= 0.0 ? ga : wa - ga) : 0.0;
+                            const double WPb = (j0 + 1 < d) ? (xb >= 0.0 ? gb : wb - gb) : 0.0;
+                            sumW += WPa;
+                            sumWv = fma(Ra - sg * ta + sg * aa * aa, WPa, sumWv);
+                            sumW += WPb;
+                            sumWv = fma(Rb - sg * tb + sg * ab * ab, WPb, sumWv);
                         }
                     }
                     const X1Sums xs{u, quad_sum(Dst), quad_sum(Qst), quad_sum(Vst), quad_sum(sumW), quad_sum(sumWv)};

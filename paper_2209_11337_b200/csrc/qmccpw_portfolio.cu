@@ -18,7 +18,7 @@ namespace qmccpw {
 //    owning thread only: deterministic, and no 64 KB of per-option smem, so two
 //    blocks fit per SM).
 // ---------------------------------------------------------------------------
-constexpr int kStatW = 8;  // staged per (point, family): SA, lnSA, IA, IA/SA, Smax, lnSmax, Imax, near-tie flag
+constexpr int kStatW = 8;  // staged per (point, family): SA, lnSA, IA, IA/SA, Smax, lnSmax, Imax/Smax, near-tie flag
 
 template <int KF, bool OWEN>
 __global__ void __launch_bounds__(128, 3) portfolio_kernel(const PortfolioArgs P) {  // 3 blocks: 72.5 KB smem each
@@ -171,18 +171,24 @@ __global__ void __launch_bounds__(128, 3) portfolio_kernel(const PortfolioArgs P
                     st[3] = sI / sS;  // I_A / S~_A (binary vega)
                     st[4] = Smax;
                     st[5] = lnSmax;
-                    st[6] = Smax * ym;
+                    st[6] = ym;  // I_max / S~_max (lookback vega)
                     st[7] = (P.has_lookback && em - es < 1e-12) ? 1.0 : 0.0;
                 }
             }
         }
         __syncthreads();
         // ---- phase B -------------------------------------------------------
-        // per-option constants (P:396-414, P:544-600 with the divisions hoisted)
+        // per-option constants (P:396-414, P:544-600 with the divisions hoisted).  Calls
+        // (arithmetic, lookback) use A S~ phi(psi - s) = D K phi(psi) (psi = (ln K - ln S~ -
+        // omega t_1)/s, omega + sigma^2/2 = r), so A S~ Phibar(psi - s) is D K phi(psi) R(psi - s)
+        // for psi >= s and A S~ - D K phi(psi) R(s - psi) below, R the Mills ratio: one phi per
+        // option and point instead of two; vega takes I/S~ from the staged statistics.  The
+        // binary call needs Phibar(psi) alone.  The option table is ordered by type, so a warp
+        // runs one type (one Mills pair for two binaries, four otherwise).
         struct OptC {
             const double* st;  // stats of the option's family, point 0
-            int lb, bin;
-            double c_lnK, c_s, inv_s, K, D, Afac, sqrt_t1, inv_sigma, c1, c3;
+            int lb, bin, slot;
+            double c_lnK, c_s, inv_s, K, D, DK, Afac, sqrt_t1, inv_sigma, inv_S0, c1, c3;
             double piv[4];
         };
         auto load_opt = [&](int o, OptC& c) {
@@ -192,30 +198,37 @@ __global__ void __launch_bounds__(128, 3) portfolio_kernel(const PortfolioArgs P
             c.st = stats + (size_t)op.family * kStatW;
             c.lb = op.type == kLookback;
             c.bin = op.type == kBinary;
+            c.slot = op.slot;
             c.c_lnK = op.lnK - F.omega * F.t1;
             c.c_s = F.s;
             c.inv_s = F.inv_s;
             c.K = op.K;
             c.D = F.Dfac;
+            c.DK = F.Dfac * op.K;
             c.Afac = F.Afac;
             c.sqrt_t1 = F.sqrt_t1;
             c.inv_sigma = F.inv_sigma;
-            c.c1 = c.bin ? F.Dfac * F.inv_s * inv_S0 : F.Afac * inv_S0;                      // delta factor
+            c.inv_S0 = inv_S0;
+            c.c1 = F.Dfac * F.inv_s * inv_S0;                                                // binary delta factor
             c.c3 = (c.bin ? F.Dfac : op.K * F.Dfac) * F.inv_s * inv_S0 * inv_S0;            // gamma factor
             for (int qq = 0; qq < 4; ++qq) c.piv[qq] = op.piv[qq];
         };
-        // one point of one option: the four centred outputs
-        auto tail = [&](const OptC& c, const double* st, double Q0, double Q1, double ph, double psi, double f[4]) {
+        // one point of one option: R0 = R(|psi|), R1 = R(|psi - s|), ph = phi(psi)
+        auto tail = [&](const OptC& c, const double* st, double psi, double R0, double R1, double ph, double f[4]) {
+            const double q0 = ph * R0;
+            const double Q0 = psi >= 0.0 ? q0 : MC.one - q0;
             if (c.bin) {
                 f[0] = c.D * Q0;
                 f[1] = c.c1 * ph;
                 f[2] = c.D * ph * (st[3] * c.inv_s + psi * c.inv_sigma - c.sqrt_t1);
                 f[3] = c.c3 * ph * (psi * c.inv_s - 1.0);
             } else {
-                const double stat = c.lb ? st[4] : st[0], I = c.lb ? st[6] : st[2];
-                f[0] = c.Afac * stat * Q1 - c.D * c.K * Q0;
-                f[1] = c.c1 * stat * Q1;
-                f[2] = c.Afac * Q1 * I + c.K * c.D * ph * c.sqrt_t1;
+                const double stat = c.lb ? st[4] : st[0], IoS = c.lb ? st[6] : st[3];  // I / S~
+                const double g1 = c.DK * ph * R1;
+                const double AQ1S = (psi - c.c_s >= 0.0) ? g1 : c.Afac * stat - g1;  // A S~ Phibar(psi - s)
+                f[0] = AQ1S - c.DK * Q0;
+                f[1] = AQ1S * c.inv_S0;
+                f[2] = AQ1S * IoS + c.K * c.D * ph * c.sqrt_t1;
                 f[3] = c.c3 * ph;
             }
         };
@@ -227,6 +240,7 @@ __global__ void __launch_bounds__(128, 3) portfolio_kernel(const PortfolioArgs P
             OptC A, B;
             load_opt(o, A);
             load_opt(two ? o2 : o, B);
+            const bool bins = A.bin && B.bin;
             double s1a[4] = {0, 0, 0, 0}, s2a[4] = {0, 0, 0, 0}, s1b[4] = {0, 0, 0, 0}, s2b[4] = {0, 0, 0, 0};
 #pragma unroll 1
             for (int sl = 0; sl < 64; ++sl) {
@@ -238,17 +252,25 @@ __global__ void __launch_bounds__(128, 3) portfolio_kernel(const PortfolioArgs P
                 if (two && B.lb && sb[7] != 0.0) ++ties;
                 const double psia = (A.c_lnK - (A.lb ? sa[5] : sa[1])) * A.inv_s;
                 const double psib = (B.c_lnK - (B.lb ? sb[5] : sb[1])) * B.inv_s;
-                const double xq[4] = {psia, psia - A.c_s, psib, psib - B.c_s};
-                double Qq[4], phq[4];
-                phibar_phi_x4(xq, Qq, phq);
-                const double Q0a = Qq[0], Q1a = Qq[1], pha = phq[0], Q0b = Qq[2], Q1b = Qq[3], phb = phq[2];
+                double R[4];
+                if (bins) {
+                    mills_x2(psia, psib, R[0], R[2]);
+                    R[1] = R[3] = 0.0;
+                } else {
+                    const double xq[4] = {psia, psia - A.c_s, psib, psib - B.c_s};
+                    mills_x4(xq, R);
+                }
+                double pha, phb;
+                phi_x2(psia, psib, pha, phb);
                 double fa[4], fb[4];
-                tail(A, sa, Q0a, Q1a, pha, psia, fa);
-                tail(B, sb, Q0b, Q1b, phb, psib, fb);
+                tail(A, sa, psia, R[0], R[1], pha, fa);
+                tail(B, sb, psib, R[2], R[3], phb, fb);
                 if (P.path_out != nullptr) {
-                    for (int qq = 0; qq < 4; ++qq) P.path_out[((ib + pth) * nopt + o) * 4 + qq] = fa[qq];
+#pragma unroll
+                    for (int qq = 0; qq < 4; ++qq) P.path_out[((ib + pth) * nopt + A.slot) * 4 + qq] = fa[qq];
                     if (two)
-                        for (int qq = 0; qq < 4; ++qq) P.path_out[((ib + pth) * nopt + o2) * 4 + qq] = fb[qq];
+#pragma unroll
+                        for (int qq = 0; qq < 4; ++qq) P.path_out[((ib + pth) * nopt + B.slot) * 4 + qq] = fb[qq];
                 }
 #pragma unroll
                 for (int qq = 0; qq < 4; ++qq) {
@@ -261,14 +283,14 @@ __global__ void __launch_bounds__(128, 3) portfolio_kernel(const PortfolioArgs P
             }
 #pragma unroll
             for (int qq = 0; qq < 4; ++qq) {
-                prow[o * 8 + 2 * qq] += s1a[qq];
-                prow[o * 8 + 2 * qq + 1] += s2a[qq];
+                prow[A.slot * 8 + 2 * qq] += s1a[qq];
+                prow[A.slot * 8 + 2 * qq + 1] += s2a[qq];
             }
             if (two) {
 #pragma unroll
                 for (int qq = 0; qq < 4; ++qq) {
-                    prow[o2 * 8 + 2 * qq] += s1b[qq];
-                    prow[o2 * 8 + 2 * qq + 1] += s2b[qq];
+                    prow[B.slot * 8 + 2 * qq] += s1b[qq];
+                    prow[B.slot * 8 + 2 * qq + 1] += s2b[qq];
                 }
             }
         }
