@@ -4,7 +4,7 @@ seeded points.  Tolerances:
   normals                |dx| <= 2e-15 max(1, |x|)
   per-path values        |df| <= 1e-12 (|f| + |pivot_K|)    (pivot_K = the d = 1
                          Black-Scholes value of that output at the option's strike);
-                         gamma x max(1, 0.03/(sigma^2 t_1)): the threshold psi / u* carries
+                         gamma x max(1, 0.015/(sigma^2 t_1)): the threshold psi / u* carries
                          an absolute rounding of ~c eps / (sigma sqrt t_1) and gamma
                          differentiates it once more -> relative ~ c eps / s^2 (measured
                          maximum in DESIGN.md 6 and tests/tools/parity_report.py)
@@ -16,6 +16,8 @@ seeded points.  Tolerances:
   counters               equal
 """
 
+import os
+
 import numpy as np
 import pytest
 
@@ -24,6 +26,19 @@ import workloads as W
 pytestmark = pytest.mark.gpu
 
 MODES_ALL = [(0, 0), (1, 0), (2, 0), (0, 1), (1, 1), (2, 1)]  # (construction, conditioning)
+# gamma's per-path bound 1e-12 max(1, GAMMA_C / (sigma^2 t_1)); GAMMA_C from the measured
+# maximum of err_gamma x sigma^2 t_1 over this whole file: 5.25e-15 over all 582 per-path checks
+# (QMCCPW_PARITY_LOG run on a B200, profiles/r02/parity_per_path_deviations.txt) -> 0.015 keeps
+# a 2.9x margin
+GAMMA_C = 0.015
+
+
+def _log_dev(err4, s2):
+    """QMCCPW_PARITY_LOG=<file>: append this check's max per-output deviations (and gamma x s2)."""
+    path = os.environ.get("QMCCPW_PARITY_LOG")
+    if path:
+        with open(path, "a") as fh:
+            fh.write(" ".join(f"{v:.3e}" for v in err4) + f" {err4[3] * s2:.3e}\n")
 
 
 @pytest.fixture(scope="module")
@@ -93,7 +108,8 @@ def _pv_check(q, O, otype, K, d, constr, cond, method, rep, k0, k1, S0=W.S0, sig
     piv = np.abs(O.pivots(otype, K, mk))
     err = np.abs(g - o) / (np.abs(o) + piv)
     s2 = sigma * sigma * T / d
-    tol = np.array([1e-12, 1e-12, 1e-12, 1e-12 * max(1.0, 0.03 / s2)])
+    tol = np.array([1e-12, 1e-12, 1e-12, 1e-12 * max(1.0, GAMMA_C / s2)])
+    _log_dev(err.max(axis=0), s2)
     assert np.all(err <= tol), (otype, K, d, constr, cond, method, err.max(axis=0),
                                 np.unravel_index(np.argmax(err / tol), err.shape))
 
@@ -380,7 +396,8 @@ def test_portfolio_path_values(q, O, d, rand):
         piv = np.abs(O.pivots(o["type"], o["K"], mk)) + np.abs(O.pivots(o["type"], o["S0"], mk))
         err = np.abs(g[:, j, :] - ref) / (np.abs(ref) + piv)
         s2 = o["sigma"] ** 2 * o["T"] / d
-        tol = np.array([1e-12, 1e-12, 1e-12, 1e-12 * max(1.0, 0.03 / s2)])
+        tol = np.array([1e-12, 1e-12, 1e-12, 1e-12 * max(1.0, GAMMA_C / s2)])
+        _log_dev(err.max(axis=0), s2)
         assert np.all(err <= tol), (j, o, err.max(axis=0))
 
 
