@@ -158,19 +158,52 @@ __device__ __forceinline__ void sobol_build_hw(const uint32_t* vt, const uint32_
 // ---------------------------------------------------------------------------
 // (MC-CPW / MC+AV-CPW / LR+MC normals, drawn in paths_kernel and lr_path: Philox4x32-10,
 // counter (k_lo, k_hi, j/4, (rep<<8)|0x02), word j%4 -- the paper's PSEUDO generator.)
+// QMCCPW_TRACK_FLAG: the near-tie test of the lookback's argmax kept as a flag ("the runner-up
+// is within 1e-12 of the running maximum", reset when a new maximum clears the old one by
+// 1e-12) instead of the runner-up value itself: the same decision (both compare the same
+// difference of two doubles), two instructions and one register pair less per date
+#ifndef QMCCPW_TRACK_FLAG
+#define QMCCPW_TRACK_FLAG 1
+#endif
 struct W1Acc {
     double sumS, sumI, emax, esec, ymax;
+    bool tie;
     __device__ __forceinline__ void reset() {
         sumS = 0.0; sumI = 0.0; emax = -CUDART_INF; esec = -CUDART_INF; ymax = 0.0;
+        tie = false;
     }
     // lookback: lowest argmax of e_j (= argmax of S~_j) and the runner-up exponent,
     // with plain compare-selects (no NaN-aware fmax/fmin: e is always finite)
     __device__ __forceinline__ void track(double e, double y) {
+#if QMCCPW_TRACK_FLAG
+        const double dd = e - emax;  // -inf - (-inf) never happens: emax starts at -inf, e is finite
+        const bool gt = dd > 0.0;
+        const bool near = fabs(dd) < 1e-12;
+        tie = gt ? near : (tie || near);
+        ymax = gt ? y : ymax;
+        emax = gt ? e : emax;
+#else
         const bool gt = e > emax;
         const double cand = gt ? emax : e;
         esec = cand > esec ? cand : esec;
         ymax = gt ? y : ymax;
         emax = gt ? e : emax;
+#endif
+    }
+    // a near-tie of the argmax (reading 20): the runner-up within 1e-12 of the maximum in log
+    __device__ __forceinline__ bool near_tie() const {
+#if QMCCPW_TRACK_FLAG
+        return tie;
+#else
+        return emax - esec < 1e-12;
+#endif
+    }
+    // set from a (max, runner-up) pair reduced elsewhere (the PCA quad reduction)
+    __device__ __forceinline__ void set_max(double em, double es, double ym) {
+        emax = em;
+        esec = es;
+        ymax = ym;
+        tie = em - es < 1e-12;
     }
     // date index j (0-based, t_{j+1} - t_1 = j dt), Wt = W~(t_{j+1} - t_1)
     __device__ __forceinline__ void push(const PathArgs& P, int j, double Wt) {

@@ -310,24 +310,48 @@ __device__ __forceinline__ void normal_from_u32_x2(uint32_t ya, uint32_t yb, dou
 // of the polynomial do not sit in the hot loop's instruction stream
 static __device__ __noinline__ double normal_from_u32_call(uint32_t y) { return normal_from_u32(y); }
 
-// four lattice points -> four standard normals (same arithmetic as normal_from_u32): four
-// interleaved Horner chains, so each coefficient loaded into a uniform register feeds four
-// DFMAs (half the constant-load instructions per normal of the paired form)
-__device__ __forceinline__ void normal_from_u32_x4(const uint32_t (&y)[4], double (&x)[4]) {
-    bool up[4];
-    double u[4], z[4], t[4], w[4], v[4], p[4];
+// ln t for N arguments at once (same arithmetic as fast_log / fast_log_x2)
+template <int N>
+__device__ __forceinline__ void fast_log_xn(const double (&t)[N], double (&l)[N]) {
+    double m[N], k[N], r[N], p[N];
+    double2 c[N];
 #pragma unroll
-    for (int i = 0; i < 4; ++i) {
+    for (int i = 0; i < N; ++i) {
+        const int h = __double2hiint(t[i]);
+        m[i] = __hiloint2double((h & 0x000FFFFF) | 0x3FF00000, __double2loint(t[i]));
+        k[i] = (double)((h >> 20) - 1023);
+        c[i] = QMCCPW_LOG_TAB((h >> 14) & 63);
+        r[i] = fma(m[i], c[i].x, -MC.one);
+        p[i] = LOG_P[kLogDeg];
+    }
+#pragma unroll
+    for (int j = kLogDeg - 1; j >= 0; --j)
+#pragma unroll
+        for (int i = 0; i < N; ++i) p[i] = fma(p[i], r[i], LOG_P[j]);
+#pragma unroll
+    for (int i = 0; i < N; ++i) {
+        const double s = fma(r[i] * r[i], p[i], r[i]) + c[i].y;
+        l[i] = fma(k[i], MC.ln2_hi, fma(k[i], MC.ln2_lo, s));
+    }
+}
+
+// N lattice points -> N standard normals (same arithmetic as normal_from_u32): N interleaved
+// Horner chains, so each coefficient loaded into a uniform register feeds N DFMAs
+template <int N>
+__device__ __forceinline__ void normal_from_u32_xn(const uint32_t (&y)[N], double (&x)[N]) {
+    bool up[N];
+    double u[N], z[N], t[N], w[N], v[N], p[N];
+#pragma unroll
+    for (int i = 0; i < N; ++i) {
         up[i] = (y[i] >> 31) != 0u;
         const uint32_t l = up[i] ? ~y[i] : y[i];
         u[i] = fma((double)l, MC.p32, MC.p33);
         z[i] = fma(MC.two, u[i], -MC.one);
         t[i] = (MC.four * u[i]) * (MC.one - u[i]);
     }
-    fast_log_x2(t[0], t[1], w[0], w[1]);
-    fast_log_x2(t[2], t[3], w[2], w[3]);
+    fast_log_xn<N>(t, w);
 #pragma unroll
-    for (int i = 0; i < 4; ++i) {
+    for (int i = 0; i < N; ++i) {
         w[i] = -w[i];
         v[i] = w[i] - ICDF_CENTRAL_CENTER;
         p[i] = ICDF_C[kIcdfDeg];
@@ -335,13 +359,18 @@ __device__ __forceinline__ void normal_from_u32_x4(const uint32_t (&y)[4], doubl
 #pragma unroll
     for (int j = kIcdfDeg - 1; j >= 0; --j)
 #pragma unroll
-        for (int i = 0; i < 4; ++i) p[i] = fma(p[i], v[i], ICDF_C[j]);
+        for (int i = 0; i < N; ++i) p[i] = fma(p[i], v[i], ICDF_C[j]);
 #pragma unroll
-    for (int i = 0; i < 4; ++i) {
+    for (int i = 0; i < N; ++i) {
         if (w[i] >= MC.w_split) p[i] = icdf_tail_poly(w[i]);  // u < 4.8e-4: rare, divergent
         const double r = z[i] * p[i];
         x[i] = up[i] ? -r : r;
     }
+}
+// four lattice points -> four standard normals: each coefficient loaded into a uniform register
+// feeds four DFMAs (half the constant-load instructions per normal of the paired form)
+__device__ __forceinline__ void normal_from_u32_x4(const uint32_t (&y)[4], double (&x)[4]) {
+    normal_from_u32_xn<4>(y, x);
 }
 
 __device__ __forceinline__ double normal_pdf(double x) {

@@ -28,6 +28,11 @@ namespace qmccpw {
 // grouped bridge: exps of four dates at once (push4) and the rare single normals out of line
 // A/B on one B200, C4 BB-W1 (ms/step): neither 26.43, push4 26.90, out-of-line single normals
 // 26.07, both 26.40
+// the seven static normals of a group as 4 + 3 interleaved chains (two coefficient streams)
+// instead of 4 + 2 + 1 (three)
+#ifndef QMCCPW_BB_X3
+#define QMCCPW_BB_X3 1
+#endif
 #ifndef QMCCPW_BB_PUSH4
 #define QMCCPW_BB_PUSH4 0
 #endif
@@ -245,10 +250,10 @@ __global__ void __launch_bounds__(128, paths_min_blocks<CONSTR, COND, METHOD>())
                     if (METHOD == kMcAv) w1m.push(P, d - 1, -Wpend);
                 }
             }
-            if (P.has_lookback && w1.emax - w1.esec < 1e-12) ++ties;
+            if (P.has_lookback && w1.near_tie()) ++ties;
             tail_w1_all(P, w1, f);
             if (METHOD == kMcAv) {
-                if (P.has_lookback && w1m.emax - w1m.esec < 1e-12) ++ties;
+                if (P.has_lookback && w1m.near_tie()) ++ties;
                 double fm[kMaxOpt][4];
                 tail_w1_all(P, w1m, fm);
 #pragma unroll
@@ -316,8 +321,19 @@ __global__ void __launch_bounds__(128, paths_min_blocks<CONSTR, COND, METHOD>())
                     double x[7];
                     double x4[4];
                     normal_from_u32_x4(y4, x4);
+#if QMCCPW_BB_X3
+                    {  // the last three as three interleaved chains (one coefficient stream)
+                        const uint32_t y3[3] = {sob.get(pos + 4), sob.get(pos + 5), sob.get(pos + 6)};
+                        double x3[3];
+                        normal_from_u32_xn<3>(y3, x3);
+                        x[4] = x3[0];
+                        x[5] = x3[1];
+                        x[6] = x3[2];
+                    }
+#else
                     normal_from_u32_x2(sob.get(pos + 4), sob.get(pos + 5), x[4], x[5]);
                     x[6] = normal_from_u32(sob.get(pos + 6));
+#endif
                     pos += 7;
                     const double M4 = fma(b2, x4[0], 0.5 * (Wl + R));   // W(8g+4)
                     const double M2 = fma(b1, x4[1], 0.5 * (Wl + M4));  // W(8g+2)
@@ -517,13 +533,11 @@ __global__ void __launch_bounds__(128, paths_min_blocks<CONSTR, COND, METHOD>())
                     if (rt == mine) {
                         w1.sumS = a0;
                         w1.sumI = a1;
-                        w1.emax = a2;
-                        w1.esec = a3;
-                        w1.ymax = a4;
+                        w1.set_max(a2, a3, a4);
                     }
                 }
             }
-            if (P.has_lookback && w1.emax - w1.esec < 1e-12) ++ties;
+            if (P.has_lookback && w1.near_tie()) ++ties;
             tail_w1_all(P, w1, f);
         } else {
             // X1: c_j = ln S0 + omega t_j + sigma R_j, R = M x with x_1 := 0

@@ -31,6 +31,9 @@ namespace qmccpw {
 #ifndef QMCCPW_PCA_WARPSUM
 #define QMCCPW_PCA_WARPSUM 1
 #endif
+#ifndef QMCCPW_PCA_X1_SMEMC
+#define QMCCPW_PCA_X1_SMEMC 1
+#endif
 #ifndef QMCCPW_PCA_X1_MINB
 #define QMCCPW_PCA_X1_MINB 5
 #endif
@@ -78,7 +81,12 @@ __global__ void __launch_bounds__(128, pca_min_blocks<COND, KF, LB>()) pca_kerne
     const int ppt = kCellPoints >> tpb_log2;
     const int nw = tpb >> 5;
     const int n_acc = P.n_opt * 8;
-    constexpr bool kWarpSum = COND == kW1 && QMCCPW_PCA_WARPSUM;
+    // X1 without a lookback (QMCCPW_PCA_X1_SMEMC): the lane's c_j go to shared memory after the
+    // contraction and the per-strike passes loop over them rolled (small code, 32 registers
+    // freed); the centred sums are warp-reduced like W1's
+    constexpr bool kSmemC = COND == kX1 && !LB && QMCCPW_PCA_X1_SMEMC;
+    constexpr int kXU = kSmemC ? 1 : 2 * JT;  // unroll of the X1 per-date loops
+    constexpr bool kWarpSum = (COND == kW1 && QMCCPW_PCA_WARPSUM) || kSmemC;
     const int n_acc_smem = kWarpSum ? 0 : n_acc;  // smem accumulator rows
     // per-path accumulators in smem: X1 as scalars (one quad lane per path), W1 as (S1, S2) pairs
     double* accs = reinterpret_cast<double*>(smem_raw);
@@ -95,6 +103,7 @@ __global__ void __launch_bounds__(128, pca_min_blocks<COND, KF, LB>()) pca_kerne
     // walks the upper envelope of its own path (the quad layout holds a path over 4 lanes)
     double* stage_base = reinterpret_cast<double*>(smem_raw + pca_stage_offset(n_acc_smem, d, tpb));
     double* stage = stage_base + (size_t)(tid >> 5) * d * 32;
+    double* cst = stage_base + tid;  // kSmemC: c_j of this lane at [v][tpb], v < 2 JT
     // ... then the slopes sigma a_j, 1/(sigma a_j) [d] each and the lanes' hulls [nw][d][32] bytes
     double* sl_b = stage_base + (size_t)tpb * d;
     double* sl_isa = sl_b + d;
@@ -224,9 +233,7 @@ __global__ void __launch_bounds__(128, pca_min_blocks<COND, KF, LB>()) pca_kerne
                 if ((lane >> 3) == rt) {
                     w1own.sumS = a0;
                     w1own.sumI = a1;
-                    w1own.emax = a2;
-                    w1own.esec = a3;
-                    w1own.ymax = a4;
+                    w1own.set_max(a2, a3, a4);
                 }
             } else {
                 // X1: c_j = ln S0 + omega t_j + sigma R_j, then one Newton solve per strike group
@@ -236,6 +243,14 @@ __global__ void __launch_bounds__(128, pca_min_blocks<COND, KF, LB>()) pca_kerne
                     cv[2 * jt] = fma(sg, cv[2 * jt], fma(P.omega, (double)(j0 + 1) * P.t1, P.lnS0));
                     cv[2 * jt + 1] = fma(sg, cv[2 * jt + 1], fma(P.omega, (double)(j0 + 2) * P.t1, P.lnS0));
                 }
+                if (kSmemC) {
+#pragma unroll
+                    for (int v = 0; v < 2 * JT; ++v) {
+                        QMCCPW_CHK_SMEM(&cst[(size_t)v * tpb]);
+                        cst[(size_t)v * tpb] = cv[v];
+                    }
+                }
+#define CV(v) (kSmemC ? cst[(size_t)(v) * tpb] : cv[(v)])
                 if (LB) {
                     double* sw = stage + 8 * rt + q;
 #pragma unroll
@@ -257,14 +272,15 @@ __global__ void __launch_bounds__(128, pca_min_blocks<COND, KF, LB>()) pca_kerne
                     const double lnK = P.lnK[o], lndK = P.lndK[o];
                     // bracket [min_j (lnK - c_j)/(sigma a_j), min_j (ln dK - c_j)/(sigma a_j)] and mean c
                     double ulo = CUDART_INF, uhi = CUDART_INF, sumc = 0.0;
-#pragma unroll
+#pragma unroll kXU
                     for (int v = 0; v < 2 * JT; ++v) {
                         const int j = 8 * (v >> 1) + 2 * r4 + (v & 1);
                         if (j < d) {
                             const double isa = __ldg(P.inv_sa + j);
-                            ulo = fmin(ulo, (lnK - cv[v]) * isa);
-                            uhi = fmin(uhi, (lndK - cv[v]) * isa);
-                            sumc += cv[v];
+                            const double cvv = CV(v);
+                            ulo = fmin(ulo, (lnK - cvv) * isa);
+                            uhi = fmin(uhi, (lndK - cvv) * isa);
+                            sumc += cvv;
                         }
                     }
                     ulo = quad_min(ulo);
@@ -275,13 +291,13 @@ __global__ void __launch_bounds__(128, pca_min_blocks<COND, KF, LB>()) pca_kerne
 #pragma unroll 1
                     for (int it = 0; it < kNewtonMax; ++it) {
                         double S = 0.0, SA = 0.0, SAA = 0.0;
-#pragma unroll
+#pragma unroll kXU
                         for (int jt = 0; jt < JT; ++jt) {
                             const int j0 = 8 * jt + 2 * r4;
                             const double aa = (j0 < d) ? __ldg(P.a + j0) : 0.0;
                             const double ab = (j0 + 1 < d) ? __ldg(P.a + j0 + 1) : 0.0;
                             double Ea, Eb;
-                            fast_exp_x2(fma(sg * aa, u, cv[2 * jt]), fma(sg * ab, u, cv[2 * jt + 1]), Ea, Eb);
+                            fast_exp_x2(fma(sg * aa, u, CV(2 * jt)), fma(sg * ab, u, CV(2 * jt + 1)), Ea, Eb);
                             Ea = (j0 < d) ? Ea : 0.0;
                             Eb = (j0 + 1 < d) ? Eb : 0.0;
                             S += Ea;
@@ -310,13 +326,13 @@ __global__ void __launch_bounds__(128, pca_min_blocks<COND, KF, LB>()) pca_kerne
                         double Qu_, Q2_, ph2_;
                         phibar_phi_x2(u, u, Qu_, Q2_, phu, ph2_);
                     }
-#pragma unroll
+#pragma unroll kXU
                     for (int jt = 0; jt < JT; ++jt) {
                         const int j0 = 8 * jt + 2 * r4;
                         const double aa = (j0 < d) ? __ldg(P.a + j0) : 0.0;
                         const double ab = (j0 + 1 < d) ? __ldg(P.a + j0 + 1) : 0.0;
                         const double ta = (double)(j0 + 1) * P.t1, tb = ta + P.t1;
-                        const double ca = cv[2 * jt], cb2 = cv[2 * jt + 1];
+                        const double ca = CV(2 * jt), cb2 = CV(2 * jt + 1);
                         const double Ra = (ca - P.lnS0 - P.omega * ta) * P.inv_sigma;
                         const double Rb = (cb2 - P.lnS0 - P.omega * tb) * P.inv_sigma;
                         double Ea, Eb;
@@ -356,22 +372,27 @@ __global__ void __launch_bounds__(128, pca_min_blocks<COND, KF, LB>()) pca_kerne
                             if (o == P.hook_option && P.type[o] != kLookback)
                                 for (int qq = 0; qq < 4; ++qq) P.path_out[ip * 4 + qq] = f[o][qq];
                     }
+                    if (!kSmemC) {
 #pragma unroll
-                    for (int o = 0; o < kMaxOpt; ++o) {
-                        if (o < P.n_opt && P.type[o] != kLookback) {
+                        for (int o = 0; o < kMaxOpt; ++o) {
+                            if (o < P.n_opt && P.type[o] != kLookback) {
 #pragma unroll
-                            for (int qq = 0; qq < 4; ++qq) {
-                                const double y = f[o][qq] - P.piv[o][qq];
-                                double* a1 = accs + (size_t)(o * 8 + qq * 2) * tpb + tp;
-                                QMCCPW_CHK_SMEM(&a1[tpb]);
-                                a1[0] += y;
-                                a1[tpb] = fma(y, y, a1[tpb]);
+                                for (int qq = 0; qq < 4; ++qq) {
+                                    const double y = f[o][qq] - P.piv[o][qq];
+                                    double* a1 = accs + (size_t)(o * 8 + qq * 2) * tpb + tp;
+                                    QMCCPW_CHK_SMEM(&a1[tpb]);
+                                    a1[0] += y;
+                                    a1[tpb] = fma(y, y, a1[tpb]);
+                                }
                             }
                         }
                     }
                 }
+                // the quad's four lanes hold the same f: lane r4 = 0 contributes each path once
+                if (kSmemC) warp_slot_sums(f, P, valid && r4 == 0, lane, wacc + (tid >> 5) * 32);
             }
         }
+#undef CV
         if (COND == kX1 && LB) {
             // lookback options: lane L walks the envelope of path wbase + L from the staged c_j
             __syncwarp();
@@ -406,7 +427,7 @@ __global__ void __launch_bounds__(128, pca_min_blocks<COND, KF, LB>()) pca_kerne
             const uint64_t i = i0 + tid + ((uint64_t)a << tpb_log2);
             const bool valid = i < P.n_points;  // all lanes run: the warp reduction needs them
             npts += valid ? 1u : 0u;
-            if (valid && P.has_lookback && w1.emax - w1.esec < 1e-12) ++ties;
+            if (valid && P.has_lookback && w1.near_tie()) ++ties;
             double f[kMaxOpt][4];
             tail_w1_all(P, w1, f);
             if (P.path_out != nullptr && valid) {
@@ -420,13 +441,16 @@ __global__ void __launch_bounds__(128, pca_min_blocks<COND, KF, LB>()) pca_kerne
         }
     }
     if (COND == kW1 && !kWarpSum) acc2_to_wacc(P, acc2, wacc, tpb, tid);
-    block_epilogue(P, COND == kX1 ? accs : nullptr, wacc, red, n_acc, tpb, tid, cell, unconverged, ties, npts);
+    block_epilogue(P, (COND == kX1 && !kSmemC) ? accs : nullptr, wacc, red, n_acc, tpb, tid, cell, unconverged, ties,
+                   npts);
 }
 
 static size_t pca_smem_bytes(const PathArgs& a, bool lb, int cond) {
     const size_t tpb = (size_t)1 << a.tpb_log2;
-    const bool warpsum = cond == kW1 && QMCCPW_PCA_WARPSUM;
+    const bool smemc = cond == kX1 && !lb && QMCCPW_PCA_X1_SMEMC;
+    const bool warpsum = (cond == kW1 && QMCCPW_PCA_WARPSUM) || smemc;
     size_t b = pca_stage_offset(warpsum ? 0 : a.n_opt * 8, a.d, (int)tpb);
+    if (smemc) b += (size_t)(a.M_ld / 4) * tpb * sizeof(double);  // c_j [2 JT][tpb]
     if (lb) b += tpb * a.d * sizeof(double);  // [nw][d][32] staging
     if (lb && QMCCPW_LB_SMEM) b += 2 * a.d * sizeof(double) + (QMCCPW_LB_HULL ? tpb * a.d : 0);  // slopes, hulls
     return b;
