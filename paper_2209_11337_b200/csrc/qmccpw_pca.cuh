@@ -31,6 +31,10 @@ namespace qmccpw {
 #ifndef QMCCPW_PCA_WARPSUM
 #define QMCCPW_PCA_WARPSUM 1
 #endif
+// normals four k-steps at a time (QMCCPW_PCA_X4) instead of two
+#ifndef QMCCPW_PCA_X4
+#define QMCCPW_PCA_X4 0
+#endif
 #ifndef QMCCPW_PCA_X1_SMEMC
 #define QMCCPW_PCA_X1_SMEMC 1
 #endif
@@ -84,6 +88,7 @@ __global__ void __launch_bounds__(128, pca_min_blocks<COND, KF, LB>()) pca_kerne
     // X1 without a lookback (QMCCPW_PCA_X1_SMEMC): the lane's c_j go to shared memory after the
     // contraction and the per-strike passes loop over them rolled (small code, 32 registers
     // freed); the centred sums are warp-reduced like W1's
+    constexpr bool kX4 = QMCCPW_PCA_X4 && (KF % 4 == 0);
     constexpr bool kSmemC = COND == kX1 && !LB && QMCCPW_PCA_X1_SMEMC;
     constexpr int kXU = kSmemC ? 1 : 2 * JT;  // unroll of the X1 per-date loops
     constexpr bool kWarpSum = (COND == kW1 && QMCCPW_PCA_WARPSUM) || kSmemC;
@@ -160,6 +165,37 @@ __global__ void __launch_bounds__(128, pca_min_blocks<COND, KF, LB>()) pca_kerne
 #pragma unroll
             for (int v = 0; v < 2 * JT; ++v) cv[v] = 0.0;
             double W1v = 0.0;
+            if (kX4) {
+                // four k-steps per iteration: four normals as interleaved chains (one coefficient
+                // stream per four), then four DMMAs per column tile in the same k order
+#pragma unroll 1
+                for (int f = 0; f < KF; f += 4) {
+                    uint32_t y4[4];
+                    double x4[4], a4[4];
+#pragma unroll
+                    for (int i = 0; i < 4; ++i) {
+                        const int jj = 4 * (f + i) + r4;
+                        y4[i] = sp.get(jj < d ? jj : d - 1);
+                    }
+                    normal_from_u32_x4(y4, x4);
+#pragma unroll
+                    for (int i = 0; i < 4; ++i) {
+                        const int jj = 4 * (f + i) + r4;
+                        a4[i] = (jj < d && !(COND == kX1 && jj == 0)) ? x4[i] : 0.0;
+                    }
+#pragma unroll
+                    for (int jt = 0; jt < JT; ++jt) {
+                        const double* Mrow = P.M + (size_t)(8 * jt + q) * DP + r4 + 4 * f;
+#pragma unroll
+                        for (int i = 0; i < 4; ++i) {
+                            const double b = __ldg(Mrow + 4 * i);
+                            asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+                                         : "+d"(cv[2 * jt]), "+d"(cv[2 * jt + 1])
+                                         : "d"(a4[i]), "d"(b));
+                        }
+                    }
+                }
+            } else
 #pragma unroll 1
             for (int f = 0; f < KF; f += 2) {
                 const int ja = 4 * f + r4, jb = 4 * (f + 1) + r4;
