@@ -640,6 +640,148 @@ __device__ __forceinline__ void x1_lookback(const PathArgs& P, int o, const doub
     f[3] = D * K * ph / (S0 * S0 * sg * __ldg(P.a + j0));
 }
 
+// Lookback under X1 over a quad (the PCA kernel's layout: lane r4 holds the path's lines
+// j = 8 jt + 2 r4 + e, e = 0, 1, at slot v = 2 jt + e; cq(v, lane_r4) returns c_j of slot v held
+// by quad lane lane_r4).  The same envelope integral as x1_lookback, built by gift wrapping
+// instead of a per-lane hull: from j0 = argmin_j u_j (the top line at u*), the next segment's
+// line is the steeper line that overtakes the active one first, x(act, k) = (c_act - c_k) /
+// (b_k - b_act) minimal (ties: the steeper), found by the four lanes over their 16 lines each
+// and a quad reduction; division-free comparisons (b_k > b_act).  Slopes strictly increase
+// with j for BB, PCA and GPCA; equal slopes (STD) leave the single highest line.
+template <int NV, class CQ>
+__device__ __forceinline__ void x1_lookback_quad(const PathArgs& P, int o, int r4, CQ cq, double f[4]) {
+    const int d = P.d;
+    const double sg = P.sigma, lnK = P.lnK[o];
+    // u* and j0 (lowest j among the minima)
+    double ust = CUDART_INF;
+    int j0 = 0x7fffffff;
+#pragma unroll 1
+    for (int v = 0; v < NV; ++v) {
+        const int j = 8 * (v >> 1) + 2 * r4 + (v & 1);
+        if (j < d) {
+            const double uj = (lnK - cq(v, r4)) * __ldg(P.inv_sa + j);
+            if (uj < ust || (uj == ust && j < j0)) {
+                ust = uj;
+                j0 = j;
+            }
+        }
+    }
+#pragma unroll
+    for (int off = 1; off <= 2; off <<= 1) {
+        const double pu = __shfl_xor_sync(0xffffffffu, ust, off);
+        const int pj = __shfl_xor_sync(0xffffffffu, j0, off);
+        if (pu < ust || (pu == ust && pj < j0)) {
+            ust = pu;
+            j0 = pj;
+        }
+    }
+    auto cj = [&](int j) { return cq(2 * (j >> 3) + (j & 1), (j & 7) >> 1); };
+    double J = 0.0, V = 0.0;
+    int act = j0;
+    double lo = ust;
+    const bool flat = __ldg(P.a) == __ldg(P.a + d - 1);
+    if (flat) {  // STD: all slopes equal -> the single highest line (lowest j on ties), from u*
+        double cb = -CUDART_INF;
+        int jb = 0x7fffffff;
+#pragma unroll 1
+        for (int v = 0; v < NV; ++v) {
+            const int j = 8 * (v >> 1) + 2 * r4 + (v & 1);
+            if (j < d) {
+                const double c = cq(v, r4);
+                if (c > cb || (c == cb && j < jb)) {
+                    cb = c;
+                    jb = j;
+                }
+            }
+        }
+#pragma unroll
+        for (int off = 1; off <= 2; off <<= 1) {
+            const double pc = __shfl_xor_sync(0xffffffffu, cb, off);
+            const int pj = __shfl_xor_sync(0xffffffffu, jb, off);
+            if (pc > cb || (pc == cb && pj < jb)) {
+                cb = pc;
+                jb = pj;
+            }
+        }
+        act = jb;
+    }
+    // the quads of a warp finish after different segment counts, and the loop shuffles with a
+    // full mask: it runs until every quad is done (warp-uniform exit), finished quads idle
+    bool done = false;
+#pragma unroll 1
+    for (;;) {
+        if (!__any_sync(0xffffffffu, !done)) break;
+        const double ca = cj(act), ba = sg * __ldg(P.a + act);
+        // my best overtaking line: smallest x = N / D (D > 0), ties to the larger j
+        double Nb = 0.0, Db = 0.0;
+        int kb = -1;
+        if (!flat) {
+            // my lines are j(v) = 8 (v >> 1) + 2 r4 + (v & 1), increasing in v: start at the first
+            // one beyond act (act only grows, so the scans shrink along the walk)
+            const int rel = act + 1 - 2 * r4;  // smallest j - 2 r4 wanted
+            int v = rel <= 0 ? 0 : 2 * (rel >> 3) + ((rel & 7) == 0 ? 0 : ((rel & 7) == 1 ? 1 : 2));
+#pragma unroll 1
+            for (; v < NV; ++v) {
+                const int j = 8 * (v >> 1) + 2 * r4 + (v & 1);
+                if (j > act && j < d) {
+                    const double D = sg * __ldg(P.a + j) - ba;
+                    if (D > 0.0) {
+                        const double N = ca - cq(v, r4);
+                        const double lhs = N * Db, rhs = Nb * D;
+                        if (kb < 0 || lhs < rhs || (lhs == rhs && j > kb)) {
+                            Nb = N;
+                            Db = D;
+                            kb = j;
+                        }
+                    }
+                }
+            }
+        }
+#pragma unroll
+        for (int off = 1; off <= 2; off <<= 1) {
+            const double pN = __shfl_xor_sync(0xffffffffu, Nb, off);
+            const double pD = __shfl_xor_sync(0xffffffffu, Db, off);
+            const int pk = __shfl_xor_sync(0xffffffffu, kb, off);
+            if (pk >= 0) {
+                const double lhs = pN * Db, rhs = Nb * pD;
+                if (kb < 0 || lhs < rhs || (lhs == rhs && pk > kb)) {
+                    Nb = pN;
+                    Db = pD;
+                    kb = pk;
+                }
+            }
+        }
+        if (done) continue;
+        double hi = kb >= 0 ? Nb / Db : CUDART_INF;
+        hi = fmax(hi, lo);
+        const double aa = ba / sg;
+        const double tj = (double)(act + 1) * P.t1;
+        const double Rj = (ca - P.lnS0 - P.omega * tj) * P.inv_sigma;
+        const double w = fast_exp(fma(0.5 * ba, ba, ca));
+        double Qlo, Qhi, plo, phi_hi;
+        phibar_phi_x2(lo - ba, (kb < 0) ? 0.0 : hi - ba, Qlo, Qhi, plo, phi_hi);
+        if (kb < 0) {
+            Qhi = 0.0;
+            phi_hi = 0.0;
+        }
+        J = fma(w, Qlo - Qhi, J);
+        V = fma(w, (Rj - sg * tj + sg * aa * aa) * (Qlo - Qhi) + aa * (plo - phi_hi), V);
+        if (kb < 0) {
+            done = true;
+        } else {
+            act = kb;
+            lo = hi;
+        }
+    }
+    const double D = P.Dfac, S0 = P.S0, K = P.K[o];
+    double Qu, Q2, ph, ph2;
+    phibar_phi_x2(ust, ust, Qu, Q2, ph, ph2);
+    f[0] = D * (J - K * Qu);
+    f[1] = D * J / S0;
+    f[2] = D * V;
+    f[3] = D * K * ph / (S0 * S0 * sg * __ldg(P.a + j0));
+}
+
 // all options of the launch: one Newton solve (and one set of E*-sums) per distinct strike
 __device__ __forceinline__ void tail_x1_all(const PathArgs& P, const double* cb, int stride, double f[kMaxOpt][4],
                                             unsigned& unconverged, const X1Slopes& sl = X1Slopes{nullptr, nullptr},
@@ -714,32 +856,38 @@ __device__ __forceinline__ void lr_path(const PathArgs& P, uint32_t rep, uint64_
 // over xor 2, 1; lanes 4s..4s+3 end with the warp total of slot s = lane >> 2, and
 // lane 4s adds it to the warp's running sums wacc[o*8 + s] in shared memory (no
 // per-thread accumulators, nothing live in registers across paths).
+__device__ __forceinline__ void warp_slot_sums_one(const double (&f4)[4], const double (&piv)[4], bool valid, int lane,
+                                                   double* wacc8) {
+    double v[8];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+        const double y = valid ? f4[q] - piv[q] : 0.0;
+        v[2 * q] = y;
+        v[2 * q + 1] = y * y;
+    }
+#pragma unroll
+    for (int half = 4; half > 0; half >>= 1) {
+        const bool up = (lane & (half * 4)) != 0;
+#pragma unroll
+        for (int j = 0; j < half; ++j) {
+            const double send = up ? v[j] : v[j + half];
+            const double keep = up ? v[j + half] : v[j];
+            v[j] = keep + __shfl_xor_sync(0xffffffffu, send, half * 4);
+        }
+    }
+    v[0] += __shfl_xor_sync(0xffffffffu, v[0], 2);
+    v[0] += __shfl_xor_sync(0xffffffffu, v[0], 1);
+    if ((lane & 3) == 0) wacc8[lane >> 2] += v[0];
+}
+// skip_lookback: leave the lookback options' slots alone (their values arrive separately)
 __device__ __forceinline__ void warp_slot_sums(const double (&f)[kMaxOpt][4], const PathArgs& P, bool valid,
-                                               int lane, double* wacc) {
+                                               int lane, double* wacc, bool skip_lookback = false) {
 #pragma unroll
     for (int o = 0; o < kMaxOpt; ++o) {
         if (o >= P.n_opt) break;  // warp-uniform
-        double v[8];
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-            const double y = valid ? f[o][q] - P.piv[o][q] : 0.0;
-            v[2 * q] = y;
-            v[2 * q + 1] = y * y;
-        }
-#pragma unroll
-        for (int half = 4; half > 0; half >>= 1) {
-            const bool up = (lane & (half * 4)) != 0;
-#pragma unroll
-            for (int j = 0; j < half; ++j) {
-                const double send = up ? v[j] : v[j + half];
-                const double keep = up ? v[j + half] : v[j];
-                v[j] = keep + __shfl_xor_sync(0xffffffffu, send, half * 4);
-            }
-        }
-        v[0] += __shfl_xor_sync(0xffffffffu, v[0], 2);
-        v[0] += __shfl_xor_sync(0xffffffffu, v[0], 1);
-        QMCCPW_CHECK(o * 8 + (lane >> 2) < 32);
-        if ((lane & 3) == 0) wacc[o * 8 + (lane >> 2)] += v[0];
+        if (skip_lookback && P.type[o] == kLookback) continue;
+        QMCCPW_CHECK(o * 8 + 7 < 32);
+        warp_slot_sums_one(f[o], P.piv[o], valid, lane, wacc + o * 8);
     }
 }
 

@@ -31,9 +31,17 @@ namespace qmccpw {
 #ifndef QMCCPW_PCA_WARPSUM
 #define QMCCPW_PCA_WARPSUM 1
 #endif
-// normals four k-steps at a time (QMCCPW_PCA_X4) instead of two
-#ifndef QMCCPW_PCA_X4
-#define QMCCPW_PCA_X4 0
+#ifndef QMCCPW_LB_QUAD
+#define QMCCPW_LB_QUAD 1
+#endif
+// quad-walk lookback kernel: A/B on one B200, C4 PCA-X1 with the lookback (ms/step): per-lane
+// hull 202.0; quad walk at 3 / 4 / 5 blocks/SM 230.5 / 207.0 / 192.8 (scans from the first line
+// beyond the active one)
+#ifndef QMCCPW_LB_MINB
+#define QMCCPW_LB_MINB 5
+#endif
+#ifndef QMCCPW_LB_ROLLED
+#define QMCCPW_LB_ROLLED 0
 #endif
 #ifndef QMCCPW_PCA_X1_SMEMC
 #define QMCCPW_PCA_X1_SMEMC 1
@@ -46,7 +54,8 @@ namespace qmccpw {
 // (with a lookback the [d][32] per-warp staging allows 2 blocks/SM at d = 64: registers are free)
 template <int COND, int KF, bool LB>
 constexpr int pca_min_blocks() {
-    return KF > 16 ? 0 : (LB ? 2 : (COND == kW1 ? QMCCPW_PCA_W1_MINB : QMCCPW_PCA_X1_MINB));
+    return KF > 16 ? 0
+                   : (LB ? (QMCCPW_LB_QUAD ? QMCCPW_LB_MINB : 2) : (COND == kW1 ? QMCCPW_PCA_W1_MINB : QMCCPW_PCA_X1_MINB));
 }
 // byte offset of the X1 lookback staging: accs [n_acc][tpb] | vt, sh, G (+ pad) | HW / red
 __host__ __device__ __forceinline__ size_t pca_stage_offset(int n_acc, int d, int tpb) {
@@ -88,10 +97,17 @@ __global__ void __launch_bounds__(128, pca_min_blocks<COND, KF, LB>()) pca_kerne
     // X1 without a lookback (QMCCPW_PCA_X1_SMEMC): the lane's c_j go to shared memory after the
     // contraction and the per-strike passes loop over them rolled (small code, 32 registers
     // freed); the centred sums are warp-reduced like W1's
-    constexpr bool kX4 = QMCCPW_PCA_X4 && (KF % 4 == 0);
-    constexpr bool kSmemC = COND == kX1 && !LB && QMCCPW_PCA_X1_SMEMC;
-    constexpr int kXU = kSmemC ? 1 : 2 * JT;  // unroll of the X1 per-date loops
-    constexpr bool kWarpSum = (COND == kW1 && QMCCPW_PCA_WARPSUM) || kSmemC;
+    // X1 lookback by a quad-cooperative envelope walk (QMCCPW_LB_QUAD, x1_lookback_quad): the
+    // c_j stay in the quad layout (shared memory, as kSmemC), no per-warp [d][32] staging
+    constexpr bool kLbQuad = COND == kX1 && LB && QMCCPW_LB_QUAD && QMCCPW_PCA_X1_SMEMC;
+    constexpr bool kSmemC = COND == kX1 && (!LB || kLbQuad) && QMCCPW_PCA_X1_SMEMC;
+    // with a lookback (QMCCPW_LB_ROLLED) the per-strike passes read c_j from the lookback's
+    // per-warp staging instead (row stride kSS = 36 doubles: a quad's four dates fall in
+    // different bank pairs)
+    constexpr bool kLbRolled = COND == kX1 && LB && !kLbQuad && QMCCPW_LB_ROLLED;
+    constexpr int kSS = kLbRolled ? 36 : 32;
+    constexpr int kXU = (kSmemC || kLbRolled) ? 1 : 2 * JT;  // unroll of the X1 per-date loops
+    constexpr bool kWarpSum = (COND == kW1 && QMCCPW_PCA_WARPSUM) || kSmemC || kLbRolled;
     const int n_acc_smem = kWarpSum ? 0 : n_acc;  // smem accumulator rows
     // per-path accumulators in smem: X1 as scalars (one quad lane per path), W1 as (S1, S2) pairs
     double* accs = reinterpret_cast<double*>(smem_raw);
@@ -107,10 +123,10 @@ __global__ void __launch_bounds__(128, pca_min_blocks<COND, KF, LB>()) pca_kerne
     // X1 with a lookback: c_j of the warp's 32 paths staged [d][32] per warp, so that each lane
     // walks the upper envelope of its own path (the quad layout holds a path over 4 lanes)
     double* stage_base = reinterpret_cast<double*>(smem_raw + pca_stage_offset(n_acc_smem, d, tpb));
-    double* stage = stage_base + (size_t)(tid >> 5) * d * 32;
+    double* stage = stage_base + (size_t)(tid >> 5) * d * kSS;
     double* cst = stage_base + tid;  // kSmemC: c_j of this lane at [v][tpb], v < 2 JT
     // ... then the slopes sigma a_j, 1/(sigma a_j) [d] each and the lanes' hulls [nw][d][32] bytes
-    double* sl_b = stage_base + (size_t)tpb * d;
+    double* sl_b = stage_base + (size_t)tpb * d * kSS / 32;
     double* sl_isa = sl_b + d;
     uint8_t* hull_w = reinterpret_cast<uint8_t*>(sl_isa + d) + (size_t)(tid >> 5) * d * 32;
     const uint64_t K0 = P.point_offset + i0;
@@ -158,6 +174,8 @@ __global__ void __launch_bounds__(128, pca_min_blocks<COND, KF, LB>()) pca_kerne
             const SobolBlock sp{G, HWb, d, nw, (int)(kp0 & 31), (int)((kp0 >> 5) & (uint64_t)(nw - 1)),
                                 (int)((kp0 >> tpb_log2) - Ab), OWEN ? sh : nullptr};
             // k-steps f (pairs) outer, not unrolled: each step draws this lane's two A
+            // elements (four k-steps per iteration with four-way normals measured slower:
+            // C4 PCA-W1 46.4 -> 50.7 ms at 8 blocks/SM, 47.2 at 6;
             // elements x[path][4 f + r4] and feeds them to all JT column tiles at once, so
             // the code holds one normal pair and 2 JT DMMAs instead of KF/2 pairs and KF JT
             // (the unrolled form was instruction-fetch bound); same k order, same bits.
@@ -165,37 +183,6 @@ __global__ void __launch_bounds__(128, pca_min_blocks<COND, KF, LB>()) pca_kerne
 #pragma unroll
             for (int v = 0; v < 2 * JT; ++v) cv[v] = 0.0;
             double W1v = 0.0;
-            if (kX4) {
-                // four k-steps per iteration: four normals as interleaved chains (one coefficient
-                // stream per four), then four DMMAs per column tile in the same k order
-#pragma unroll 1
-                for (int f = 0; f < KF; f += 4) {
-                    uint32_t y4[4];
-                    double x4[4], a4[4];
-#pragma unroll
-                    for (int i = 0; i < 4; ++i) {
-                        const int jj = 4 * (f + i) + r4;
-                        y4[i] = sp.get(jj < d ? jj : d - 1);
-                    }
-                    normal_from_u32_x4(y4, x4);
-#pragma unroll
-                    for (int i = 0; i < 4; ++i) {
-                        const int jj = 4 * (f + i) + r4;
-                        a4[i] = (jj < d && !(COND == kX1 && jj == 0)) ? x4[i] : 0.0;
-                    }
-#pragma unroll
-                    for (int jt = 0; jt < JT; ++jt) {
-                        const double* Mrow = P.M + (size_t)(8 * jt + q) * DP + r4 + 4 * f;
-#pragma unroll
-                        for (int i = 0; i < 4; ++i) {
-                            const double b = __ldg(Mrow + 4 * i);
-                            asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
-                                         : "+d"(cv[2 * jt]), "+d"(cv[2 * jt + 1])
-                                         : "d"(a4[i]), "d"(b));
-                        }
-                    }
-                }
-            } else
 #pragma unroll 1
             for (int f = 0; f < KF; f += 2) {
                 const int ja = 4 * f + r4, jb = 4 * (f + 1) + r4;
@@ -286,15 +273,21 @@ __global__ void __launch_bounds__(128, pca_min_blocks<COND, KF, LB>()) pca_kerne
                         cst[(size_t)v * tpb] = cv[v];
                     }
                 }
-#define CV(v) (kSmemC ? cst[(size_t)(v) * tpb] : cv[(v)])
-                if (LB) {
+#define CV(v)                                                                                        \
+    (kSmemC ? cst[(size_t)(v) * tpb]                                                                     \
+            : kLbRolled ? ((8 * ((v) >> 1) + 2 * r4 + ((v) & 1)) < d                                     \
+                               ? stage[(size_t)(8 * ((v) >> 1) + 2 * r4 + ((v) & 1)) * kSS + 8 * rt + q] \
+                               : 0.0)                                                                    \
+                        : cv[(v)])
+                if (LB && !kLbQuad) {
                     double* sw = stage + 8 * rt + q;
+                    constexpr int SS = kSS;
 #pragma unroll
                     for (int jt = 0; jt < JT; ++jt) {
                         const int j0 = 8 * jt + 2 * r4;
-                        if (j0 < d) QMCCPW_CHK_SMEM(&sw[j0 * 32]);
-                        if (j0 < d) sw[j0 * 32] = cv[2 * jt];
-                        if (j0 + 1 < d) sw[(j0 + 1) * 32] = cv[2 * jt + 1];
+                        if (j0 < d) QMCCPW_CHK_SMEM(&sw[j0 * SS]);
+                        if (j0 < d) sw[j0 * SS] = cv[2 * jt];
+                        if (j0 + 1 < d) sw[(j0 + 1) * SS] = cv[2 * jt + 1];
                     }
                 }
                 double f[kMaxOpt][4];
@@ -400,15 +393,32 @@ __global__ void __launch_bounds__(128, pca_min_blocks<COND, KF, LB>()) pca_kerne
                     for (int o2 = 0; o2 < kMaxOpt; ++o2)
                         if (o2 < P.n_opt && P.tail_leader[o2] == o) x1_outputs(P, o2, xs, f[o2]);
                 }
+                if (kLbQuad) {
+                    const double* cbase = stage_base + (tid & ~3);
+                    auto cq = [&](int v, int L) { return cbase[(size_t)v * tpb + L]; };
+#pragma unroll 1
+                    for (int o = 0; o < kMaxOpt; ++o) {
+                        if (o >= P.n_opt) break;
+                        if (P.type[o] != kLookback) continue;
+                        double fl[4];
+                        x1_lookback_quad<2 * JT>(P, o, r4, cq, fl);
+                        // f[o] = fl through selects (no dynamic register indexing)
+#pragma unroll
+                        for (int o3 = 0; o3 < kMaxOpt; ++o3)
+                            if (o3 == o)
+#pragma unroll
+                                for (int qq = 0; qq < 4; ++qq) f[o3][qq] = fl[qq];
+                    }
+                }
                 if (r4 == 0 && valid) {  // one lane per path records it
                     ++npts;
                     if (P.path_out != nullptr) {
 #pragma unroll
                         for (int o = 0; o < kMaxOpt; ++o)
-                            if (o == P.hook_option && P.type[o] != kLookback)
+                            if (o == P.hook_option && (kLbQuad || P.type[o] != kLookback))
                                 for (int qq = 0; qq < 4; ++qq) P.path_out[ip * 4 + qq] = f[o][qq];
                     }
-                    if (!kSmemC) {
+                    if (!kSmemC && !kLbRolled) {
 #pragma unroll
                         for (int o = 0; o < kMaxOpt; ++o) {
                             if (o < P.n_opt && P.type[o] != kLookback) {
@@ -425,11 +435,13 @@ __global__ void __launch_bounds__(128, pca_min_blocks<COND, KF, LB>()) pca_kerne
                     }
                 }
                 // the quad's four lanes hold the same f: lane r4 = 0 contributes each path once
-                if (kSmemC) warp_slot_sums(f, P, valid && r4 == 0, lane, wacc + (tid >> 5) * 32);
+                if (kSmemC || kLbRolled)
+                    warp_slot_sums(f, P, valid && r4 == 0, lane, wacc + (tid >> 5) * 32,
+                                   /*skip_lookback=*/LB && !kLbQuad);
             }
         }
 #undef CV
-        if (COND == kX1 && LB) {
+        if (COND == kX1 && LB && !kLbQuad) {
             // lookback options: lane L walks the envelope of path wbase + L from the staged c_j
             __syncwarp();
             const int tp = wbase + lane;
@@ -440,13 +452,15 @@ __global__ void __launch_bounds__(128, pca_min_blocks<COND, KF, LB>()) pca_kerne
                 if (P.type[o] != kLookback) continue;
                 double fl[4];
                 if (QMCCPW_LB_SMEM)
-                    x1_lookback(P, o, stage + lane, 32, fl, X1Slopes{sl_b, sl_isa},
+                    x1_lookback(P, o, stage + lane, kSS, fl, X1Slopes{sl_b, sl_isa},
                                 QMCCPW_LB_HULL ? hull_w + lane : nullptr, 32);
                 else
-                    x1_lookback(P, o, stage + lane, 32, fl);
-                if (valid) {
-                    if (P.path_out != nullptr && o == P.hook_option)
-                        for (int qq = 0; qq < 4; ++qq) P.path_out[ip * 4 + qq] = fl[qq];
+                    x1_lookback(P, o, stage + lane, kSS, fl);
+                if (valid && P.path_out != nullptr && o == P.hook_option)
+                    for (int qq = 0; qq < 4; ++qq) P.path_out[ip * 4 + qq] = fl[qq];
+                if (kLbRolled) {
+                    warp_slot_sums_one(fl, P.piv[o], valid, lane, wacc + (tid >> 5) * 32 + o * 8);
+                } else if (valid) {
 #pragma unroll
                     for (int qq = 0; qq < 4; ++qq) {
                         const double y = fl[qq] - P.piv[o][qq];
@@ -477,17 +491,19 @@ __global__ void __launch_bounds__(128, pca_min_blocks<COND, KF, LB>()) pca_kerne
         }
     }
     if (COND == kW1 && !kWarpSum) acc2_to_wacc(P, acc2, wacc, tpb, tid);
-    block_epilogue(P, (COND == kX1 && !kSmemC) ? accs : nullptr, wacc, red, n_acc, tpb, tid, cell, unconverged, ties,
+    block_epilogue(P, (COND == kX1 && !kWarpSum) ? accs : nullptr, wacc, red, n_acc, tpb, tid, cell, unconverged, ties,
                    npts);
 }
 
 static size_t pca_smem_bytes(const PathArgs& a, bool lb, int cond) {
     const size_t tpb = (size_t)1 << a.tpb_log2;
-    const bool smemc = cond == kX1 && !lb && QMCCPW_PCA_X1_SMEMC;
-    const bool warpsum = (cond == kW1 && QMCCPW_PCA_WARPSUM) || smemc;
+    const bool lbquad = cond == kX1 && lb && QMCCPW_LB_QUAD && QMCCPW_PCA_X1_SMEMC;
+    const bool smemc = cond == kX1 && (!lb || lbquad) && QMCCPW_PCA_X1_SMEMC;
+    lb = lb && !lbquad;  // no per-warp staging
+    const bool warpsum = (cond == kW1 && QMCCPW_PCA_WARPSUM) || smemc || (cond == kX1 && lb && QMCCPW_LB_ROLLED);
     size_t b = pca_stage_offset(warpsum ? 0 : a.n_opt * 8, a.d, (int)tpb);
     if (smemc) b += (size_t)(a.M_ld / 4) * tpb * sizeof(double);  // c_j [2 JT][tpb]
-    if (lb) b += tpb * a.d * sizeof(double);  // [nw][d][32] staging
+    if (lb) b += tpb * a.d * sizeof(double) * (QMCCPW_LB_ROLLED ? 36 : 32) / 32;  // [nw][d][kSS] staging
     if (lb && QMCCPW_LB_SMEM) b += 2 * a.d * sizeof(double) + (QMCCPW_LB_HULL ? tpb * a.d : 0);  // slopes, hulls
     return b;
 }
