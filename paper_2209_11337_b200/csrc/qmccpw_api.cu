@@ -22,6 +22,10 @@
 
 using namespace qmccpw;
 
+#ifndef QMCCPW_BB_X1_MMA
+#define QMCCPW_BB_X1_MMA 1
+#endif
+
 namespace {
 
 thread_local std::string g_last_error;
@@ -368,6 +372,15 @@ int carve(const Plan& pl, bool own_partials, uint32_t table_reps, Scratch* s, St
     return QMCCPW_OK;
 }
 
+// BB-X1 without a lookback at d <= 128 runs on the PCA kernel's quad layout with the bridge's
+// matrix (launch_paths): Alg. 4 as W = M x on the FP64 tensor cores
+bool bb_x1_on_mma(const Plan& pl) {
+    bool lookback = false;
+    for (int o = 0; o < pl.n_opt; ++o) lookback |= pl.types[o] == QMCCPW_LOOKBACK_CALL;
+    return QMCCPW_BB_X1_MMA && pl.cfg.method == QMCCPW_QMC_CPW && pl.cfg.construction == QMCCPW_BB &&
+           pl.cfg.conditioning == QMCCPW_COND_X1 && !lookback && pl.d <= 128 && !pl.portfolio;
+}
+
 int build_tables(DeviceCache* c, const Plan& pl, uint32_t rep_base, uint32_t table_reps, const Scratch& s,
                  cudaStream_t st) {
     const qmccpw_config& cfg = pl.cfg;
@@ -389,7 +402,8 @@ int build_tables(DeviceCache* c, const Plan& pl, uint32_t rep_base, uint32_t tab
     if (cfg.method == QMCCPW_QMC_CPW && (cfg.construction == QMCCPW_PCA || cfg.conditioning == QMCCPW_COND_X1))
         CUDA_TRY(launch_path_matrix(cfg.construction, pl.d, (pl.d + 7) & ~7, pl.portfolio ? 1.0 : pl.p[0].T,
                                     pl.p[0].sigma,
-                                    cfg.construction == QMCCPW_PCA ? s.M : nullptr, s.a, s.inv_sa, st));
+                                    (cfg.construction == QMCCPW_PCA || bb_x1_on_mma(pl)) ? s.M : nullptr, s.a,
+                                    s.inv_sa, st));
     if (cfg.method == QMCCPW_QMC_CPW && pl.gpca) {
         const qmccpw_params& q = pl.p[0];
         CUDA_TRY(launch_gpca_rotate(s.M, (pl.d + 7) & ~7, pl.d, q.T, q.r - 0.5 * q.sigma * q.sigma, q.sigma, s.a,

@@ -640,6 +640,16 @@ __device__ __forceinline__ void x1_lookback(const PathArgs& P, int o, const doub
     f[3] = D * K * ph / (S0 * S0 * sg * __ldg(P.a + j0));
 }
 
+// sum / min over the four lanes of a quad (lanes 4q .. 4q + 3)
+__device__ __forceinline__ double quad_sum(double v) {
+    v += __shfl_xor_sync(0xffffffffu, v, 1);
+    return v + __shfl_xor_sync(0xffffffffu, v, 2);
+}
+__device__ __forceinline__ double quad_min(double v) {
+    v = fmin(v, __shfl_xor_sync(0xffffffffu, v, 1));
+    return fmin(v, __shfl_xor_sync(0xffffffffu, v, 2));
+}
+
 // Lookback under X1 over a quad (the PCA kernel's layout: lane r4 holds the path's lines
 // j = 8 jt + 2 r4 + e, e = 0, 1, at slot v = 2 jt + e; cq(v, lane_r4) returns c_j of slot v held
 // by quad lane lane_r4).  The same envelope integral as x1_lookback, built by gift wrapping
@@ -707,7 +717,31 @@ __device__ __forceinline__ void x1_lookback_quad(const PathArgs& P, int o, int r
     }
     // the quads of a warp finish after different segment counts, and the loop shuffles with a
     // full mask: it runs until every quad is done (warp-uniform exit), finished quads idle
+    // The segment integrals are dealt round-robin over the quad: segment s of the walk is kept
+    // by lane s mod 4 and every fourth iteration each lane integrates the one it holds, so a
+    // round of four segments costs one integral instead of four; J and V are quad-summed.
     bool done = false;
+    int it = 0, p_act = -1;
+    double p_lo = 0.0, p_hi = 0.0;
+    bool p_last = false;
+    auto integrate = [&]() {
+        if (p_act >= 0) {
+            const double ba = sg * __ldg(P.a + p_act), ca = cj(p_act);
+            const double aa = ba / sg;
+            const double tj = (double)(p_act + 1) * P.t1;
+            const double Rj = (ca - P.lnS0 - P.omega * tj) * P.inv_sigma;
+            const double w = fast_exp(fma(0.5 * ba, ba, ca));
+            double Qlo, Qhi, plo, phi_hi;
+            phibar_phi_x2(p_lo - ba, p_last ? 0.0 : p_hi - ba, Qlo, Qhi, plo, phi_hi);
+            if (p_last) {
+                Qhi = 0.0;
+                phi_hi = 0.0;
+            }
+            J = fma(w, Qlo - Qhi, J);
+            V = fma(w, (Rj - sg * tj + sg * aa * aa) * (Qlo - Qhi) + aa * (plo - phi_hi), V);
+            p_act = -1;
+        }
+    };
 #pragma unroll 1
     for (;;) {
         if (!__any_sync(0xffffffffu, !done)) break;
@@ -751,28 +785,28 @@ __device__ __forceinline__ void x1_lookback_quad(const PathArgs& P, int o, int r
                 }
             }
         }
-        if (done) continue;
-        double hi = kb >= 0 ? Nb / Db : CUDART_INF;
-        hi = fmax(hi, lo);
-        const double aa = ba / sg;
-        const double tj = (double)(act + 1) * P.t1;
-        const double Rj = (ca - P.lnS0 - P.omega * tj) * P.inv_sigma;
-        const double w = fast_exp(fma(0.5 * ba, ba, ca));
-        double Qlo, Qhi, plo, phi_hi;
-        phibar_phi_x2(lo - ba, (kb < 0) ? 0.0 : hi - ba, Qlo, Qhi, plo, phi_hi);
-        if (kb < 0) {
-            Qhi = 0.0;
-            phi_hi = 0.0;
+        if (!done) {
+            double hi = kb >= 0 ? Nb / Db : CUDART_INF;
+            hi = fmax(hi, lo);
+            if ((it & 3) == r4) {  // every live quad is at segment it of its walk
+                p_act = act;
+                p_lo = lo;
+                p_hi = hi;
+                p_last = kb < 0;
+            }
+            if (kb < 0) {
+                done = true;
+            } else {
+                act = kb;
+                lo = hi;
+            }
         }
-        J = fma(w, Qlo - Qhi, J);
-        V = fma(w, (Rj - sg * tj + sg * aa * aa) * (Qlo - Qhi) + aa * (plo - phi_hi), V);
-        if (kb < 0) {
-            done = true;
-        } else {
-            act = kb;
-            lo = hi;
-        }
+        if ((it & 3) == 3) integrate();  // warp-uniform: it is the iteration count
+        ++it;
     }
+    integrate();
+    J = quad_sum(J);
+    V = quad_sum(V);
     const double D = P.Dfac, S0 = P.S0, K = P.K[o];
     double Qu, Q2, ph, ph2;
     phibar_phi_x2(ust, ust, Qu, Q2, ph, ph2);
@@ -964,13 +998,5 @@ __device__ __forceinline__ void block_epilogue(const PathArgs& P, const double* 
     }
 }
 
-__device__ __forceinline__ double quad_sum(double v) {
-    v += __shfl_xor_sync(0xffffffffu, v, 1);
-    return v + __shfl_xor_sync(0xffffffffu, v, 2);
-}
-__device__ __forceinline__ double quad_min(double v) {
-    v = fmin(v, __shfl_xor_sync(0xffffffffu, v, 1));
-    return fmin(v, __shfl_xor_sync(0xffffffffu, v, 2));
-}
 
 }  // namespace qmccpw

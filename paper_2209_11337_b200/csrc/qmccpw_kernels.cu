@@ -96,6 +96,30 @@ __global__ void path_matrix_kernel(int construction, int d, int ld, double T, do
         const double s = sinpi((double)num / (double)den);
         M[idx] = sqrt(dt / (4.0 * sh * sh)) * sqrt(4.0 / (double)den) * s;
     }
+    if (construction == kBB && M != nullptr && idx < ld * ld) {
+        // Alg. 4 as a matrix (the Levy-Ciesielski form of the bridge): Sobol' dimension 0 is the
+        // terminal, W_j gains t_j / sqrt(T) x_0; dimension k >= 1 is the midpoint of interval
+        // jj = 2^lev - 1 - k at level lev (2^lev <= 2k + 1 < 2^(lev+1)), mid = (2 jj + 1) 2^c,
+        // c = m - lev, and W_j gains b_lev x_k times the hat max(0, 1 - |j - mid| / 2^c)
+        const int j = idx / ld + 1, k = idx % ld;
+        double v = 0.0;
+        if (j <= d && k < d) {
+            if (k == 0) {
+                v = (double)j * dt / sqrt(T);
+            } else {
+                int m = 0;
+                while ((1 << m) < d) ++m;
+                int lev = 0;
+                while ((2 << lev) <= k) ++lev;  // 2^lev <= k < 2^(lev+1)
+                ++lev;                            // levels are 1-based: dimension 1 is level 1
+                const int jj = (1 << lev) - 1 - k, c = m - lev;
+                const int mid = (2 * jj + 1) << c, half = 1 << c;
+                const int dist = j > mid ? j - mid : mid - j;
+                if (dist < half) v = sqrt(T / ldexp(1.0, lev + 1)) * (1.0 - (double)dist / (double)half);
+            }
+        }
+        M[idx] = v;
+    }
     if (idx < d) {
         const int j = idx + 1;
         double aj;
@@ -115,7 +139,7 @@ __global__ void path_matrix_kernel(int construction, int d, int ld, double T, do
 
 cudaError_t launch_path_matrix(int construction, int d, int ld, double T, double sigma, double* d_M, double* d_a,
                                double* d_inv_sa, cudaStream_t st) {
-    const int n = (construction == kPca && d_M) ? (ld * ld > d ? ld * ld : d) : d;
+    const int n = ((construction == kPca || construction == kBB) && d_M) ? (ld * ld > d ? ld * ld : d) : d;
     const int tpb = 256;
     path_matrix_kernel<<<(n + tpb - 1) / tpb, tpb, 0, st>>>(construction, d, ld, T, sigma, d_M, d_a, d_inv_sa);
     ++launch_counter();

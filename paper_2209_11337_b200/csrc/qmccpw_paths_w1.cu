@@ -3,6 +3,10 @@
 #define QMCCPW_SMEM_TABLES 1  // exp / log tables in shared memory (see qmccpw_math.cuh)
 #include "qmccpw_paths.cuh"
 
+#ifndef QMCCPW_BB_X1_MMA
+#define QMCCPW_BB_X1_MMA 1
+#endif
+
 namespace qmccpw {
 
 cudaError_t launch_paths(const PathArgs& args, int construction, int conditioning, int method, cudaStream_t st,
@@ -12,8 +16,9 @@ cudaError_t launch_paths(const PathArgs& args, int construction, int conditionin
                                                   : launch_paths_t<kStd, kW1, kMc, false>(args, st, smem_out);
     if (method == kMcAv) return construction == kBB ? launch_paths_t<kBB, kW1, kMcAv, false>(args, st, smem_out)
                                                     : launch_paths_t<kStd, kW1, kMcAv, false>(args, st, smem_out);
-    if (construction == kPca && method == kQmc) {
-        // fragment-native tensor-core path for d <= 128
+    if (method == kQmc && (construction == kPca ||
+                           (construction == kBB && conditioning == kX1 && !args.has_lookback && QMCCPW_BB_X1_MMA))) {
+        // fragment-native tensor-core path for d <= 128 (BB-X1: the bridge's matrix, qmccpw_api.cu)
         bool handled = false;
         cudaError_t e = conditioning == kW1 ? launch_pca_w1(args, st, &handled) : launch_pca_x1(args, st, &handled);
         if (handled) return e;
