@@ -25,6 +25,9 @@ using namespace qmccpw;
 #ifndef QMCCPW_BB_X1_MMA
 #define QMCCPW_BB_X1_MMA 1
 #endif
+#ifndef QMCCPW_STD_X1_MMA
+#define QMCCPW_STD_X1_MMA 0  // measured slower: C4 STD-X1 57.9 ms on the path kernel, 66.2 on the quad kernel
+#endif
 
 namespace {
 
@@ -372,13 +375,15 @@ int carve(const Plan& pl, bool own_partials, uint32_t table_reps, Scratch* s, St
     return QMCCPW_OK;
 }
 
-// BB-X1 without a lookback at d <= 128 runs on the PCA kernel's quad layout with the bridge's
-// matrix (launch_paths): Alg. 4 as W = M x on the FP64 tensor cores
+// BB-X1 and STD-X1 without a lookback at d <= 128 run on the PCA kernel's quad layout with the
+// construction's matrix (launch_paths): Alg. 4 / Alg. 3 as W = M x on the FP64 tensor cores
 bool bb_x1_on_mma(const Plan& pl) {
     bool lookback = false;
     for (int o = 0; o < pl.n_opt; ++o) lookback |= pl.types[o] == QMCCPW_LOOKBACK_CALL;
-    return QMCCPW_BB_X1_MMA && pl.cfg.method == QMCCPW_QMC_CPW && pl.cfg.construction == QMCCPW_BB &&
-           pl.cfg.conditioning == QMCCPW_COND_X1 && !lookback && pl.d <= 128 && !pl.portfolio;
+    const bool constr = (pl.cfg.construction == QMCCPW_BB && QMCCPW_BB_X1_MMA) ||
+                        (pl.cfg.construction == QMCCPW_STD && QMCCPW_STD_X1_MMA);
+    return constr && pl.cfg.method == QMCCPW_QMC_CPW && pl.cfg.conditioning == QMCCPW_COND_X1 && !lookback &&
+           pl.d <= 128 && !pl.portfolio;
 }
 
 int build_tables(DeviceCache* c, const Plan& pl, uint32_t rep_base, uint32_t table_reps, const Scratch& s,

@@ -362,18 +362,43 @@ __device__ __forceinline__ X1Sums x1_solve(const PathArgs& P, int o, bool arith,
     if (P.a[0] == P.a[d - 1]) {
         // equal slopes (STD): S(u) = e^{sigma a u} sum_j e^{c_j}, so the threshold is closed-form,
         // u* = (ln(d K) - ln sum_j e^{c_j}) / (sigma a) -- no iteration
-        double S = 0.0;
+        // ... and every final sum factors through S = sum_j e^{c_j}, S_R = sum e^{c_j} R_j and
+        // S_t = sum e^{c_j} t_j (E_j = g e^{c_j}, g = e^{sigma a u}; w_j = h e^{c_j}, h = e^{sigma^2 a^2/2};
+        // one common Phibar(u - sigma a)): one pass of exponentials for threshold and payoff
+        double S = 0.0, SR = 0.0, St = 0.0;
         int j = 0;
 #pragma unroll 1
         for (; j + 1 < d; j += 2) {
+            const double ca = cb[j * stride], cbb = cb[(j + 1) * stride];
+            const double ta = (double)(j + 1) * P.t1, tb = (double)(j + 2) * P.t1;
             double Ea, Eb;
-            fast_exp_x2(cb[j * stride], cb[(j + 1) * stride], Ea, Eb);
+            fast_exp_x2(ca, cbb, Ea, Eb);
             S += Ea;
+            SR = fma(Ea, (ca - P.lnS0 - P.omega * ta) * P.inv_sigma, SR);
+            St = fma(Ea, ta, St);
             S += Eb;
+            SR = fma(Eb, (cbb - P.lnS0 - P.omega * tb) * P.inv_sigma, SR);
+            St = fma(Eb, tb, St);
         }
-        if (j < d) S += fast_exp(cb[j * stride]);
-        u = fmin((lndK - fast_log(S)) / (sg * P.a[0]), u_hi);
-        conv = true;
+        if (j < d) {
+            const double ca = cb[j * stride], ta = (double)(j + 1) * P.t1;
+            const double Ea = fast_exp(ca);
+            S += Ea;
+            SR = fma(Ea, (ca - P.lnS0 - P.omega * ta) * P.inv_sigma, SR);
+            St = fma(Ea, ta, St);
+        }
+        const double a = P.a[0];
+        u = fmin((lndK - fast_log(S)) / (sg * a), u_hi);
+        double g, h;
+        fast_exp_x2(sg * a * u, 0.5 * sg * sg * a * a, g, h);
+        double sumW = 0.0, sumWv = 0.0;
+        if (arith) {
+            double Pf, Q2, p1, p2;
+            phibar_phi_x2(u - sg * a, u - sg * a, Pf, Q2, p1, p2);
+            sumW = h * Pf * S;
+            sumWv = h * Pf * (SR - sg * St + sg * a * a * S);
+        }
+        return X1Sums{u, a * g * S, a * a * g * S, g * (SR - sg * St + a * u * S), sumW, sumWv};
     } else
     for (int it = 0; it < kNewtonMax; ++it) {
         double S = 0.0, SA = 0.0, SAA = 0.0;
@@ -717,31 +742,11 @@ __device__ __forceinline__ void x1_lookback_quad(const PathArgs& P, int o, int r
     }
     // the quads of a warp finish after different segment counts, and the loop shuffles with a
     // full mask: it runs until every quad is done (warp-uniform exit), finished quads idle
-    // The segment integrals are dealt round-robin over the quad: segment s of the walk is kept
-    // by lane s mod 4 and every fourth iteration each lane integrates the one it holds, so a
-    // round of four segments costs one integral instead of four; J and V are quad-summed.
+    // the quads of a warp finish after different segment counts, and the loop shuffles with a
+    // full mask: it runs until every quad is done (warp-uniform exit), finished quads idle.
+    // (Dealing the segment integrals round-robin over the quad measured slower: 192.4 -> 198.1
+    // ms for C4 PCA-X1 with the lookback, register pressure.)
     bool done = false;
-    int it = 0, p_act = -1;
-    double p_lo = 0.0, p_hi = 0.0;
-    bool p_last = false;
-    auto integrate = [&]() {
-        if (p_act >= 0) {
-            const double ba = sg * __ldg(P.a + p_act), ca = cj(p_act);
-            const double aa = ba / sg;
-            const double tj = (double)(p_act + 1) * P.t1;
-            const double Rj = (ca - P.lnS0 - P.omega * tj) * P.inv_sigma;
-            const double w = fast_exp(fma(0.5 * ba, ba, ca));
-            double Qlo, Qhi, plo, phi_hi;
-            phibar_phi_x2(p_lo - ba, p_last ? 0.0 : p_hi - ba, Qlo, Qhi, plo, phi_hi);
-            if (p_last) {
-                Qhi = 0.0;
-                phi_hi = 0.0;
-            }
-            J = fma(w, Qlo - Qhi, J);
-            V = fma(w, (Rj - sg * tj + sg * aa * aa) * (Qlo - Qhi) + aa * (plo - phi_hi), V);
-            p_act = -1;
-        }
-    };
 #pragma unroll 1
     for (;;) {
         if (!__any_sync(0xffffffffu, !done)) break;
@@ -785,28 +790,28 @@ __device__ __forceinline__ void x1_lookback_quad(const PathArgs& P, int o, int r
                 }
             }
         }
-        if (!done) {
-            double hi = kb >= 0 ? Nb / Db : CUDART_INF;
-            hi = fmax(hi, lo);
-            if ((it & 3) == r4) {  // every live quad is at segment it of its walk
-                p_act = act;
-                p_lo = lo;
-                p_hi = hi;
-                p_last = kb < 0;
-            }
-            if (kb < 0) {
-                done = true;
-            } else {
-                act = kb;
-                lo = hi;
-            }
+        if (done) continue;
+        double hi = kb >= 0 ? Nb / Db : CUDART_INF;
+        hi = fmax(hi, lo);
+        const double aa = ba / sg;
+        const double tj = (double)(act + 1) * P.t1;
+        const double Rj = (ca - P.lnS0 - P.omega * tj) * P.inv_sigma;
+        const double w = fast_exp(fma(0.5 * ba, ba, ca));
+        double Qlo, Qhi, plo, phi_hi;
+        phibar_phi_x2(lo - ba, (kb < 0) ? 0.0 : hi - ba, Qlo, Qhi, plo, phi_hi);
+        if (kb < 0) {
+            Qhi = 0.0;
+            phi_hi = 0.0;
         }
-        if ((it & 3) == 3) integrate();  // warp-uniform: it is the iteration count
-        ++it;
+        J = fma(w, Qlo - Qhi, J);
+        V = fma(w, (Rj - sg * tj + sg * aa * aa) * (Qlo - Qhi) + aa * (plo - phi_hi), V);
+        if (kb < 0) {
+            done = true;
+        } else {
+            act = kb;
+            lo = hi;
+        }
     }
-    integrate();
-    J = quad_sum(J);
-    V = quad_sum(V);
     const double D = P.Dfac, S0 = P.S0, K = P.K[o];
     double Qu, Q2, ph, ph2;
     phibar_phi_x2(ust, ust, Qu, Q2, ph, ph2);

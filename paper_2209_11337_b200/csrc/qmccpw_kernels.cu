@@ -96,6 +96,11 @@ __global__ void path_matrix_kernel(int construction, int d, int ld, double T, do
         const double s = sinpi((double)num / (double)den);
         M[idx] = sqrt(dt / (4.0 * sh * sh)) * sqrt(4.0 / (double)den) * s;
     }
+    if (construction == kStd && M != nullptr && idx < ld * ld) {
+        // Alg. 3 as a matrix: W(t_j) = sqrt(dt) (x_1 + ... + x_j), Sobol' dimension k -> x_{k+1}
+        const int j = idx / ld + 1, k = idx % ld;
+        M[idx] = (j <= d && k < j) ? sqrt(dt) : 0.0;
+    }
     if (construction == kBB && M != nullptr && idx < ld * ld) {
         // Alg. 4 as a matrix (the Levy-Ciesielski form of the bridge): Sobol' dimension 0 is the
         // terminal, W_j gains t_j / sqrt(T) x_0; dimension k >= 1 is the midpoint of interval
@@ -139,7 +144,7 @@ __global__ void path_matrix_kernel(int construction, int d, int ld, double T, do
 
 cudaError_t launch_path_matrix(int construction, int d, int ld, double T, double sigma, double* d_M, double* d_a,
                                double* d_inv_sa, cudaStream_t st) {
-    const int n = ((construction == kPca || construction == kBB) && d_M) ? (ld * ld > d ? ld * ld : d) : d;
+    const int n = d_M ? (ld * ld > d ? ld * ld : d) : d;
     const int tpb = 256;
     path_matrix_kernel<<<(n + tpb - 1) / tpb, tpb, 0, st>>>(construction, d, ld, T, sigma, d_M, d_a, d_inv_sa);
     ++launch_counter();

@@ -6,6 +6,9 @@
 #ifndef QMCCPW_BB_X1_MMA
 #define QMCCPW_BB_X1_MMA 1
 #endif
+#ifndef QMCCPW_STD_X1_MMA
+#define QMCCPW_STD_X1_MMA 0  // measured slower: C4 STD-X1 57.9 ms on the path kernel, 66.2 on the quad kernel
+#endif
 
 namespace qmccpw {
 
@@ -17,7 +20,8 @@ cudaError_t launch_paths(const PathArgs& args, int construction, int conditionin
     if (method == kMcAv) return construction == kBB ? launch_paths_t<kBB, kW1, kMcAv, false>(args, st, smem_out)
                                                     : launch_paths_t<kStd, kW1, kMcAv, false>(args, st, smem_out);
     if (method == kQmc && (construction == kPca ||
-                           (construction == kBB && conditioning == kX1 && !args.has_lookback && QMCCPW_BB_X1_MMA))) {
+                           (conditioning == kX1 && !args.has_lookback &&
+                            ((construction == kBB && QMCCPW_BB_X1_MMA) || (construction == kStd && QMCCPW_STD_X1_MMA))))) {
         // fragment-native tensor-core path for d <= 128 (BB-X1: the bridge's matrix, qmccpw_api.cu)
         bool handled = false;
         cudaError_t e = conditioning == kW1 ? launch_pca_w1(args, st, &handled) : launch_pca_x1(args, st, &handled);

@@ -317,6 +317,7 @@ __global__ void __launch_bounds__(128, pca_min_blocks<COND, KF, LB>()) pca_kerne
                     sumc = quad_sum(sumc);
                     double u = fmin(uhi, (lnK - sumc / d) / (sg * P.mean_a));
                     bool conv = false;
+                    const bool need_arith = P.x1_need_arith[o] != 0;
 #pragma unroll 1
                     for (int it = 0; it < kNewtonMax; ++it) {
                         double S = 0.0, SA = 0.0, SAA = 0.0;
@@ -346,7 +347,6 @@ __global__ void __launch_bounds__(128, pca_min_blocks<COND, KF, LB>()) pca_kerne
                     }
                     if (r4 == 0 && valid && !conv) ++unconverged;
                     double Dst = 0.0, Qst = 0.0, Vst = 0.0, sumW = 0.0, sumWv = 0.0;
-                    const bool need_arith = P.x1_need_arith[o] != 0;
                     // arithmetic sums: w_j Phibar(x_j), x_j = u - sigma a_j, without a per-date phi:
                     // w_j phi(x_j) = phi(u) E_j, so it is phi(u) E_j R(x_j) for x_j >= 0 and
                     // w_j - phi(u) E_j R(-x_j) below (R the Mills ratio)
