@@ -530,44 +530,15 @@ __device__ __forceinline__ void x1_outputs(const PathArgs& P, int o, const X1Sum
 // b_j = sigma a_j; u* = min_j (ln K - c_j)/b_j in closed form; G integrates
 // exp(max_j l_j(u)) phi(u) over [u*, inf), walking the upper envelope from u*:
 // on each segment the next breakpoint is the first steeper line to overtake.
-// Slopes of the X1 lines b_j = sigma a_j and 1/(sigma a_j), either from the call's tables in
-// global memory or staged once per block in shared memory (x1_stage_slopes): the envelope walk
-// reloads them on every hull pop, and from shared memory a reload is one LDS instead of an
-// L1 round trip.
-struct X1Slopes {
-    const double* b;     // [d] sigma a_j (shared) or nullptr: sigma * P.a[j]
-    const double* isa;   // [d] 1/(sigma a_j) (shared) or nullptr: P.inv_sa[j]
-    __device__ __forceinline__ double bj(const PathArgs& P, int j) const {
-        return b != nullptr ? b[j] : P.sigma * __ldg(P.a + j);
-    }
-    __device__ __forceinline__ double isaj(const PathArgs& P, int j) const {
-        return isa != nullptr ? isa[j] : __ldg(P.inv_sa + j);
-    }
-};
-__device__ __forceinline__ void x1_stage_slopes(const PathArgs& P, double* b, double* isa, int tid, int tpb) {
-    for (int j = tid; j < P.d; j += tpb) {
-        QMCCPW_CHK_SMEM(&b[j]);
-        QMCCPW_CHK_SMEM(&isa[j]);
-        b[j] = P.sigma * __ldg(P.a + j);
-        isa[j] = __ldg(P.inv_sa + j);
-    }
-}
-
-// Lookback under X1 (next-row f1).  Lines l_j(u) = c_j + b_j u,
-// b_j = sigma a_j; u* = min_j (ln K - c_j)/b_j in closed form; G integrates
-// exp(max_j l_j(u)) phi(u) over [u*, inf), walking the upper envelope from u*:
-// on each segment the next breakpoint is the first steeper line to overtake.
-// hsm: the hull's line indices in shared memory (element k at hsm[k * hstride]), or nullptr
-// for a per-thread array.
-__device__ __forceinline__ void x1_lookback(const PathArgs& P, int o, const double* cb, int stride, double f[4],
-                                            const X1Slopes& sl = X1Slopes{nullptr, nullptr},
-                                            uint8_t* hsm = nullptr, int hstride = 1) {
+// (Slopes and hull in shared memory measured slower: bank conflicts of the divergent per-lane
+// reads, and 9 KB more per block cost the PCA variant an occupancy step.)
+__device__ __forceinline__ void x1_lookback(const PathArgs& P, int o, const double* cb, int stride, double f[4]) {
     const int d = P.d;
     const double sg = P.sigma, lnK = P.lnK[o];
     double ustar = CUDART_INF;
     int j0 = 0;
     for (int j = 0; j < d; ++j) {
-        const double uj = (lnK - cb[j * stride]) * sl.isaj(P, j);
+        const double uj = (lnK - cb[j * stride]) * __ldg(P.inv_sa + j);
         if (uj < ustar) {
             ustar = uj;
             j0 = j;
@@ -580,11 +551,9 @@ __device__ __forceinline__ void x1_lookback(const PathArgs& P, int o, const doub
     // than it overtakes its predecessor.  Equal slopes keep the higher line.  Only u >= u*
     // matters: there line j0 is the highest (c_j + b_j u* <= c_j + b_j u_j = ln K), and a
     // flatter line below it stays below, so the pass starts at j0.
-    uint8_t hull_local[kMaxDimGpu];  // line indices (d <= 256), unless the caller gives shared memory
-    uint8_t* hull = hsm != nullptr ? hsm : hull_local;
-    const int hs = hsm != nullptr ? hstride : 1;
+    uint8_t hull[kMaxDimGpu];  // line indices (d <= 256)
     int top = 0;
-    if (sl.bj(P, 0) == sl.bj(P, d - 1)) {  // STD: all slopes equal -> the single highest line (lowest j on ties)
+    if (__ldg(P.a) == __ldg(P.a + d - 1)) {  // STD: all slopes equal -> the single highest line (lowest j on ties)
         int best = 0;
         for (int j = 1; j < d; ++j) best = cb[j * stride] > cb[best * stride] ? j : best;
         hull[0] = (uint8_t)best;
@@ -593,15 +562,15 @@ __device__ __forceinline__ void x1_lookback(const PathArgs& P, int o, const doub
         // the top two hull lines (T = top, S = second) stay in registers; a pop reloads S
         double bT = 0.0, cT = 0.0, bS = 0.0, cS = 0.0;
         for (int j = j0; j < d; ++j) {
-            const double b3 = sl.bj(P, j), c3 = cb[j * stride];
+            const double b3 = sg * __ldg(P.a + j), c3 = cb[j * stride];
             if (top > 0 && bT == b3) {
                 if (c3 <= cT) continue;
                 --top;  // same slope, higher line: replaces the top
                 bT = bS;
                 cT = cS;
                 if (top >= 2) {
-                    const int l = hull[(top - 2) * hs];
-                    bS = sl.bj(P, l);
+                    const int l = hull[top - 2];
+                    bS = sg * __ldg(P.a + l);
                     cS = cb[l * stride];
                 }
             }
@@ -611,14 +580,13 @@ __device__ __forceinline__ void x1_lookback(const PathArgs& P, int o, const doub
                 bT = bS;
                 cT = cS;
                 if (top >= 2) {
-                    const int l = hull[(top - 2) * hs];
-                    bS = sl.bj(P, l);
+                    const int l = hull[top - 2];
+                    bS = sg * __ldg(P.a + l);
                     cS = cb[l * stride];
                 }
             }
             QMCCPW_CHECK(top < kMaxDimGpu);
-            hull[top * hs] = (uint8_t)j;
-            ++top;
+            hull[top++] = (uint8_t)j;
             bS = bT;
             cS = cT;
             bT = b3;
@@ -629,18 +597,18 @@ __device__ __forceinline__ void x1_lookback(const PathArgs& P, int o, const doub
     // dominates just after)
     int k = 0;
     while (k + 1 < top) {
-        const int l1 = hull[k * hs], l2 = hull[(k + 1) * hs];
-        const double x = (cb[l1 * stride] - cb[l2 * stride]) / (sl.bj(P, l2) - sl.bj(P, l1));
+        const int l1 = hull[k], l2 = hull[k + 1];
+        const double x = (cb[l1 * stride] - cb[l2 * stride]) / (sg * (__ldg(P.a + l2) - __ldg(P.a + l1)));
         if (x > ustar) break;
         ++k;
     }
     double J = 0.0, V = 0.0, lo = ustar;
     for (; k < top; ++k) {
-        const int act = hull[k * hs];
-        const double bact = sl.bj(P, act), cact = cb[act * stride];
-        const int nxt = (k + 1 < top) ? hull[(k + 1) * hs] : -1;
+        const int act = hull[k];
+        const double bact = sg * __ldg(P.a + act), cact = cb[act * stride];
+        const int nxt = (k + 1 < top) ? hull[k + 1] : -1;
         double hi = CUDART_INF;
-        if (nxt >= 0) hi = (cact - cb[nxt * stride]) / (sl.bj(P, nxt) - bact);
+        if (nxt >= 0) hi = (cact - cb[nxt * stride]) / (sg * __ldg(P.a + nxt) - bact);
         hi = fmax(hi, lo);
         const double aa = bact / sg;
         const double tj = (double)(act + 1) * P.t1;
@@ -823,14 +791,13 @@ __device__ __forceinline__ void x1_lookback_quad(const PathArgs& P, int o, int r
 
 // all options of the launch: one Newton solve (and one set of E*-sums) per distinct strike
 __device__ __forceinline__ void tail_x1_all(const PathArgs& P, const double* cb, int stride, double f[kMaxOpt][4],
-                                            unsigned& unconverged, const X1Slopes& sl = X1Slopes{nullptr, nullptr},
-                                            uint8_t* hsm = nullptr, int hstride = 1) {
+                                            unsigned& unconverged) {
     X1Sums xs[kMaxOpt];
 #pragma unroll
     for (int o = 0; o < kMaxOpt; ++o) {
         if (o >= P.n_opt) break;
         if (P.type[o] == kLookback) {
-            x1_lookback(P, o, cb, stride, f[o], sl, hsm, hstride);
+            x1_lookback(P, o, cb, stride, f[o]);
             xs[o] = X1Sums{0, 0, 0, 0, 0, 0};
             continue;
         }

@@ -53,18 +53,6 @@ constexpr int paths_min_blocks() {
            : (COND == kW1 && METHOD == kMcAv && CONSTR == kBB) ? QMCCPW_BBAV_MINB
                                                                 : 0;
 }
-// X1 lookback envelope staging (QMCCPW_LB_SMEM, see qmccpw_pca.cuh): defined here for both
-// kernels of this header
-#ifndef QMCCPW_LB_SMEM
-#define QMCCPW_LB_SMEM 0
-#endif
-#ifndef QMCCPW_LB_HULL
-#define QMCCPW_LB_HULL 0
-#endif
-static __host__ __device__ size_t path_smem_base_bytes(const PathArgs& a, int constr, int cond, int method);
-__host__ __device__ __forceinline__ size_t path_lb_offset(const PathArgs& a, int constr, int cond, int method) {
-    return (path_smem_base_bytes(a, constr, cond, method) + 7) & ~(size_t)7;
-}
 // OWEN: nested scrambling of the Sobol' coordinates (row f4) -- a template flag so
 // that the other randomisations pay nothing for it (measured 0.5-4 % as a runtime test)
 template <int CONSTR, int COND, int METHOD, bool OWEN>
@@ -103,12 +91,6 @@ __global__ void __launch_bounds__(128, paths_min_blocks<CONSTR, COND, METHOD>())
     double* red = reinterpret_cast<double*>(HW);
     const int hw_size = 2 * nw * d;
     uint32_t* BS = HW + 2 * hw_size;  // [d] incremental Gray bases (sobol_build_hw_inc)
-    // X1 with a lookback (QMCCPW_LB_SMEM): the slopes sigma a_j, 1/(sigma a_j) [d] and each
-    // thread's envelope hull [d][tpb] bytes after the HW / reduction region
-    constexpr bool kLbSmem = (COND == kX1) && (METHOD == kQmc) && QMCCPW_LB_SMEM;
-    double* sl_b = reinterpret_cast<double*>(smem_raw + path_lb_offset(P, CONSTR, COND, METHOD));
-    double* sl_isa = sl_b + d;
-    uint8_t* hull_t = reinterpret_cast<uint8_t*>(sl_isa + d) + tid;
 
     const uint64_t K0 = P.point_offset + i0;
     const uint64_t Ab = K0 >> tpb_log2;
@@ -120,7 +102,6 @@ __global__ void __launch_bounds__(128, paths_min_blocks<CONSTR, COND, METHOD>())
     // dimension lookup
     constexpr bool kPerm = (CONSTR == kBB && METHOD == kQmc);
     math_tables_load(tid, tpb);
-    if (kLbSmem && P.has_lookback) x1_stage_slopes(P, sl_b, sl_isa, tid, tpb);
     if (METHOD != kQmc) __syncthreads();  // QMC: the barrier below publishes the tables
     if (METHOD == kQmc) {
         const uint32_t* src = P.vscr + (size_t)rep_local * d * 32;
@@ -343,15 +324,10 @@ __global__ void __launch_bounds__(128, paths_min_blocks<CONSTR, COND, METHOD>())
                     const double W6 = fma(b1, x[4], 0.5 * (M4 + R));
                     const double W5 = fma(b0, x[5], 0.5 * (M4 + W6));
                     const double W7 = fma(b0, x[6], 0.5 * (W6 + R));
-#if QMCCPW_BB_PUSH4
-                    w1.push4(P, 8 * g, Wa - W1, M2 - W1, W3 - W1, M4 - W1);
-                    w1.push4(P, 8 * g + 4, W5 - W1, W6 - W1, W7 - W1, R - W1);
-#else
                     w1.push2(P, 8 * g, Wa - W1, M2 - W1);
                     w1.push2(P, 8 * g + 2, W3 - W1, M4 - W1);
                     w1.push2(P, 8 * g + 4, W5 - W1, W6 - W1);
                     w1.push2(P, 8 * g + 6, W7 - W1, R - W1);
-#endif
                     Wl = R;
                 }
             } else if (CONSTR == kBB) {
@@ -667,10 +643,7 @@ __global__ void __launch_bounds__(128, paths_min_blocks<CONSTR, COND, METHOD>())
                 __syncwarp();
 
             }
-            if (kLbSmem && P.has_lookback)
-                tail_x1_all(P, cb, tpb, f, unconverged, X1Slopes{sl_b, sl_isa}, QMCCPW_LB_HULL ? hull_t : nullptr, tpb);
-            else
-                tail_x1_all(P, cb, tpb, f, unconverged);
+            tail_x1_all(P, cb, tpb, f, unconverged);
         }
 
         if (!valid) {
@@ -696,14 +669,6 @@ __global__ void __launch_bounds__(128, paths_min_blocks<CONSTR, COND, METHOD>())
 
 
 static size_t path_smem_bytes(const PathArgs& a, int constr, int cond, int method) {
-    size_t b = path_smem_base_bytes(a, constr, cond, method);
-    if (QMCCPW_LB_SMEM && cond == kX1 && method == kQmc && a.has_lookback)
-        b = path_lb_offset(a, constr, cond, method) + 2 * (size_t)a.d * sizeof(double) +
-            (QMCCPW_LB_HULL ? ((size_t)1 << a.tpb_log2) * (size_t)a.d : 0);  // slopes, hulls
-    return b;
-}
-
-static __host__ __device__ size_t path_smem_base_bytes(const PathArgs& a, int constr, int cond, int method) {
     const size_t tpb = (size_t)1 << a.tpb_log2, nw = tpb / 32;
     const bool need_buf = method == kQmc && (constr == kPca || cond == kX1);
     const bool two_buf = method == kQmc && constr == kPca && cond == kX1;

@@ -40,9 +40,6 @@ namespace qmccpw {
 #ifndef QMCCPW_LB_MINB
 #define QMCCPW_LB_MINB 5
 #endif
-#ifndef QMCCPW_LB_ROLLED
-#define QMCCPW_LB_ROLLED 0
-#endif
 #ifndef QMCCPW_PCA_X1_SMEMC
 #define QMCCPW_PCA_X1_SMEMC 1
 #endif
@@ -66,19 +63,8 @@ __host__ __device__ __forceinline__ size_t pca_stage_offset(int n_acc, int d, in
     b += hw > red ? hw : red;
     return (b + 7) & ~(size_t)7;
 }
-// X1 lookback: the envelope walk reads the slopes from shared memory (QMCCPW_LB_SMEM, one LDS
-// per reload instead of an L1 load of P.a) and, with QMCCPW_LB_HULL, keeps each lane's hull in
-// shared memory instead of a per-thread local array.  A/B on one B200, C4 PCA-X1 with the
-// lookback (ms/step): global slopes + local hull 215.5; shared slopes 234.1; shared slopes and
-// hull 300.3 (the extra 9 KB per block drop the kernel from 2 blocks/SM to 1).  BB-X1 with the
-// lookback (paths kernel): 164.9 / 188.5 / 187.2.  Divergent per-lane slope reads conflict in
-// the shared-memory banks; through L1 they cost less -- both options stay off.
-#ifndef QMCCPW_LB_SMEM
-#define QMCCPW_LB_SMEM 0
-#endif
-#ifndef QMCCPW_LB_HULL
-#define QMCCPW_LB_HULL 0
-#endif
+// (X1 lookback with the per-lane hull: slopes and hulls in shared memory measured slower --
+// 215.5 -> 234.1 / 300.3 ms -- bank conflicts of divergent reads and an occupancy step; removed.)
 // LB (X1 only): the launch has a lookback option (staging + per-lane envelope walk)
 template <int COND, int KF, bool OWEN, bool LB>
 __global__ void __launch_bounds__(128, pca_min_blocks<COND, KF, LB>()) pca_kernel(const PathArgs P) {
@@ -101,13 +87,8 @@ __global__ void __launch_bounds__(128, pca_min_blocks<COND, KF, LB>()) pca_kerne
     // c_j stay in the quad layout (shared memory, as kSmemC), no per-warp [d][32] staging
     constexpr bool kLbQuad = COND == kX1 && LB && QMCCPW_LB_QUAD && QMCCPW_PCA_X1_SMEMC;
     constexpr bool kSmemC = COND == kX1 && (!LB || kLbQuad) && QMCCPW_PCA_X1_SMEMC;
-    // with a lookback (QMCCPW_LB_ROLLED) the per-strike passes read c_j from the lookback's
-    // per-warp staging instead (row stride kSS = 36 doubles: a quad's four dates fall in
-    // different bank pairs)
-    constexpr bool kLbRolled = COND == kX1 && LB && !kLbQuad && QMCCPW_LB_ROLLED;
-    constexpr int kSS = kLbRolled ? 36 : 32;
-    constexpr int kXU = (kSmemC || kLbRolled) ? 1 : 2 * JT;  // unroll of the X1 per-date loops
-    constexpr bool kWarpSum = (COND == kW1 && QMCCPW_PCA_WARPSUM) || kSmemC || kLbRolled;
+    constexpr int kXU = kSmemC ? 1 : 2 * JT;  // unroll of the X1 per-date loops
+    constexpr bool kWarpSum = (COND == kW1 && QMCCPW_PCA_WARPSUM) || kSmemC;
     const int n_acc_smem = kWarpSum ? 0 : n_acc;  // smem accumulator rows
     // per-path accumulators in smem: X1 as scalars (one quad lane per path), W1 as (S1, S2) pairs
     double* accs = reinterpret_cast<double*>(smem_raw);
@@ -123,12 +104,8 @@ __global__ void __launch_bounds__(128, pca_min_blocks<COND, KF, LB>()) pca_kerne
     // X1 with a lookback: c_j of the warp's 32 paths staged [d][32] per warp, so that each lane
     // walks the upper envelope of its own path (the quad layout holds a path over 4 lanes)
     double* stage_base = reinterpret_cast<double*>(smem_raw + pca_stage_offset(n_acc_smem, d, tpb));
-    double* stage = stage_base + (size_t)(tid >> 5) * d * kSS;
+    double* stage = stage_base + (size_t)(tid >> 5) * d * 32;
     double* cst = stage_base + tid;  // kSmemC: c_j of this lane at [v][tpb], v < 2 JT
-    // ... then the slopes sigma a_j, 1/(sigma a_j) [d] each and the lanes' hulls [nw][d][32] bytes
-    double* sl_b = stage_base + (size_t)tpb * d * kSS / 32;
-    double* sl_isa = sl_b + d;
-    uint8_t* hull_w = reinterpret_cast<uint8_t*>(sl_isa + d) + (size_t)(tid >> 5) * d * 32;
     const uint64_t K0 = P.point_offset + i0;
     const uint64_t Ab = K0 >> tpb_log2;
     {
@@ -143,7 +120,6 @@ __global__ void __launch_bounds__(128, pca_min_blocks<COND, KF, LB>()) pca_kerne
             QMCCPW_CHK_SMEM(&sh[idx]);
             sh[idx] = P.shift[(size_t)rep_local * d + idx];
         }
-        if (COND == kX1 && LB && QMCCPW_LB_SMEM) x1_stage_slopes(P, sl_b, sl_isa, tid, tpb);
         __syncthreads();
         sobol_build_g(vt, d, G, tid, tpb);
     }
@@ -273,15 +249,10 @@ __global__ void __launch_bounds__(128, pca_min_blocks<COND, KF, LB>()) pca_kerne
                         cst[(size_t)v * tpb] = cv[v];
                     }
                 }
-#define CV(v)                                                                                        \
-    (kSmemC ? cst[(size_t)(v) * tpb]                                                                     \
-            : kLbRolled ? ((8 * ((v) >> 1) + 2 * r4 + ((v) & 1)) < d                                     \
-                               ? stage[(size_t)(8 * ((v) >> 1) + 2 * r4 + ((v) & 1)) * kSS + 8 * rt + q] \
-                               : 0.0)                                                                    \
-                        : cv[(v)])
+#define CV(v) (kSmemC ? cst[(size_t)(v) * tpb] : cv[(v)])
                 if (LB && !kLbQuad) {
                     double* sw = stage + 8 * rt + q;
-                    constexpr int SS = kSS;
+                    constexpr int SS = 32;
 #pragma unroll
                     for (int jt = 0; jt < JT; ++jt) {
                         const int j0 = 8 * jt + 2 * r4;
@@ -418,7 +389,7 @@ __global__ void __launch_bounds__(128, pca_min_blocks<COND, KF, LB>()) pca_kerne
                             if (o == P.hook_option && (kLbQuad || P.type[o] != kLookback))
                                 for (int qq = 0; qq < 4; ++qq) P.path_out[ip * 4 + qq] = f[o][qq];
                     }
-                    if (!kSmemC && !kLbRolled) {
+                    if (!kSmemC) {
 #pragma unroll
                         for (int o = 0; o < kMaxOpt; ++o) {
                             if (o < P.n_opt && P.type[o] != kLookback) {
@@ -435,7 +406,7 @@ __global__ void __launch_bounds__(128, pca_min_blocks<COND, KF, LB>()) pca_kerne
                     }
                 }
                 // the quad's four lanes hold the same f: lane r4 = 0 contributes each path once
-                if (kSmemC || kLbRolled)
+                if (kSmemC)
                     warp_slot_sums(f, P, valid && r4 == 0, lane, wacc + (tid >> 5) * 32,
                                    /*skip_lookback=*/LB && !kLbQuad);
             }
@@ -451,16 +422,10 @@ __global__ void __launch_bounds__(128, pca_min_blocks<COND, KF, LB>()) pca_kerne
             for (int o = 0; o < P.n_opt; ++o) {
                 if (P.type[o] != kLookback) continue;
                 double fl[4];
-                if (QMCCPW_LB_SMEM)
-                    x1_lookback(P, o, stage + lane, kSS, fl, X1Slopes{sl_b, sl_isa},
-                                QMCCPW_LB_HULL ? hull_w + lane : nullptr, 32);
-                else
-                    x1_lookback(P, o, stage + lane, kSS, fl);
+                x1_lookback(P, o, stage + lane, 32, fl);
                 if (valid && P.path_out != nullptr && o == P.hook_option)
                     for (int qq = 0; qq < 4; ++qq) P.path_out[ip * 4 + qq] = fl[qq];
-                if (kLbRolled) {
-                    warp_slot_sums_one(fl, P.piv[o], valid, lane, wacc + (tid >> 5) * 32 + o * 8);
-                } else if (valid) {
+                if (valid) {
 #pragma unroll
                     for (int qq = 0; qq < 4; ++qq) {
                         const double y = fl[qq] - P.piv[o][qq];
@@ -500,11 +465,10 @@ static size_t pca_smem_bytes(const PathArgs& a, bool lb, int cond) {
     const bool lbquad = cond == kX1 && lb && QMCCPW_LB_QUAD && QMCCPW_PCA_X1_SMEMC;
     const bool smemc = cond == kX1 && (!lb || lbquad) && QMCCPW_PCA_X1_SMEMC;
     lb = lb && !lbquad;  // no per-warp staging
-    const bool warpsum = (cond == kW1 && QMCCPW_PCA_WARPSUM) || smemc || (cond == kX1 && lb && QMCCPW_LB_ROLLED);
+    const bool warpsum = (cond == kW1 && QMCCPW_PCA_WARPSUM) || smemc;
     size_t b = pca_stage_offset(warpsum ? 0 : a.n_opt * 8, a.d, (int)tpb);
     if (smemc) b += (size_t)(a.M_ld / 4) * tpb * sizeof(double);  // c_j [2 JT][tpb]
-    if (lb) b += tpb * a.d * sizeof(double) * (QMCCPW_LB_ROLLED ? 36 : 32) / 32;  // [nw][d][kSS] staging
-    if (lb && QMCCPW_LB_SMEM) b += 2 * a.d * sizeof(double) + (QMCCPW_LB_HULL ? tpb * a.d : 0);  // slopes, hulls
+    if (lb) b += tpb * a.d * sizeof(double);  // [nw][d][32] staging
     return b;
 }
 
