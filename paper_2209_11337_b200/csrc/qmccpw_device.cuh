@@ -789,6 +789,75 @@ __device__ __forceinline__ void x1_lookback_quad(const PathArgs& P, int o, int r
     f[3] = D * K * ph / (S0 * S0 * sg * __ldg(P.a + j0));
 }
 
+// STD-X1 streamed (equal slopes a_j = a): every strike's threshold, the arithmetic / binary sums
+// and the lookback's single top line follow from S = sum e^{c_j}, S_R = sum e^{c_j} R_j,
+// S_t = sum e^{c_j} t_j and the highest c_j (lowest j on ties), all accumulated while the path is
+// generated -- no per-date storage (the one-pass algebra of x1_solve's equal-slope branch; the
+// lookback's envelope is the single top line, x1_lookback's equal-slope branch)
+struct X1Stream {
+    double S, SR, St, cmax;
+    int jmax;
+    __device__ __forceinline__ void reset() {
+        S = 0.0; SR = 0.0; St = 0.0; cmax = -CUDART_INF; jmax = 0;
+    }
+    // date j (0-based): c = c_j, t = t_j = (j + 1) t_1, E = e^{c_j}
+    __device__ __forceinline__ void push(const PathArgs& P, int j, double c, double t, double E) {
+        S += E;
+        SR = fma(E, (c - P.lnS0 - P.omega * t) * P.inv_sigma, SR);
+        St = fma(E, t, St);
+        if (c > cmax) {
+            cmax = c;
+            jmax = j;
+        }
+    }
+};
+__device__ __forceinline__ void tail_x1_stream(const PathArgs& P, const X1Stream& st, double f[kMaxOpt][4]) {
+    const double sg = P.sigma, a = __ldg(P.a), isa = __ldg(P.inv_sa);
+    const double lnS = fast_log(st.S);
+    double h, hd;
+    fast_exp_x2(0.5 * sg * sg * a * a, 0.0, h, hd);
+#pragma unroll 1
+    for (int o = 0; o < P.n_opt; ++o) {
+        if (P.type[o] == kLookback) {
+            // envelope = line jmax from u* = (ln K - c_max) / (sigma a) on
+            const double ustar = (P.lnK[o] - st.cmax) * isa;
+            const double bact = sg * a, cact = st.cmax, aa = bact / sg;
+            const double tj = (double)(st.jmax + 1) * P.t1;
+            const double Rj = (cact - P.lnS0 - P.omega * tj) * P.inv_sigma;
+            const double w = fast_exp(fma(0.5 * bact, bact, cact));
+            double Qlo, Qhi, plo, phi_hi;
+            phibar_phi_x2(ustar - bact, 0.0, Qlo, Qhi, plo, phi_hi);
+            const double J = w * Qlo;
+            const double V = w * ((Rj - sg * tj + sg * aa * aa) * Qlo + aa * plo);
+            const double D = P.Dfac, S0 = P.S0, K = P.K[o];
+            double Qu, Q2, ph, ph2;
+            phibar_phi_x2(ustar, ustar, Qu, Q2, ph, ph2);
+            double fl[4] = {D * (J - K * Qu), D * J / S0, D * V, D * K * ph / (S0 * S0 * sg * a)};
+#pragma unroll
+            for (int o3 = 0; o3 < kMaxOpt; ++o3)
+                if (o3 == o)
+#pragma unroll
+                    for (int qq = 0; qq < 4; ++qq) f[o3][qq] = fl[qq];
+            continue;
+        }
+        if (P.tail_leader[o] != o) continue;
+        const double u_hi = (P.lndK[o] - st.cmax) * isa;
+        const double u = fmin((P.lndK[o] - lnS) / (sg * a), u_hi);
+        const double g = fast_exp(sg * a * u);
+        double sumW = 0.0, sumWv = 0.0;
+        if (P.x1_need_arith[o]) {
+            double Pf, Q2, p1, p2;
+            phibar_phi_x2(u - sg * a, u - sg * a, Pf, Q2, p1, p2);
+            sumW = h * Pf * st.S;
+            sumWv = h * Pf * (st.SR - sg * st.St + sg * a * a * st.S);
+        }
+        const X1Sums xs{u, a * g * st.S, a * a * g * st.S, g * (st.SR - sg * st.St + a * u * st.S), sumW, sumWv};
+#pragma unroll
+        for (int o2 = 0; o2 < kMaxOpt; ++o2)
+            if (o2 < P.n_opt && P.tail_leader[o2] == o) x1_outputs(P, o2, xs, f[o2]);
+    }
+}
+
 // all options of the launch: one Newton solve (and one set of E*-sums) per distinct strike
 __device__ __forceinline__ void tail_x1_all(const PathArgs& P, const double* cb, int stride, double f[kMaxOpt][4],
                                             unsigned& unconverged) {

@@ -25,6 +25,15 @@ namespace qmccpw {
 #ifndef QMCCPW_BB_GROUPED
 #define QMCCPW_BB_GROUPED 1
 #endif
+// STD-X1 streamed through one pass (X1Stream, no per-date storage)
+#ifndef QMCCPW_STD_X1_STREAM
+#define QMCCPW_STD_X1_STREAM 1
+#endif
+// A/B on one B200, C4 STD-X1 (ms/step, arithmetic + binary / with the lookback): per-date columns
+// 45.0 / 53.6; streamed at 4 / 6 / 8 blocks/SM 27.6 / 28.4, 27.9 / 28.7, 28.3 / 29.2
+#ifndef QMCCPW_STDX1_MINB
+#define QMCCPW_STDX1_MINB 4
+#endif
 // grouped bridge: exps of four dates at once (push4) and the rare single normals out of line
 // A/B on one B200, C4 BB-W1 (ms/step): neither 26.43, push4 26.90, out-of-line single normals
 // 26.07, both 26.40
@@ -50,6 +59,7 @@ namespace qmccpw {
 template <int CONSTR, int COND, int METHOD>
 constexpr int paths_min_blocks() {
     return (COND == kW1 && METHOD == kQmc) ? (CONSTR == kBB ? QMCCPW_BB_MINB : CONSTR == kStd ? QMCCPW_STD_MINB : 0)
+           : (COND == kX1 && METHOD == kQmc && CONSTR == kStd && QMCCPW_STD_X1_STREAM) ? QMCCPW_STDX1_MINB
            : (COND == kW1 && METHOD == kMcAv && CONSTR == kBB) ? QMCCPW_BBAV_MINB
                                                                 : 0;
 }
@@ -68,7 +78,9 @@ __global__ void __launch_bounds__(128, paths_min_blocks<CONSTR, COND, METHOD>())
     const uint64_t blk = cell % P.cells_per_rep;
     const uint64_t i0 = blk * (uint64_t)kCellPoints;
     const int ppt = kCellPoints >> tpb_log2;
-    constexpr bool kNeedBuf = (METHOD == kQmc) && (CONSTR == kPca || COND == kX1);
+    // STD-X1 streams its sums (X1Stream): no per-date c_j columns
+    constexpr bool kStdStream = (METHOD == kQmc) && CONSTR == kStd && COND == kX1 && QMCCPW_STD_X1_STREAM;
+    constexpr bool kNeedBuf = (METHOD == kQmc) && (CONSTR == kPca || COND == kX1) && !kStdStream;
     constexpr bool kTwoBuf = (METHOD == kQmc) && (CONSTR == kPca && COND == kX1);
     // X tile [M_ld][tpb + 8] in buf0 for the DMMA contraction: PCA-W1 always, PCA-X1 up to
     // d = 128 (beyond, the X tile and the c_j columns do not both fit: per-thread matvec)
@@ -518,7 +530,35 @@ __global__ void __launch_bounds__(128, paths_min_blocks<CONSTR, COND, METHOD>())
         } else {
             // X1: c_j = ln S0 + omega t_j + sigma R_j, R = M x with x_1 := 0
             double* cb = (CONSTR == kPca ? buf1 : buf0) + tid;
-            if (CONSTR == kStd) {
+            if (kStdStream) {
+                X1Stream xst;
+                xst.reset();
+                double R = 0.0;
+                {
+                    const double c0 = P.lnS0 + P.omega * P.t1, t0 = P.t1;
+                    xst.push(P, 0, c0, t0, fast_exp(c0));
+                }
+                int j = 1;
+#pragma unroll 1
+                for (; j + 1 < d; j += 2) {
+                    double xa, xb2;
+                    normal_from_u32_x2(sob.get(j), sob.get(j + 1), xa, xb2);
+                    R = fma(P.sqrt_t1, xa, R);
+                    const double ca = P.lnS0 + P.omega * (double)(j + 1) * P.t1 + P.sigma * R;
+                    R = fma(P.sqrt_t1, xb2, R);
+                    const double cb2 = P.lnS0 + P.omega * (double)(j + 2) * P.t1 + P.sigma * R;
+                    double Ea, Eb;
+                    fast_exp_x2(ca, cb2, Ea, Eb);
+                    xst.push(P, j, ca, (double)(j + 1) * P.t1, Ea);
+                    xst.push(P, j + 1, cb2, (double)(j + 2) * P.t1, Eb);
+                }
+                if (j < d) {
+                    R = fma(P.sqrt_t1, normal_from_u32(sob.get(j)), R);
+                    const double c = P.lnS0 + P.omega * (double)(j + 1) * P.t1 + P.sigma * R;
+                    xst.push(P, j, c, (double)(j + 1) * P.t1, fast_exp(c));
+                }
+                tail_x1_stream(P, xst, f);
+            } else if (CONSTR == kStd) {
                 double R = 0.0;
                 cb[0] = P.lnS0 + P.omega * P.t1;
                 int j = 1;
@@ -643,7 +683,7 @@ __global__ void __launch_bounds__(128, paths_min_blocks<CONSTR, COND, METHOD>())
                 __syncwarp();
 
             }
-            tail_x1_all(P, cb, tpb, f, unconverged);
+            if (!kStdStream) tail_x1_all(P, cb, tpb, f, unconverged);
         }
 
         if (!valid) {
@@ -670,7 +710,8 @@ __global__ void __launch_bounds__(128, paths_min_blocks<CONSTR, COND, METHOD>())
 
 static size_t path_smem_bytes(const PathArgs& a, int constr, int cond, int method) {
     const size_t tpb = (size_t)1 << a.tpb_log2, nw = tpb / 32;
-    const bool need_buf = method == kQmc && (constr == kPca || cond == kX1);
+    const bool need_buf = method == kQmc && (constr == kPca || cond == kX1) &&
+                          !(constr == kStd && cond == kX1 && QMCCPW_STD_X1_STREAM);
     const bool two_buf = method == kQmc && constr == kPca && cond == kX1;
     size_t b = 0;
     if (method == kQmc && constr == kPca && (cond == kW1 || a.M_ld <= 128))
