@@ -208,10 +208,14 @@ def test_path_values_pca_tile_edges(q, O, cond, d):
         _pv_check(q, O, otype, 100.0, d, 2, cond, 0, 1, 17, 17 + 301)
 
 
-@pytest.mark.parametrize("constr,cond", [(1, 0), (2, 0), (2, 1)])
+@pytest.mark.parametrize("constr,cond", [(1, 0), (2, 0), (2, 1), (0, 1), (1, 1)])
 def test_path_values_d256_and_other_markets(q, O, constr, cond):
-    _pv_check(q, O, 0, 100.0, 256, constr, cond, 0, 1, 0, 200)
+    # STD-X1 (streamed) and BB-X1 (bridge matrix on the tensor cores up to d = 128, the path
+    # kernel beyond) included: every option at d = 256, 128 and other markets
+    for otype in (0, 1, 2):
+        _pv_check(q, O, otype, 100.0, 256, constr, cond, 0, 1, 0, 200)
     _pv_check(q, O, 1, 70.0, 128, constr, cond, 0, 2, 50, 300, sigma=0.4, T=0.5, r=0.03)
+    _pv_check(q, O, 2, 120.0, 128, constr, cond, 0, 2, 50, 300, sigma=0.4, T=0.5, r=0.03)
     _pv_check(q, O, 0, 130.0, 32, constr, cond, 0, 0, 7, 400, sigma=0.1, T=2.0, S0=120.0)
 
 
@@ -276,16 +280,20 @@ def test_c4_fused_three_options_and_lr(q, O):
     _means_check(g, o)
 
 
-@pytest.mark.parametrize("constr", [1, 2])
+@pytest.mark.parametrize("constr", [0, 1, 2])
 def test_x1_deep_in_the_money_means(q, O, constr):
     # X1 at K = 90, all three options: the lookback gamma's mean (~1e-9) sits ~1e7 below its
     # pivot (the d = 1 Black-Scholes gamma ~1e-2), so the pivot-centred sums carry an absolute
     # rounding ~eps |p| (reading 30) -- the bound adds 1e-14 |p|
-    N, L, K = 2 * 4096 + 77, 4, 90.0
-    g = q.qmccpw_price_greeks_batch([0, 1, 2], [q.params(K=K, d=64)] * 3, N, L, qcfg(q, constr, 1))
-    o, _ = O.price_greeks([(t, K) for t in (0, 1, 2)], O.market(d=64), N, L, ocfg(O, constr, 1))
-    piv = [O.pivots(t, K, O.market(d=64)) for t in (0, 1, 2)]
-    _means_check(g, o, piv=piv)
+    N, L = 2 * 4096 + 77, 4
+    for K in (90.0, 100.0):
+        g = q.qmccpw_price_greeks_batch([0, 1, 2], [q.params(K=K, d=64)] * 3, N, L, qcfg(q, constr, 1))
+        o, _ = O.price_greeks([(t, K) for t in (0, 1, 2)], O.market(d=64), N, L, ocfg(O, constr, 1))
+        piv = [O.pivots(t, K, O.market(d=64)) for t in (0, 1, 2)]
+        _means_check(g, o, piv=piv)
+        # the lookback-free call takes another kernel for STD / BB (streamed / bridge on DMMA)
+        g2 = q.qmccpw_price_greeks_batch([0, 1], [q.params(K=K, d=64)] * 2, N, L, qcfg(q, constr, 1))
+        _means_check(g2, o[:2], piv=piv[:2])
 
 
 def test_edge_cases(q, O):
