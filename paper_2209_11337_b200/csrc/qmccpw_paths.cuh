@@ -25,6 +25,8 @@ namespace qmccpw {
 #ifndef QMCCPW_BB_GROUPED
 #define QMCCPW_BB_GROUPED 1
 #endif
+// (grouped bridge at d = 64 with the terminal and group 0's dynamic levels as one four-way
+// batch measured slower: 25.60 -> 26.42 ms, spills; removed)
 // STD-X1 streamed through one pass (X1Stream, no per-date storage)
 #ifndef QMCCPW_STD_X1_STREAM
 #define QMCCPW_STD_X1_STREAM 1
