@@ -42,6 +42,9 @@ namespace qmccpw {
 #endif
 // A/B on one B200, C4 PCA-X1 / BB-X1 (ms/step): rolled 91.5 / 91.5; unrolled by 2 90.5 / 90.5;
 // by 4 95.7 / 96.1
+#ifndef QMCCPW_LB_UNROLL
+#define QMCCPW_LB_UNROLL 1
+#endif
 #ifndef QMCCPW_X1_UNROLL
 #define QMCCPW_X1_UNROLL 2
 #endif
@@ -92,7 +95,7 @@ __global__ void __launch_bounds__(128, pca_min_blocks<COND, KF, LB>()) pca_kerne
     // c_j stay in the quad layout (shared memory, as kSmemC), no per-warp [d][32] staging
     constexpr bool kLbQuad = COND == kX1 && LB && QMCCPW_LB_QUAD && QMCCPW_PCA_X1_SMEMC;
     constexpr bool kSmemC = COND == kX1 && (!LB || kLbQuad) && QMCCPW_PCA_X1_SMEMC;
-    constexpr int kXU = kSmemC ? QMCCPW_X1_UNROLL : 2 * JT;  // unroll of the X1 per-date loops
+    constexpr int kXU = kSmemC ? (LB ? QMCCPW_LB_UNROLL : QMCCPW_X1_UNROLL) : 2 * JT;  // unroll of the X1 per-date loops
     constexpr bool kWarpSum = (COND == kW1 && QMCCPW_PCA_WARPSUM) || kSmemC;
     const int n_acc_smem = kWarpSum ? 0 : n_acc;  // smem accumulator rows
     // per-path accumulators in smem: X1 as scalars (one quad lane per path), W1 as (S1, S2) pairs
