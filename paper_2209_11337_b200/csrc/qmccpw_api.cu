@@ -443,6 +443,8 @@ PathArgs make_args(const Plan& pl, const Scratch& s) {
     a.s = p.sigma * a.sqrt_t1;
     a.inv_s = 1.0 / a.s;
     a.inv_sigma = 1.0 / p.sigma;
+    a.inv_S0 = 1.0 / p.S0;
+    a.inv_d = 1.0 / (double)d;
     a.Dfac = std::exp(-p.r * p.T);
     a.Afac = std::exp(p.r * (a.t1 - p.T));
     a.lnS0 = std::log(p.S0);

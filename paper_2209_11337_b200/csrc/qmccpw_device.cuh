@@ -285,14 +285,20 @@ struct NormalFifo {
 // launch at once.  Options with the same strike and statistic (the arithmetic
 // and binary Asians of C4) share psi, phi(psi), Phibar(psi), Phibar(psi - s):
 // P.tail_leader[o] names the first such option.
-__device__ __forceinline__ void tail_w1_all(const PathArgs& P, const W1Acc& acc, double f[kMaxOpt][4]) {
-    const double inv_d = 1.0 / (double)P.d;
-    const double SA = acc.sumS * inv_d, IA = acc.sumI * inv_d;
+// sink(o, f4) receives option o's four values (price, delta, vega, gamma) as soon as they
+// are formed, so a caller that reduces them at once keeps nothing per option live.
+// Divisions: 1/S0 and 1/d come precomputed; I/stat is y_max for the maximum statistic
+// (I_max = S_max y_max) and sumI/sumS for the average (the 1/d cancels); ln S_max =
+// ln S0 + e_max needs no logarithm.
+template <class Sink>
+__device__ __forceinline__ void tail_w1_each(const PathArgs& P, const W1Acc& acc, Sink&& sink) {
+    const double SA = acc.sumS * P.inv_d, IA = acc.sumI * P.inv_d;
     const double Smax = P.has_lookback ? acc.smax(P) : SA;
     const double Imax = Smax * acc.ymax;
-    double lnSA, lnSmax;
-    fast_log_x2(SA, Smax, lnSA, lnSmax);
+    const double lnSA = fast_log(SA);
+    const double lnSmax = P.lnS0 + acc.emax;
     double psi[kMaxOpt], Q0[kMaxOpt], Q1[kMaxOpt], ph[kMaxOpt];
+    const double D = P.Dfac, iS0 = P.inv_S0;
 #pragma unroll
     for (int o = 0; o < kMaxOpt; ++o) {
         if (o >= P.n_opt) break;
@@ -303,29 +309,39 @@ __device__ __forceinline__ void tail_w1_all(const PathArgs& P, const W1Acc& acc,
             double phs;
             phibar_phi_x2(psi[o], psi[o] - P.s, Q0[o], Q1[o], ph[o], phs);
         } else {
-            // leader index ld < o, resolved with selects (no dynamic register indexing)
-            psi[o] = ld == 0 ? psi[0] : psi[ld == 1 ? 1 : 0];
-            Q0[o] = ld == 0 ? Q0[0] : Q0[ld == 1 ? 1 : 0];
-            Q1[o] = ld == 0 ? Q1[0] : Q1[ld == 1 ? 1 : 0];
-            ph[o] = ld == 0 ? ph[0] : ph[ld == 1 ? 1 : 0];
+            // leader index ld < o (so ld is 0 or 1), resolved with selects between constant
+            // indices: an index expression here put these arrays in local memory
+            psi[o] = ld == 0 ? psi[0] : psi[1];
+            Q0[o] = ld == 0 ? Q0[0] : Q0[1];
+            Q1[o] = ld == 0 ? Q1[0] : Q1[1];
+            ph[o] = ld == 0 ? ph[0] : ph[1];
         }
         const double stat = lb ? Smax : SA;
-        const double I = lb ? Imax : IA;
-        const double K = P.K[o], D = P.Dfac, S0 = P.S0;
+        const double K = P.K[o];
+        double f4[4];
         if (P.type[o] == kBinary) {
-            f[o][0] = D * Q0[o];
-            f[o][1] = D * ph[o] * P.inv_s / S0;
-            f[o][2] = D * ph[o] * (I * P.inv_s / stat + psi[o] * P.inv_sigma - P.sqrt_t1);
-            f[o][3] = D * ph[o] * P.inv_s / (S0 * S0) * (psi[o] * P.inv_s - 1.0);
+            const double rat = lb ? acc.ymax : acc.sumI / acc.sumS;  // I / stat
+            const double Dph = D * ph[o];
+            f4[0] = D * Q0[o];
+            f4[1] = Dph * P.inv_s * iS0;
+            f4[2] = Dph * (rat * P.inv_s + psi[o] * P.inv_sigma - P.sqrt_t1);
+            f4[3] = Dph * P.inv_s * (iS0 * iS0) * (psi[o] * P.inv_s - 1.0);
         } else {
-            f[o][0] = P.Afac * stat * Q1[o] - D * K * Q0[o];
-            f[o][1] = P.Afac * (stat / S0) * Q1[o];
-            f[o][2] = P.Afac * Q1[o] * I + K * D * ph[o] * P.sqrt_t1;
-            f[o][3] = K * D * ph[o] * P.inv_s / (S0 * S0);
+            const double I = lb ? Imax : IA;
+            f4[0] = P.Afac * stat * Q1[o] - D * K * Q0[o];
+            f4[1] = P.Afac * (stat * iS0) * Q1[o];
+            f4[2] = P.Afac * Q1[o] * I + K * D * ph[o] * P.sqrt_t1;
+            f4[3] = K * D * ph[o] * P.inv_s * (iS0 * iS0);
         }
+        sink(o, f4);
     }
 }
-
+__device__ __forceinline__ void tail_w1_all(const PathArgs& P, const W1Acc& acc, double f[kMaxOpt][4]) {
+    tail_w1_each(P, acc, [&](int o, const double (&f4)[4]) {
+#pragma unroll
+        for (int q = 0; q < 4; ++q) f[o][q] = f4[q];
+    });
+}
 // (a6)+(a7) X1 mode: u* solves sum_j exp(c_j + sigma a_j u) = dK
 // by Newton from the AM-GM start, warp-uniform iteration count, clamped to the
 // bracket; then the conditional payoff and Greeks.  cb = per-thread c_j column.
@@ -874,7 +890,7 @@ __device__ __forceinline__ void tail_x1_all(const PathArgs& P, const double* cb,
         if (ld == o) {
             xs[o] = x1_solve(P, o, P.x1_need_arith[o] != 0, cb, stride, unconverged);
         } else {
-            xs[o] = ld == 0 ? xs[0] : xs[ld == 1 ? 1 : 0];
+            xs[o] = ld == 0 ? xs[0] : xs[1];
         }
         x1_outputs(P, o, xs[o], f[o]);
     }
@@ -964,6 +980,22 @@ __device__ __forceinline__ void warp_slot_sums(const double (&f)[kMaxOpt][4], co
         QMCCPW_CHECK(o * 8 + 7 < 32);
         warp_slot_sums_one(f[o], P.piv[o], valid, lane, wacc + o * 8);
     }
+}
+
+// the W1 tail reduced on the fly: option o's values go straight into the warp's slot sums
+// (and to the per-path hook), so no [option][Greek] array is held (it was kept in local
+// memory by the path kernels: 85 local loads/stores per path in BB-W1)
+__device__ __forceinline__ void tail_w1_reduce(const PathArgs& P, const W1Acc& acc, bool valid, int lane,
+                                               double* wacc, uint64_t i) {
+    tail_w1_each(P, acc, [&](int o, const double (&f4)[4]) {
+        if (P.path_out != nullptr && valid && o == P.hook_option)
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                QMCCPW_CHECK(i < P.n_points);
+                P.path_out[i * 4 + q] = f4[q];
+            }
+        warp_slot_sums_one(f4, P.piv[o], valid, lane, wacc + o * 8);
+    });
 }
 
 // per-thread (S1, S2) double2 accumulators in smem: cheaper in issue slots than the warp

@@ -74,6 +74,8 @@ struct PathArgs {
     double s;                // sigma sqrt(t1)
     double inv_s;            // 1/s
     double inv_sigma;
+    double inv_S0;           // 1/S0
+    double inv_d;            // 1/d
     double Dfac;             // e^{-rT}
     double Afac;             // e^{r(t1 - T)}
     double lnS0;

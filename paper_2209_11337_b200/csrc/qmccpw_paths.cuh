@@ -84,6 +84,8 @@ __global__ void __launch_bounds__(128, paths_min_blocks<CONSTR, COND, METHOD>())
     constexpr bool kStdStream = (METHOD == kQmc) && CONSTR == kStd && COND == kX1 && QMCCPW_STD_X1_STREAM;
     constexpr bool kNeedBuf = (METHOD == kQmc) && (CONSTR == kPca || COND == kX1) && !kStdStream;
     constexpr bool kTwoBuf = (METHOD == kQmc) && (CONSTR == kPca && COND == kX1);
+    // QMC W1 reduces each option's values as the tail forms them (tail_w1_reduce)
+    constexpr bool kFusedTail = (METHOD == kQmc) && COND == kW1;
     // X tile [M_ld][tpb + 8] in buf0 for the DMMA contraction: PCA-W1 always, PCA-X1 up to
     // d = 128 (beyond, the X tile and the c_j columns do not both fit: per-thread matvec)
     const bool kMmaX = (METHOD == kQmc) && CONSTR == kPca && (COND == kW1 || P.M_ld <= 128);
@@ -528,7 +530,7 @@ __global__ void __launch_bounds__(128, paths_min_blocks<CONSTR, COND, METHOD>())
                 }
             }
             if (P.has_lookback && w1.near_tie()) ++ties;
-            tail_w1_all(P, w1, f);
+            tail_w1_reduce(P, w1, valid, lane, wacc + (tid >> 5) * 32, i);  // kFusedTail
         } else {
             // X1: c_j = ln S0 + omega t_j + sigma R_j, R = M x with x_1 := 0
             double* cb = (CONSTR == kPca ? buf1 : buf0) + tid;
@@ -692,17 +694,19 @@ __global__ void __launch_bounds__(128, paths_min_blocks<CONSTR, COND, METHOD>())
             unconverged = unconverged0;
             ties = ties0;
         }
-        if (P.path_out != nullptr && valid) {
+        if (!kFusedTail) {
+            if (P.path_out != nullptr && valid) {
 #pragma unroll
-            for (int o = 0; o < kMaxOpt; ++o)
-                if (o == P.hook_option)
+                for (int o = 0; o < kMaxOpt; ++o)
+                    if (o == P.hook_option)
 #pragma unroll
-                    for (int q = 0; q < 4; ++q) {
-                        QMCCPW_CHECK(i < P.n_points);
-                        P.path_out[i * 4 + q] = f[o][q];
-                    }
+                        for (int q = 0; q < 4; ++q) {
+                            QMCCPW_CHECK(i < P.n_points);
+                            P.path_out[i * 4 + q] = f[o][q];
+                        }
+            }
+            warp_slot_sums(f, P, valid, lane, wacc + (tid >> 5) * 32);
         }
-        warp_slot_sums(f, P, valid, lane, wacc + (tid >> 5) * 32);
         (void)k;
     }
 

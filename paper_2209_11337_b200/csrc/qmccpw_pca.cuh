@@ -451,16 +451,19 @@ __global__ void __launch_bounds__(128, pca_min_blocks<COND, KF, LB>()) pca_kerne
             const bool valid = i < P.n_points;  // all lanes run: the warp reduction needs them
             npts += valid ? 1u : 0u;
             if (valid && P.has_lookback && w1.near_tie()) ++ties;
-            double f[kMaxOpt][4];
-            tail_w1_all(P, w1, f);
-            if (P.path_out != nullptr && valid) {
+            if (kWarpSum) {
+                tail_w1_reduce(P, w1, valid, lane, wacc + (tid >> 5) * 32, i);
+            } else {
+                double f[kMaxOpt][4];
+                tail_w1_all(P, w1, f);
+                if (P.path_out != nullptr && valid) {
 #pragma unroll
-                for (int o = 0; o < kMaxOpt; ++o)
-                    if (o == P.hook_option)
-                        for (int qq = 0; qq < 4; ++qq) P.path_out[i * 4 + qq] = f[o][qq];
+                    for (int o = 0; o < kMaxOpt; ++o)
+                        if (o == P.hook_option)
+                            for (int qq = 0; qq < 4; ++qq) P.path_out[i * 4 + qq] = f[o][qq];
+                }
+                thread_acc2(f, P, valid, acc2, tpb, tid);
             }
-            if (kWarpSum) warp_slot_sums(f, P, valid, lane, wacc + (tid >> 5) * 32);
-            else thread_acc2(f, P, valid, acc2, tpb, tid);
         }
     }
     if (COND == kW1 && !kWarpSum) acc2_to_wacc(P, acc2, wacc, tpb, tid);
