@@ -335,6 +335,7 @@ struct Scratch {
     uint32_t* vscr;
     uint32_t* shift;
     double* M;
+    double* Mf;  // M in pca_kernel's B-fragment order (launch_mma_bfrag)
     double* a;
     double* inv_sa;
     double* partials;
@@ -352,6 +353,7 @@ int carve(const Plan& pl, bool own_partials, uint32_t table_reps, Scratch* s, St
     size_t o_shift = off; off = align_up(off + (size_t)table_reps * d * 4);
     const int ld = (d + 7) & ~7;
     size_t o_M = off; off = align_up(off + (size_t)ld * ld * 8);
+    size_t o_Mf = off; off = align_up(off + (size_t)ld * ld * 8);
     size_t o_a = off; off = align_up(off + (size_t)d * 8);
     size_t o_isa = off; off = align_up(off + (size_t)d * 8);
     size_t o_part = off; off = align_up(off + (own_partials ? (size_t)pl.n_cells * pl.stride * 8 : 0));
@@ -365,6 +367,7 @@ int carve(const Plan& pl, bool own_partials, uint32_t table_reps, Scratch* s, St
     s->vscr = reinterpret_cast<uint32_t*>(b + o_vscr);
     s->shift = reinterpret_cast<uint32_t*>(b + o_shift);
     s->M = reinterpret_cast<double*>(b + o_M);
+    s->Mf = reinterpret_cast<double*>(b + o_Mf);
     s->a = reinterpret_cast<double*>(b + o_a);
     s->inv_sa = reinterpret_cast<double*>(b + o_isa);
     s->partials = own_partials ? reinterpret_cast<double*>(b + o_part) : nullptr;
@@ -414,6 +417,8 @@ int build_tables(DeviceCache* c, const Plan& pl, uint32_t rep_base, uint32_t tab
         CUDA_TRY(launch_gpca_rotate(s.M, (pl.d + 7) & ~7, pl.d, q.T, q.r - 0.5 * q.sigma * q.sigma, q.sigma, s.a,
                                     s.inv_sa, st));
     }
+    if (cfg.method == QMCCPW_QMC_CPW && !pl.portfolio && (cfg.construction == QMCCPW_PCA || bb_x1_on_mma(pl)))
+        CUDA_TRY(launch_mma_bfrag(s.M, (pl.d + 7) & ~7, s.Mf, st));
     return QMCCPW_OK;
 }
 
@@ -495,6 +500,7 @@ PathArgs make_args(const Plan& pl, const Scratch& s) {
     a.vscr = s.vscr;
     a.shift = s.shift;
     a.M = s.M;
+    a.Mf = s.Mf;
     a.M_ld = (d + 7) & ~7;
     a.a = s.a;
     a.inv_sa = s.inv_sa;

@@ -176,8 +176,19 @@ __global__ void __launch_bounds__(128, pca_min_blocks<COND, KF, LB>()) pca_kerne
                 const double a1 = (jb < d && !(COND == kX1 && jb == 0)) ? xb : 0.0;
 #pragma unroll
                 for (int jt = 0; jt < JT; ++jt) {
-                    const double* Mrow = P.M + (size_t)(8 * jt + q) * DP + r4 + 4 * f;
-                    const double b0 = __ldg(Mrow), b1 = __ldg(Mrow + 4);
+                    // M[8 jt + q][r4 + 4 f] and [.. + 4 (f + 1)], adjacent in the fragment order
+                    // (the lookback kernel keeps the two row-major loads: 194.5 vs 193.1 ms)
+                    double b0, b1;
+                    if (!LB) {
+                        const double2 bb = __ldg(reinterpret_cast<const double2*>(P.Mf) +
+                                                 ((size_t)(8 * jt + q) * (DP / 8) + (f >> 1)) * 4 + r4);
+                        b0 = bb.x;
+                        b1 = bb.y;
+                    } else {
+                        const double* Mrow = P.M + (size_t)(8 * jt + q) * DP + r4 + 4 * f;
+                        b0 = __ldg(Mrow);
+                        b1 = __ldg(Mrow + 4);
+                    }
                     asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
                                  : "+d"(cv[2 * jt]), "+d"(cv[2 * jt + 1])
                                  : "d"(a0), "d"(b0));

@@ -1,0 +1,9 @@
+#!/bin/bash
+# M in B-fragment order (one 16-byte load per two k-steps) and PCA-W1 at 7 blocks/SM: parity + A/B
+V=$PWD/paper_2209_11337_b200/build/var
+L=gpurun_out/r02ag.log; rm -f $L
+QMCCPW_LIB=$V/bf.so timeout 900 python -m pytest -q -x tests/test_gpu_parity.py tests/test_memory_safety.py tests/test_distributed_gpu.py -m gpu >> $L 2>&1; echo rc=$? >> $L
+for rep in 1 2; do for lib in ft bf bf7; do export QMCCPW_LIB=$V/$lib.so; echo "== $lib rep $rep" >> $L
+  for a in "--construction 2 --conditioning 0" "--construction 2 --conditioning 1" "--construction 1 --conditioning 1" "--construction 2 --conditioning 1 --options 0,1,2"; do
+    timeout 300 python bench.py --steps 5 --warmup 3 --no-cpu-baseline $a 2>/dev/null | python -c "import sys,json; [print('$a', json.loads(l)['ms_per_step']) for l in sys.stdin if l.startswith('{')]" >> $L
+  done; done; done
