@@ -450,6 +450,11 @@ PathArgs make_args(const Plan& pl, const Scratch& s) {
     a.inv_sigma = 1.0 / p.sigma;
     a.inv_S0 = 1.0 / p.S0;
     a.inv_d = 1.0 / (double)d;
+    a.S0_inv_d = p.S0 / (double)d;
+    for (int j = 0; j < kMaxDimGpu; ++j) {
+        const double t = (double)j * a.t1;
+        a.wt[j] = j < d ? make_double2(a.omega * t, p.sigma * t) : make_double2(0.0, 0.0);
+    }
     a.Dfac = std::exp(-p.r * p.T);
     a.Afac = std::exp(p.r * (a.t1 - p.T));
     a.lnS0 = std::log(p.S0);

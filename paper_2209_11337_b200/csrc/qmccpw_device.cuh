@@ -205,52 +205,33 @@ struct W1Acc {
         ymax = ym;
         tie = em - es < 1e-12;
     }
-    // date index j (0-based, t_{j+1} - t_1 = j dt), Wt = W~(t_{j+1} - t_1)
+    // date index j (0-based, t_{j+1} - t_1 = j dt), Wt = W~(t_{j+1} - t_1); P.wt[j] = (omega j dt,
+    // sigma j dt), read from the constant bank (j is warp-uniform in every caller).  The sums are
+    // kept without the factor S0 (S~_j = S0 X_j): sumS = sum_j X_j, sumI = sum_j X_j y_j; the
+    // tail scales by S0/d.
     __device__ __forceinline__ void push(const PathArgs& P, int j, double Wt) {
-        const double tt = (double)j * P.t1;
-        const double e = fma(P.sigma, Wt, P.omega * tt);
-        const double St = P.S0 * fast_exp(e);
-        const double y = fma(-P.sigma, tt, Wt);
-        sumS += St;
-        sumI = fma(St, y, sumI);
+        const double2 c = P.wt[j];
+        const double e = fma(P.sigma, Wt, c.x);
+        const double X = fast_exp(e);
+        const double y = Wt - c.y;
+        sumS += X;
+        sumI = fma(X, y, sumI);
         if (P.has_lookback) track(e, y);
     }
     // dates j and j+1 together (paired exp)
     __device__ __forceinline__ void push2(const PathArgs& P, int j, double Wa, double Wb) {
-        const double ta = (double)j * P.t1, tb = ta + P.t1;
-        const double ea = fma(P.sigma, Wa, P.omega * ta), eb = fma(P.sigma, Wb, P.omega * tb);
+        const double2 ca = P.wt[j], cb = P.wt[j + 1];
+        const double ea = fma(P.sigma, Wa, ca.x), eb = fma(P.sigma, Wb, cb.x);
         double Xa, Xb;
         fast_exp_x2(ea, eb, Xa, Xb);
-        const double Sa = P.S0 * Xa, Sb = P.S0 * Xb;
-        const double ya = fma(-P.sigma, ta, Wa), yb = fma(-P.sigma, tb, Wb);
-        sumS += Sa;
-        sumI = fma(Sa, ya, sumI);
-        sumS += Sb;
-        sumI = fma(Sb, yb, sumI);
+        const double ya = Wa - ca.y, yb = Wb - cb.y;
+        sumS += Xa;
+        sumI = fma(Xa, ya, sumI);
+        sumS += Xb;
+        sumI = fma(Xb, yb, sumI);
         if (P.has_lookback) {
             track(ea, ya);
             track(eb, yb);
-        }
-    }
-    // dates j .. j+3 together (four-way exp)
-    __device__ __forceinline__ void push4(const PathArgs& P, int j, double Wa, double Wb, double Wc, double Wd) {
-        const double W[4] = {Wa, Wb, Wc, Wd};
-        double e[4], X[4], t[4];
-        t[0] = (double)j * P.t1;  // the times exactly as two push2 calls form them
-        t[1] = t[0] + P.t1;
-        t[2] = (double)(j + 2) * P.t1;
-        t[3] = t[2] + P.t1;
-#pragma unroll
-        for (int i = 0; i < 4; ++i) e[i] = fma(P.sigma, W[i], P.omega * t[i]);
-        fast_exp_x4(e, X);
-#pragma unroll
-        for (int i = 0; i < 4; ++i) {
-            const double ti = t[i];
-            const double S = P.S0 * X[i];
-            const double y = fma(-P.sigma, ti, W[i]);
-            sumS += S;
-            sumI = fma(S, y, sumI);
-            if (P.has_lookback) track(e[i], y);
         }
     }
     // S~_max and I_max = S~_{j*} (W~_{j*} - sigma (t_{j*} - t_1)), rebuilt once per path
@@ -280,6 +261,15 @@ struct NormalFifo {
     }
 };
 
+// P.wt in shared memory, for callers whose date index varies across the warp (the PCA quad
+// layout): tt[j] = (omega t, sigma t) at t = j dt, j < d (t = t_{j+1} - t_1)
+__device__ __forceinline__ void date_table_fill(const PathArgs& P, double2* tt, int tid, int tpb) {
+    for (int j = tid; j < P.d; j += tpb) {
+        QMCCPW_CHK_SMEM(&tt[j]);
+        tt[j] = P.wt[j];
+    }
+}
+
 // (a6)+(a7) W1 threshold psi_d and the closed-form smoothed
 // payoff and Greeks (readings 1-5), all options of the
 // launch at once.  Options with the same strike and statistic (the arithmetic
@@ -292,7 +282,7 @@ struct NormalFifo {
 // ln S0 + e_max needs no logarithm.
 template <class Sink>
 __device__ __forceinline__ void tail_w1_each(const PathArgs& P, const W1Acc& acc, Sink&& sink) {
-    const double SA = acc.sumS * P.inv_d, IA = acc.sumI * P.inv_d;
+    const double SA = acc.sumS * P.S0_inv_d, IA = acc.sumI * P.S0_inv_d;  // sums without S0 (W1Acc)
     const double Smax = P.has_lookback ? acc.smax(P) : SA;
     const double Imax = Smax * acc.ymax;
     const double lnSA = fast_log(SA);

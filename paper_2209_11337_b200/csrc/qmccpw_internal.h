@@ -76,6 +76,8 @@ struct PathArgs {
     double inv_sigma;
     double inv_S0;           // 1/S0
     double inv_d;            // 1/d
+    double S0_inv_d;         // S0/d (the W1 sums are kept without S0)
+    double2 wt[kMaxDimGpu];  // (omega t, sigma t) at t = j dt = t_{j+1} - t_1, j < d (W1Acc)
     double Dfac;             // e^{-rT}
     double Afac;             // e^{r(t1 - T)}
     double lnS0;

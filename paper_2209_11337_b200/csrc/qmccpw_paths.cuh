@@ -470,7 +470,7 @@ __global__ void __launch_bounds__(128, paths_min_blocks<CONSTR, COND, METHOD>())
                         double Xa, Xb;
                         fast_exp_x2(ea, eb, Xa, Xb);
                         const double va = (j0 < d) ? 1.0 : 0.0, vb = (j0 + 1 < d) ? 1.0 : 0.0;
-                        const double Sa = P.S0 * Xa * va, Sb = P.S0 * Xb * vb;
+                        const double Sa = Xa * va, Sb = Xb * vb;  // W1Acc: sums without S0
                         const double ya = fma(-P.sigma, ta, Wa), yb = fma(-P.sigma, tb, Wb);
                         sS[rt] += Sa;
                         sI[rt] = fma(Sa, ya, sI[rt]);

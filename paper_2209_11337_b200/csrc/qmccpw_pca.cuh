@@ -65,7 +65,8 @@ constexpr int pca_min_blocks() {
 // byte offset of the X1 lookback staging: accs [n_acc][tpb] | vt, sh, G (+ pad) | HW / red
 __host__ __device__ __forceinline__ size_t pca_stage_offset(int n_acc, int d, int tpb) {
     const size_t nw = (size_t)tpb / 32;
-    size_t b = (size_t)n_acc * tpb * sizeof(double);
+    size_t b = (size_t)d * sizeof(double2);  // date table (date_table_fill)
+    b += (size_t)n_acc * tpb * sizeof(double);
     b += ((size_t)d * 32 * 2 + d) * sizeof(uint32_t) + 4;
     const size_t hw = (2 * 2 * nw * d + d) * sizeof(uint32_t), red = 4 * 32 * sizeof(double);
     b += hw > red ? hw : red;
@@ -99,8 +100,9 @@ __global__ void __launch_bounds__(128, pca_min_blocks<COND, KF, LB>()) pca_kerne
     constexpr bool kWarpSum = (COND == kW1 && QMCCPW_PCA_WARPSUM) || kSmemC;
     const int n_acc_smem = kWarpSum ? 0 : n_acc;  // smem accumulator rows
     // per-path accumulators in smem: X1 as scalars (one quad lane per path), W1 as (S1, S2) pairs
-    double* accs = reinterpret_cast<double*>(smem_raw);
-    double2* acc2 = reinterpret_cast<double2*>(smem_raw);
+    double2* tt = reinterpret_cast<double2*>(smem_raw);  // [d] date table (omega t, sigma t)
+    double* accs = reinterpret_cast<double*>(smem_raw + (size_t)d * sizeof(double2));
+    double2* acc2 = reinterpret_cast<double2*>(accs);
     uint32_t* vt = reinterpret_cast<uint32_t*>(accs + (size_t)n_acc_smem * tpb);
     uint32_t* sh = vt + (size_t)d * 32;
     uint32_t* G = sh + d;
@@ -118,6 +120,7 @@ __global__ void __launch_bounds__(128, pca_min_blocks<COND, KF, LB>()) pca_kerne
     const uint64_t Ab = K0 >> tpb_log2;
     {
         math_tables_load(tid, tpb);
+        if (COND == kW1) date_table_fill(P, tt, tid, tpb);
         const uint32_t* src = P.vscr + (size_t)rep_local * d * 32;
         QMCCPW_CHECK(rep_local < P.n_reps && cell < P.cell_end);
         for (int idx = tid; idx < d * 32; idx += tpb) {
@@ -204,12 +207,13 @@ __global__ void __launch_bounds__(128, pca_min_blocks<COND, KF, LB>()) pca_kerne
                 for (int jt = 0; jt < JT; ++jt) {
                     const int j0 = 8 * jt + 2 * r4;
                     const double Wa = cv[2 * jt] - W1v, Wb = cv[2 * jt + 1] - W1v;
-                    const double ta = (double)j0 * P.t1, tb = ta + P.t1;
-                    const double ea = fma(sg, Wa, P.omega * ta), eb = fma(sg, Wb, P.omega * tb);
+                    // (omega t, sigma t) of dates j0, j0 + 1 (rows past d read date 0: masked below)
+                    const double2 ca = tt[j0 < d ? j0 : 0], cb = tt[j0 + 1 < d ? j0 + 1 : 0];
+                    const double ea = fma(sg, Wa, ca.x), eb = fma(sg, Wb, cb.x);
                     double Xa, Xb;
                     fast_exp_x2(ea, eb, Xa, Xb);
-                    const double Sa = (j0 < d) ? P.S0 * Xa : 0.0, Sb = (j0 + 1 < d) ? P.S0 * Xb : 0.0;
-                    const double ya = fma(-sg, ta, Wa), yb = fma(-sg, tb, Wb);
+                    const double Sa = (j0 < d) ? Xa : 0.0, Sb = (j0 + 1 < d) ? Xb : 0.0;  // W1Acc: sums without S0
+                    const double ya = Wa - ca.y, yb = Wb - cb.y;
                     sS += Sa;
                     sI = fma(Sa, ya, sI);
                     sS += Sb;

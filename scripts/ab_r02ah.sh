@@ -1,0 +1,9 @@
+#!/bin/bash
+# W1 date table (omega t, sigma t) in shared memory and sums without S0: parity + A/B
+V=$PWD/paper_2209_11337_b200/build/var
+L=gpurun_out/r02ah.log; rm -f $L
+QMCCPW_LIB=$V/dt.so timeout 900 python -m pytest -q -x tests/ -m gpu >> $L 2>&1; echo rc=$? >> $L
+for rep in 1 2; do for lib in cur dt; do export QMCCPW_LIB=$V/$lib.so; echo "== $lib rep $rep" >> $L
+  for a in "--construction 1 --conditioning 0" "--construction 0 --conditioning 0" "--construction 2 --conditioning 0" "--method 3 --construction 1" "--method 2 --construction 0"; do
+    timeout 300 python bench.py --steps 5 --warmup 3 --no-cpu-baseline $a 2>/dev/null | python -c "import sys,json; [print('$a', json.loads(l)['ms_per_step']) for l in sys.stdin if l.startswith('{')]" >> $L
+  done; done; done
