@@ -63,9 +63,13 @@ constexpr int pca_min_blocks() {
                    : (LB ? (QMCCPW_LB_QUAD ? QMCCPW_LB_MINB : 2) : (COND == kW1 ? QMCCPW_PCA_W1_MINB : QMCCPW_PCA_X1_MINB));
 }
 // byte offset of the X1 lookback staging: accs [n_acc][tpb] | vt, sh, G (+ pad) | HW / red
-__host__ __device__ __forceinline__ size_t pca_stage_offset(int n_acc, int d, int tpb) {
+// W1 only: the date table (date_table_fill) first.  Not for X1: its 1 KB took PCA-X1 past the
+// 196 KiB shared-memory carveout at 5 blocks/SM (228 KiB: L1 hit rate 94 -> 76 %, PCA-X1
+// 87.8 -> 90.7 ms, the lookback 193 -> 203.5 ms)
+__host__ __device__ __forceinline__ size_t pca_date_table_bytes(bool w1, int d) { return w1 ? (size_t)d * 16 : 0; }
+__host__ __device__ __forceinline__ size_t pca_stage_offset(int n_acc, int d, int tpb, bool w1) {
     const size_t nw = (size_t)tpb / 32;
-    size_t b = (size_t)d * sizeof(double2);  // date table (date_table_fill)
+    size_t b = pca_date_table_bytes(w1, d);
     b += (size_t)n_acc * tpb * sizeof(double);
     b += ((size_t)d * 32 * 2 + d) * sizeof(uint32_t) + 4;
     const size_t hw = (2 * 2 * nw * d + d) * sizeof(uint32_t), red = 4 * 32 * sizeof(double);
@@ -101,7 +105,7 @@ __global__ void __launch_bounds__(128, pca_min_blocks<COND, KF, LB>()) pca_kerne
     const int n_acc_smem = kWarpSum ? 0 : n_acc;  // smem accumulator rows
     // per-path accumulators in smem: X1 as scalars (one quad lane per path), W1 as (S1, S2) pairs
     double2* tt = reinterpret_cast<double2*>(smem_raw);  // [d] date table (omega t, sigma t)
-    double* accs = reinterpret_cast<double*>(smem_raw + (size_t)d * sizeof(double2));
+    double* accs = reinterpret_cast<double*>(smem_raw + pca_date_table_bytes(COND == kW1, d));
     double2* acc2 = reinterpret_cast<double2*>(accs);
     uint32_t* vt = reinterpret_cast<uint32_t*>(accs + (size_t)n_acc_smem * tpb);
     uint32_t* sh = vt + (size_t)d * 32;
@@ -113,7 +117,7 @@ __global__ void __launch_bounds__(128, pca_min_blocks<COND, KF, LB>()) pca_kerne
     uint32_t* BS = HW + 2 * hw_size;  // [d] incremental Gray bases (sobol_build_hw_inc)
     // X1 with a lookback: c_j of the warp's 32 paths staged [d][32] per warp, so that each lane
     // walks the upper envelope of its own path (the quad layout holds a path over 4 lanes)
-    double* stage_base = reinterpret_cast<double*>(smem_raw + pca_stage_offset(n_acc_smem, d, tpb));
+    double* stage_base = reinterpret_cast<double*>(smem_raw + pca_stage_offset(n_acc_smem, d, tpb, COND == kW1));
     double* stage = stage_base + (size_t)(tid >> 5) * d * 32;
     double* cst = stage_base + tid;  // kSmemC: c_j of this lane at [v][tpb], v < 2 JT
     const uint64_t K0 = P.point_offset + i0;
@@ -492,7 +496,7 @@ static size_t pca_smem_bytes(const PathArgs& a, bool lb, int cond) {
     const bool smemc = cond == kX1 && (!lb || lbquad) && QMCCPW_PCA_X1_SMEMC;
     lb = lb && !lbquad;  // no per-warp staging
     const bool warpsum = (cond == kW1 && QMCCPW_PCA_WARPSUM) || smemc;
-    size_t b = pca_stage_offset(warpsum ? 0 : a.n_opt * 8, a.d, (int)tpb);
+    size_t b = pca_stage_offset(warpsum ? 0 : a.n_opt * 8, a.d, (int)tpb, cond == kW1);
     if (smemc) b += (size_t)(a.M_ld / 4) * tpb * sizeof(double);  // c_j [2 JT][tpb]
     if (lb) b += tpb * a.d * sizeof(double);  // [nw][d][32] staging
     return b;

@@ -1,5 +1,9 @@
 // qmccpw_pca_w1.cu -- PCA paths on DMMA tiles, W1 conditioning (d <= 128).
-#define QMCCPW_SMEM_TABLES 1  // exp / log tables in shared memory (see qmccpw_math.cuh)
+// exp / log tables in shared memory (see qmccpw_math.cuh)?
+#ifndef QMCCPW_PCA_W1_SMEM_TABLES
+#define QMCCPW_PCA_W1_SMEM_TABLES 1
+#endif
+#define QMCCPW_SMEM_TABLES QMCCPW_PCA_W1_SMEM_TABLES
 #include "qmccpw_pca.cuh"
 
 namespace qmccpw {
