@@ -111,7 +111,6 @@ __device__ __forceinline__ void sobol_build_hw_inc(const uint32_t* vt, const uin
         }
         const uint32_t b1 = b0 ^ sobol_base_step(v, p, A + 1);
         QMCCPW_CHK_SMEM(&BS[j]);
-        QMCCPW_CHK_SMEM(&v[31]);
         BS[j] = b1;
         const uint32_t v4 = v[4], v5 = v[5], v6 = v[6];
         for (int w = 0; w < nw; ++w) {

@@ -67,11 +67,18 @@ constexpr int pca_min_blocks() {
 // 196 KiB shared-memory carveout at 5 blocks/SM (228 KiB: L1 hit rate 94 -> 76 %, PCA-X1
 // 87.8 -> 90.7 ms, the lookback 193 -> 203.5 ms)
 __host__ __device__ __forceinline__ size_t pca_date_table_bytes(bool w1, int d) { return w1 ? (size_t)d * 16 : 0; }
+// QMCCPW_PCA_VT_GLOBAL: the replicate's scrambled direction numbers are read where they are
+// (global memory, L1) instead of a [d][32] shared copy: they are touched only by the table
+// builds (sobol_build_g once, ~4 words per dimension per 128 points in sobol_build_hw_inc), and
+// the 8 KB per block moves the PCA kernels to a smaller shared-memory carveout (more L1 for M)
+#ifndef QMCCPW_PCA_VT_GLOBAL
+#define QMCCPW_PCA_VT_GLOBAL 1
+#endif
 __host__ __device__ __forceinline__ size_t pca_stage_offset(int n_acc, int d, int tpb, bool w1) {
     const size_t nw = (size_t)tpb / 32;
     size_t b = pca_date_table_bytes(w1, d);
     b += (size_t)n_acc * tpb * sizeof(double);
-    b += ((size_t)d * 32 * 2 + d) * sizeof(uint32_t) + 4;
+    b += ((size_t)d * 32 * (QMCCPW_PCA_VT_GLOBAL ? 1 : 2) + d) * sizeof(uint32_t) + 4;
     const size_t hw = (2 * 2 * nw * d + d) * sizeof(uint32_t), red = 4 * 32 * sizeof(double);
     b += hw > red ? hw : red;
     return (b + 7) & ~(size_t)7;
@@ -107,8 +114,13 @@ __global__ void __launch_bounds__(128, pca_min_blocks<COND, KF, LB>()) pca_kerne
     double2* tt = reinterpret_cast<double2*>(smem_raw);  // [d] date table (omega t, sigma t)
     double* accs = reinterpret_cast<double*>(smem_raw + pca_date_table_bytes(COND == kW1, d));
     double2* acc2 = reinterpret_cast<double2*>(accs);
+#if QMCCPW_PCA_VT_GLOBAL
+    const uint32_t* vt = P.vscr + (size_t)rep_local * d * 32;
+    uint32_t* sh = reinterpret_cast<uint32_t*>(accs + (size_t)n_acc_smem * tpb);
+#else
     uint32_t* vt = reinterpret_cast<uint32_t*>(accs + (size_t)n_acc_smem * tpb);
     uint32_t* sh = vt + (size_t)d * 32;
+#endif
     uint32_t* G = sh + d;
     uint32_t* HW = G + (size_t)d * 32;
     HW += ((uintptr_t)HW & 7) ? 1 : 0;
@@ -125,12 +137,14 @@ __global__ void __launch_bounds__(128, pca_min_blocks<COND, KF, LB>()) pca_kerne
     {
         math_tables_load(tid, tpb);
         if (COND == kW1) date_table_fill(P, tt, tid, tpb);
-        const uint32_t* src = P.vscr + (size_t)rep_local * d * 32;
         QMCCPW_CHECK(rep_local < P.n_reps && cell < P.cell_end);
+#if !QMCCPW_PCA_VT_GLOBAL
+        const uint32_t* src = P.vscr + (size_t)rep_local * d * 32;
         for (int idx = tid; idx < d * 32; idx += tpb) {
             QMCCPW_CHK_SMEM(&vt[idx]);
             vt[idx] = src[idx];
         }
+#endif
         for (int idx = tid; idx < d; idx += tpb) {
             QMCCPW_CHK_SMEM(&sh[idx]);
             sh[idx] = P.shift[(size_t)rep_local * d + idx];
