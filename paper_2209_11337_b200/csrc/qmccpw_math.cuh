@@ -191,6 +191,12 @@ constexpr int kIcdfDeg = QMCCPW_ICDF_DEG;
 #error "QMCCPW_ICDF_DEG must be 22, 23 or 24"
 #endif
 
+// -r when the lattice point is in the upper half (y >= 2^31), else r: the sign bit of y moved into
+// r's sign bit (one integer op; the select form cost a DADD negation and two FSELs)
+__device__ __forceinline__ double mirror_upper(double r, uint32_t y) {
+    return __hiloint2double(__double2hiint(r) ^ (int)(y & 0x80000000u), __double2loint(r));
+}
+
 // (a3) lattice point -> standard normal, Phi^{-1}((y + 1/2) 2^-32).
 // Lower half (y < 2^31) evaluated, upper half mirrored (exact symmetry).
 // Giles' variable w = -ln(1 - z^2) = -ln(4u(1-u)), z = 2u - 1 (exact):
@@ -215,8 +221,7 @@ __device__ __forceinline__ double normal_from_u32(uint32_t y) {
 #pragma unroll
         for (int j = 23; j >= 0; --j) p = fma(p, v, ICDF_TAIL[j]);
     }
-    const double x = z * p;
-    return upper ? -x : x;
+    return mirror_upper(z * p, y);
 }
 
 // phi(x); flushes to 0 below e^-700 (|x| > 37.4), where fast_exp's exponent
@@ -301,8 +306,8 @@ __device__ __forceinline__ void normal_from_u32_x2(uint32_t ya, uint32_t yb, dou
     if (wa >= MC.w_split) pa = icdf_tail_poly(wa);  // u < 4.8e-4: rare, divergent
     if (wb >= MC.w_split) pb = icdf_tail_poly(wb);
     const double ra = za * pa, rb = zb * pb;
-    xa = upa ? -ra : ra;
-    xb = upb ? -rb : rb;
+    xa = mirror_upper(ra, ya);
+    xb = mirror_upper(rb, yb);
 }
 
 // one lattice point -> one normal, out of line: for the bridge's rare data-dependent levels
@@ -363,8 +368,7 @@ __device__ __forceinline__ void normal_from_u32_xn(const uint32_t (&y)[N], doubl
 #pragma unroll
     for (int i = 0; i < N; ++i) {
         if (w[i] >= MC.w_split) p[i] = icdf_tail_poly(w[i]);  // u < 4.8e-4: rare, divergent
-        const double r = z[i] * p[i];
-        x[i] = up[i] ? -r : r;
+        x[i] = mirror_upper(z[i] * p[i], y[i]);
     }
 }
 // four lattice points -> four standard normals: each coefficient loaded into a uniform register
