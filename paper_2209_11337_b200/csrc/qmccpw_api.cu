@@ -418,7 +418,7 @@ int build_tables(DeviceCache* c, const Plan& pl, uint32_t rep_base, uint32_t tab
                                     s.inv_sa, st));
     }
     if (cfg.method == QMCCPW_QMC_CPW && !pl.portfolio && (cfg.construction == QMCCPW_PCA || bb_x1_on_mma(pl)))
-        CUDA_TRY(launch_mma_bfrag(s.M, (pl.d + 7) & ~7, s.Mf, st));
+        CUDA_TRY(launch_mma_bfrag(s.M, (pl.d + 7) & ~7, cfg.conditioning == QMCCPW_COND_W1, s.Mf, st));
     return QMCCPW_OK;
 }
 

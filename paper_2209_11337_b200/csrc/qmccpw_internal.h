@@ -101,7 +101,7 @@ struct PathArgs {
     const uint32_t* vscr;    // [n_reps][d][32] scrambled direction numbers
     const uint32_t* shift;   // [n_reps][d]
     const double* M;         // [M_ld][M_ld] path matrix (PCA), zero-padded to a multiple of 8
-    const double* Mf;        // the same in pca_kernel's B-fragment order (launch_mma_bfrag)
+    const double* Mf;        // the same in pca_kernel's B-fragment order (launch_mma_bfrag); W1: rows minus row 0
     int M_ld;
     const double* a;         // [d] first column a_j of the path matrix (X1)
     const double* inv_sa;    // [d] 1/(sigma a_j)   (X1)
@@ -161,7 +161,7 @@ cudaError_t launch_randomization(const uint32_t* d_base_v, const uint32_t* d_bas
                                  cudaStream_t st);
 cudaError_t launch_path_matrix(int construction, int d, int ld, double T, double sigma, double* d_M, double* d_a,
                                double* d_inv_sa, cudaStream_t st);
-cudaError_t launch_mma_bfrag(const double* d_M, int ld, double* d_Mf, cudaStream_t st);
+cudaError_t launch_mma_bfrag(const double* d_M, int ld, bool shift_row0, double* d_Mf, cudaStream_t st);
 cudaError_t launch_gpca_rotate(double* d_M, int ld, int d, double T, double omega, double sigma, double* d_a,
                                double* d_inv_sa, cudaStream_t st);
 cudaError_t launch_paths_x1(const PathArgs& args, int construction, cudaStream_t st, int* smem_out);

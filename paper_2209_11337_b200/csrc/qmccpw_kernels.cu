@@ -145,18 +145,21 @@ __global__ void path_matrix_kernel(int construction, int d, int ld, double T, do
 // M (row-major [ld][ld]) in the order pca_kernel reads its m8n8k4 B fragments: lane (q, r4)
 // of a warp needs M[row][r4 + 4 f] and M[row][r4 + 4 (f + 1)] for each even k-step f, so
 // Mf[((row * ld/8) + f/2) * 8 + 2 r4 + e] = M[row][r4 + 4 (f + e)]: one 16-byte load per
-// pair of k-steps instead of two 8-byte loads.  A permutation: the values are M's bits.
-__global__ void mma_bfrag_kernel(const double* __restrict__ M, int ld, double* __restrict__ Mf) {
+// pair of k-steps instead of two 8-byte loads.  shift_row0 (W1): every row minus row 0, so the
+// contraction yields W~(t_j) = W(t_j) - W(t_1) directly (W1's increments) and the
+// kernel needs no per-date subtraction.
+__global__ void mma_bfrag_kernel(const double* __restrict__ M, int ld, int shift_row0, double* __restrict__ Mf) {
     const int idx = blockIdx.x * blockDim.x + threadIdx.x;
     if (idx >= ld * ld) return;
     const int row = idx / ld, rem = idx % ld;
     const int fp = rem >> 3, r4 = (rem & 7) >> 1, e = rem & 1;
-    Mf[idx] = M[(size_t)row * ld + r4 + 4 * (2 * fp + e)];
+    const int col = r4 + 4 * (2 * fp + e);
+    Mf[idx] = M[(size_t)row * ld + col] - (shift_row0 ? M[col] : 0.0);
 }
 
-cudaError_t launch_mma_bfrag(const double* d_M, int ld, double* d_Mf, cudaStream_t st) {
+cudaError_t launch_mma_bfrag(const double* d_M, int ld, bool shift_row0, double* d_Mf, cudaStream_t st) {
     const int n = ld * ld, tpb = 256;
-    mma_bfrag_kernel<<<(n + tpb - 1) / tpb, tpb, 0, st>>>(d_M, ld, d_Mf);
+    mma_bfrag_kernel<<<(n + tpb - 1) / tpb, tpb, 0, st>>>(d_M, ld, shift_row0 ? 1 : 0, d_Mf);
     ++launch_counter();
     return cudaGetLastError();
 }

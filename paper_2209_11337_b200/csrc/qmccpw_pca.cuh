@@ -187,7 +187,6 @@ __global__ void __launch_bounds__(128, pca_min_blocks<COND, KF, LB>()) pca_kerne
             double cv[2 * JT];  // W(t_j) (W1) or c_j (X1) at j = 8 jt + 2 r4 + e
 #pragma unroll
             for (int v = 0; v < 2 * JT; ++v) cv[v] = 0.0;
-            double W1v = 0.0;
 #pragma unroll 1
             for (int f = 0; f < KF; f += 2) {
                 const int ja = 4 * f + r4, jb = 4 * (f + 1) + r4;
@@ -219,12 +218,12 @@ __global__ void __launch_bounds__(128, pca_min_blocks<COND, KF, LB>()) pca_kerne
                 }
             }
             if (COND == kW1) {
-                W1v = __shfl_sync(0xffffffffu, cv[0], lane & ~3);  // W(t_1) of this path
+                // Mf's rows are M's minus row 0 (launch_mma_bfrag): cv holds W~(t_j) = W(t_j) - W(t_1)
                 double sS = 0.0, sI = 0.0, em = -CUDART_INF, es = -CUDART_INF, ym = 0.0;
 #pragma unroll
                 for (int jt = 0; jt < JT; ++jt) {
                     const int j0 = 8 * jt + 2 * r4;
-                    const double Wa = cv[2 * jt] - W1v, Wb = cv[2 * jt + 1] - W1v;
+                    const double Wa = cv[2 * jt], Wb = cv[2 * jt + 1];
                     // (omega t, sigma t) of dates j0, j0 + 1 (rows past d read date 0: masked below)
                     const double2 ca = tt[j0 < d ? j0 : 0], cb = tt[j0 + 1 < d ? j0 + 1 : 0];
                     const double ea = fma(sg, Wa, ca.x), eb = fma(sg, Wb, cb.x);
