@@ -7,6 +7,9 @@
 
 namespace qmccpw {
 
+#ifndef QMCCPW_BB_SHIFT_W1
+#define QMCCPW_BB_SHIFT_W1 1
+#endif
 #ifndef QMCCPW_BB_MINB
 #define QMCCPW_BB_MINB 8
 #endif
@@ -296,6 +299,7 @@ __global__ void __launch_bounds__(128, paths_min_blocks<CONSTR, COND, METHOD>())
                 int pos = 0;
                 stW[0] = P.sqrtT * NORMAL1(sob.get(pos++));  // terminal: W(T) = sqrt(T) x_0
                 double Wl = 0.0, W1 = 0.0;
+                (void)W1;
 #pragma unroll 1
                 for (int g = 0; g < (d >> 3); ++g) {
                     const int e0 = (g == 0) ? m : 2 + __ffs(g);
@@ -332,6 +336,31 @@ __global__ void __launch_bounds__(128, paths_min_blocks<CONSTR, COND, METHOD>())
                     x[6] = normal_from_u32(sob.get(pos + 6));
 #endif
                     pos += 7;
+#if QMCCPW_BB_SHIFT_W1
+                    double M4 = fma(b2, x4[0], 0.5 * (Wl + R));   // W(8g+4)
+                    double M2 = fma(b1, x4[1], 0.5 * (Wl + M4));  // W(8g+2)
+                    double Wa = fma(b0, x4[2], 0.5 * (Wl + M2));  // W(8g+1)
+                    // once W(t_1) is known (group 0), every live value -- the group's M4, M2, R and
+                    // the stack -- is shifted by it; the bridge is linear, so all later midpoints
+                    // come out as W~ = W - W(t_1) and W1's increments need no per-date subtraction
+                    const double shift = (g == 0) ? Wa : 0.0;
+                    if (g == 0) {
+#pragma unroll 1
+                        for (int i = 0; i <= sp; ++i) stW[i] -= shift;
+                    }
+                    M4 -= shift;
+                    M2 -= shift;
+                    R -= shift;
+                    Wa -= shift;
+                    const double W3 = fma(b0, x4[3], 0.5 * (M2 + M4));
+                    const double W6 = fma(b1, x[4], 0.5 * (M4 + R));
+                    const double W5 = fma(b0, x[5], 0.5 * (M4 + W6));
+                    const double W7 = fma(b0, x[6], 0.5 * (W6 + R));
+                    w1.push2(P, 8 * g, Wa, M2);
+                    w1.push2(P, 8 * g + 2, W3, M4);
+                    w1.push2(P, 8 * g + 4, W5, W6);
+                    w1.push2(P, 8 * g + 6, W7, R);
+#else
                     const double M4 = fma(b2, x4[0], 0.5 * (Wl + R));   // W(8g+4)
                     const double M2 = fma(b1, x4[1], 0.5 * (Wl + M4));  // W(8g+2)
                     const double Wa = fma(b0, x4[2], 0.5 * (Wl + M2));  // W(8g+1)
@@ -344,6 +373,7 @@ __global__ void __launch_bounds__(128, paths_min_blocks<CONSTR, COND, METHOD>())
                     w1.push2(P, 8 * g + 2, W3 - W1, M4 - W1);
                     w1.push2(P, 8 * g + 4, W5 - W1, W6 - W1);
                     w1.push2(P, 8 * g + 6, W7 - W1, R - W1);
+#endif
                     Wl = R;
                 }
             } else if (CONSTR == kBB) {
