@@ -65,20 +65,21 @@ def fp64_model_per_path(d, constr, cond, types, strikes):
     c_icdf = 50, c_exp = 17, c_tail = 160, c_W = 1 (STD) / 2 (BB) / d (PCA, GPCA).  d_icdf = d - 1
     where x_1 is not needed (STD-W1, every X1 mode), else d.  W1: n_solve = 0 (closed-form psi_d).
     X1 (reading 29): for each distinct-strike group of arithmetic / binary options one
-    threshold solve of 4 passes (SURVEY's count), 1 pass under STD (equal slopes: closed form);
-    a lookback under X1 (row f1) adds one envelope pass.  The per-date Phi-bar of the arithmetic
-    X1 sums (App. A.4) is NOT in 8(d)'s model and is not credited here."""
+    threshold solve of 4 passes (SURVEY's count); a lookback under X1 (row f1) adds one envelope
+    pass.  Under STD (equal slopes) the threshold is in closed form and the envelope is a single
+    line, both from the sums the path's own exponentials already give: no extra pass is charged.
+    The per-date Phi-bar of the arithmetic X1 sums (App. A.4) is NOT in 8(d)'s model and is not
+    credited here."""
     c_icdf, c_exp, c_tail = 50, 17, 160
     c_w = {0: 1, 1: 2, 2: d, 3: d}[constr]
     n_opt = len(types)
     d_icdf = d - 1 if (cond == 1 or constr == 0) else d
     w = d_icdf * c_icdf + d * (c_exp + c_w + 6) + n_opt * c_tail
-    if cond == 1:
-        passes = 1 if constr == 0 else 4
+    if cond == 1 and constr != 0:
         nonlb = [(t, K) for t, K in zip(types, strikes) if t != W.LOOKBACK]
         n_groups = len({K for _, K in nonlb})
         n_lb = sum(1 for t in types if t == W.LOOKBACK)
-        w += (n_groups * passes + n_lb) * d * (c_exp + 3)
+        w += (n_groups * 4 + n_lb) * d * (c_exp + 3)
     return w
 
 

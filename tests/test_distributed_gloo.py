@@ -202,3 +202,7 @@ def test_bench_work_model_follows_survey_8d():
     # two strikes under X1 -> two solves; same strike -> one
     two = bench.fp64_model_per_path(64, 2, 1, [0, 1], [95.0, 105.0])
     assert two - 14158 == 4 * 64 * 20
+    # STD-X1: closed-form threshold and a one-line envelope, no pass charged beyond the path's own
+    assert bench.fp64_model_per_path(64, 0, 1, C4, [100.0] * 3) == 63 * 50 + 64 * 24 + 3 * 160
+    # a lookback under PCA-X1 adds one envelope pass
+    assert bench.fp64_model_per_path(64, 2, 1, C4, [100.0] * 3) - 14158 == 64 * 20 + 160
