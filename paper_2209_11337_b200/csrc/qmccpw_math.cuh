@@ -145,8 +145,19 @@ __device__ __forceinline__ double rcp_newton(double y) {
 
 // ln(t) for normal t > 0 by table lookup: t = 2^k m, m in [1, 2), i = top 6 mantissa
 // bits, ln t = k ln2 + ln c_i + log1p(r), r = fma(m, 1/c_i, -1) (|r| <= 2^-7, one
-// rounding), log1p(r) = r + r^2 L(r).  ~10 FP64 ops and no MUFU against ~22 + a MUFU
+// rounding), log1p(r) = r + r^2 L(r).  QMCCPW_LOG1P_FACTORED (set by the W1 units): r (1 + r L(r))
+// added to ln c_i in one fma, two FP64 operations for r + r^2 L + ln c_i instead of three and one
+// rounding fewer (A/B: W1 modes -0.6 %, but C5 +2 % -- its constant-bank layout; off elsewhere).
+// ~10 FP64 ops and no MUFU against ~22 + a MUFU
 // for the atanh form; the 1 KB table is staged in shared memory (math_tables_load).
+#ifndef QMCCPW_LOG1P_FACTORED
+#define QMCCPW_LOG1P_FACTORED 0
+#endif
+#if QMCCPW_LOG1P_FACTORED
+#define LOG1P_PLUS(r, p, c) fma((r), fma((r), (p), MC.one), (c))
+#else
+#define LOG1P_PLUS(r, p, c) (fma((r) * (r), (p), (r)) + (c))
+#endif
 __device__ __forceinline__ void fast_log_x2(double ta, double tb, double& la, double& lb) {
     const int ha = __double2hiint(ta), hb = __double2hiint(tb);
     const double ma = __hiloint2double((ha & 0x000FFFFF) | 0x3FF00000, __double2loint(ta));
@@ -161,7 +172,7 @@ __device__ __forceinline__ void fast_log_x2(double ta, double tb, double& la, do
         pa = fma(pa, ra, LOG_P[j]);
         pb = fma(pb, rb, LOG_P[j]);
     }
-    const double sa = fma(ra * ra, pa, ra) + ca.y, sb = fma(rb * rb, pb, rb) + cb.y;
+    const double sa = LOG1P_PLUS(ra, pa, ca.y), sb = LOG1P_PLUS(rb, pb, cb.y);
     la = fma(ka, MC.ln2_hi, fma(ka, MC.ln2_lo, sa));
     lb = fma(kb, MC.ln2_hi, fma(kb, MC.ln2_lo, sb));
 }
@@ -175,7 +186,7 @@ __device__ __forceinline__ double fast_log(double t) {
     double p = LOG_P[kLogDeg];
 #pragma unroll
     for (int j = kLogDeg - 1; j >= 0; --j) p = fma(p, r, LOG_P[j]);
-    return fma(k, MC.ln2_hi, fma(k, MC.ln2_lo, fma(r * r, p, r) + c.y));
+    return fma(k, MC.ln2_hi, fma(k, MC.ln2_lo, LOG1P_PLUS(r, p, c.y)));
 }
 
 // degree of the central Phi^{-1} polynomial (fit_device_polys.py: max rel. error of the
@@ -343,7 +354,7 @@ __device__ __forceinline__ void fast_log_xn(const double (&t)[N], double (&l)[N]
         for (int i = 0; i < N; ++i) p[i] = fma(p[i], r[i], LOG_P[j]);
 #pragma unroll
     for (int i = 0; i < N; ++i) {
-        const double s = fma(r[i] * r[i], p[i], r[i]) + c[i].y;
+        const double s = LOG1P_PLUS(r[i], p[i], c[i].y);
         l[i] = fma(k[i], MC.ln2_hi, fma(k[i], MC.ln2_lo, s));
     }
 }

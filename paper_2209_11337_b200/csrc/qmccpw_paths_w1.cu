@@ -1,6 +1,7 @@
 // qmccpw_paths_w1.cu -- path kernels with W1 conditioning (all methods) and the
 // launch_paths dispatcher (X1 kernels: qmccpw_paths_x1.cu; PCA on DMMA: qmccpw_pca_*.cu).
 #define QMCCPW_SMEM_TABLES 1  // exp / log tables in shared memory (see qmccpw_math.cuh)
+#define QMCCPW_LOG1P_FACTORED 1  // (qmccpw_math.cuh fast_log)
 #include "qmccpw_paths.cuh"
 
 #ifndef QMCCPW_BB_X1_MMA

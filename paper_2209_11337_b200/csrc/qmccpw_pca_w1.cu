@@ -4,6 +4,7 @@
 #define QMCCPW_PCA_W1_SMEM_TABLES 1
 #endif
 #define QMCCPW_SMEM_TABLES QMCCPW_PCA_W1_SMEM_TABLES
+#define QMCCPW_LOG1P_FACTORED 1  // (qmccpw_math.cuh fast_log)
 #include "qmccpw_pca.cuh"
 
 namespace qmccpw {
