@@ -102,11 +102,25 @@ __shared__ double s_exp_tab[64];
 #define QMCCPW_LOG_TAB(i) __ldg(reinterpret_cast<const double2*>(LOG_TAB) + (i))
 #define QMCCPW_EXP_TAB(i) __ldg(EXP_TAB + (i))
 #endif
+// QMCCPW_ICDF_SHIFTED_LOG (W1 units, with the shared tables): the normals' logarithm returns
+// ln t + 3.125 directly -- a second table (1/c_i, ln c_i + 3.125) -- so the central polynomial's
+// variable v = -ln t - 3.125 is its negation (free in the DFMA) and the tail test w >= 6.25 is the
+// integer test hi(ln t + 3.125) >= hi(-3.125) on the sign-magnitude word (no DADD, no DSETP)
+#ifndef QMCCPW_ICDF_SHIFTED_LOG
+#define QMCCPW_ICDF_SHIFTED_LOG 0
+#endif
+#if QMCCPW_SMEM_TABLES && QMCCPW_ICDF_SHIFTED_LOG
+__shared__ double2 s_log_tab_c[64];
+#endif
 __device__ __forceinline__ void math_tables_load(int tid, int nthreads) {
 #if QMCCPW_SMEM_TABLES
     for (int i = tid; i < 64; i += nthreads) {
         s_log_tab[i] = __ldg(reinterpret_cast<const double2*>(LOG_TAB) + i);
         s_exp_tab[i] = __ldg(EXP_TAB + i);
+#if QMCCPW_ICDF_SHIFTED_LOG
+        const double2 c = __ldg(reinterpret_cast<const double2*>(LOG_TAB) + i);
+        s_log_tab_c[i] = make_double2(c.x, c.y + 3.125);
+#endif
     }
 #else
     (void)tid;
@@ -306,6 +320,10 @@ static __device__ __noinline__ double icdf_tail_poly(double w) {
 }
 
 // two lattice points -> two standard normals (same arithmetic as normal_from_u32)
+#ifndef QMCCPW_ICDF_SHIFTED_X2
+#define QMCCPW_ICDF_SHIFTED_X2 0
+#endif
+#if !(QMCCPW_SMEM_TABLES && QMCCPW_ICDF_SHIFTED_LOG && QMCCPW_ICDF_SHIFTED_X2)  // (else: the xn<2> form, below)
 __device__ __forceinline__ void normal_from_u32_x2(uint32_t ya, uint32_t yb, double& xa, double& xb) {
     const bool upa = (ya >> 31) != 0u, upb = (yb >> 31) != 0u;
     const uint32_t la = upa ? ~ya : ya, lb = upb ? ~yb : yb;
@@ -328,6 +346,7 @@ __device__ __forceinline__ void normal_from_u32_x2(uint32_t ya, uint32_t yb, dou
     xa = mirror_upper(ra, ya);
     xb = mirror_upper(rb, yb);
 }
+#endif
 
 // one lattice point -> one normal, out of line: for the bridge's rare data-dependent levels
 // (the terminal and the levels c >= 3 of each group's first descent), so that their copies
@@ -335,7 +354,8 @@ __device__ __forceinline__ void normal_from_u32_x2(uint32_t ya, uint32_t yb, dou
 static __device__ __noinline__ double normal_from_u32_call(uint32_t y) { return normal_from_u32(y); }
 
 // ln t for N arguments at once (same arithmetic as fast_log / fast_log_x2)
-template <int N>
+// SHIFTED (QMCCPW_ICDF_SHIFTED_LOG): l = ln t + 3.125
+template <int N, bool SHIFTED = false>
 __device__ __forceinline__ void fast_log_xn(const double (&t)[N], double (&l)[N]) {
     double m[N], k[N], r[N], p[N];
     double2 c[N];
@@ -344,7 +364,11 @@ __device__ __forceinline__ void fast_log_xn(const double (&t)[N], double (&l)[N]
         const int h = __double2hiint(t[i]);
         m[i] = __hiloint2double((h & 0x000FFFFF) | 0x3FF00000, __double2loint(t[i]));
         k[i] = (double)((h >> 20) - 1023);
+#if QMCCPW_SMEM_TABLES && QMCCPW_ICDF_SHIFTED_LOG
+        c[i] = SHIFTED ? s_log_tab_c[(h >> 14) & 63] : QMCCPW_LOG_TAB((h >> 14) & 63);
+#else
         c[i] = QMCCPW_LOG_TAB((h >> 14) & 63);
+#endif
         r[i] = fma(m[i], c[i].x, -MC.one);
         p[i] = LOG_P[kLogDeg];
     }
@@ -372,6 +396,25 @@ __device__ __forceinline__ void normal_from_u32_xn(const uint32_t (&y)[N], doubl
         z[i] = z_from_lower(l);
         t[i] = fma(-z[i], z[i], 1.0);
     }
+#if QMCCPW_SMEM_TABLES && QMCCPW_ICDF_SHIFTED_LOG
+    fast_log_xn<N, true>(t, w);  // w = ln t + 3.125 = -(v)
+#pragma unroll
+    for (int i = 0; i < N; ++i) {
+        v[i] = -w[i];
+        p[i] = ICDF_C[kIcdfDeg];
+    }
+#pragma unroll
+    for (int j = kIcdfDeg - 1; j >= 0; --j)
+#pragma unroll
+        for (int i = 0; i < N; ++i) p[i] = fma(p[i], v[i], ICDF_C[j]);
+#pragma unroll
+    for (int i = 0; i < N; ++i) {
+        // -ln t >= 6.25  <=>  ln t + 3.125 <= -3.125: the high word of a negative double grows
+        // with its magnitude, and -3.125's low word is zero
+        if ((uint32_t)__double2hiint(w[i]) >= 0xC0090000u) p[i] = icdf_tail_poly(3.125 - w[i]);
+        x[i] = mirror_upper(z[i] * p[i], y[i]);
+    }
+#else
     fast_log_xn<N>(t, w);
 #pragma unroll
     for (int i = 0; i < N; ++i) {
@@ -388,7 +431,18 @@ __device__ __forceinline__ void normal_from_u32_xn(const uint32_t (&y)[N], doubl
         if (w[i] >= MC.w_split) p[i] = icdf_tail_poly(w[i]);  // u < 4.8e-4: rare, divergent
         x[i] = mirror_upper(z[i] * p[i], y[i]);
     }
+#endif
 }
+#if QMCCPW_SMEM_TABLES && QMCCPW_ICDF_SHIFTED_LOG && QMCCPW_ICDF_SHIFTED_X2
+// (per unit: the PCA-W1 kernel gains with it, STD-W1 loses 7 % -- measured)
+__device__ __forceinline__ void normal_from_u32_x2(uint32_t ya, uint32_t yb, double& xa, double& xb) {
+    const uint32_t y[2] = {ya, yb};
+    double x[2];
+    normal_from_u32_xn<2>(y, x);
+    xa = x[0];
+    xb = x[1];
+}
+#endif
 // four lattice points -> four standard normals: each coefficient loaded into a uniform register
 // feeds four DFMAs (half the constant-load instructions per normal of the paired form)
 __device__ __forceinline__ void normal_from_u32_x4(const uint32_t (&y)[4], double (&x)[4]) {

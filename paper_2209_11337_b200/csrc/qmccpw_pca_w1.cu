@@ -5,6 +5,12 @@
 #endif
 #define QMCCPW_SMEM_TABLES QMCCPW_PCA_W1_SMEM_TABLES
 #define QMCCPW_LOG1P_FACTORED 1  // (qmccpw_math.cuh fast_log)
+#ifndef QMCCPW_ICDF_SHIFTED_LOG
+#define QMCCPW_ICDF_SHIFTED_LOG 1  // (qmccpw_math.cuh normal_from_u32_xn)
+#endif
+#ifndef QMCCPW_ICDF_SHIFTED_X2
+#define QMCCPW_ICDF_SHIFTED_X2 1  // the paired normals too
+#endif
 #include "qmccpw_pca.cuh"
 
 namespace qmccpw {
