@@ -7,6 +7,9 @@
 
 namespace qmccpw {
 
+#ifndef QMCCPW_STD_X4
+#define QMCCPW_STD_X4 1
+#endif
 #ifndef QMCCPW_BB_SHIFT_W1
 #define QMCCPW_BB_SHIFT_W1 1
 #endif
@@ -270,6 +273,21 @@ __global__ void __launch_bounds__(128, paths_min_blocks<CONSTR, COND, METHOD>())
                 double Wt = 0.0;
                 w1.push(P, 0, 0.0);
                 int j = 1;
+#if QMCCPW_STD_X4
+                // four dates per step: the normals as four interleaved chains (as BB-W1's groups)
+#pragma unroll 1
+                for (; j + 3 < d; j += 4) {
+                    const uint32_t y4[4] = {sob.get(j), sob.get(j + 1), sob.get(j + 2), sob.get(j + 3)};
+                    double x4[4];
+                    normal_from_u32_x4(y4, x4);
+                    const double Wa = fma(P.sqrt_t1, x4[0], Wt);
+                    const double Wb = fma(P.sqrt_t1, x4[1], Wa);
+                    const double Wc = fma(P.sqrt_t1, x4[2], Wb);
+                    Wt = fma(P.sqrt_t1, x4[3], Wc);
+                    w1.push2(P, j, Wa, Wb);
+                    w1.push2(P, j + 2, Wc, Wt);
+                }
+#endif
 #pragma unroll 1
                 for (; j + 1 < d; j += 2) {
                     double xa, xb;
