@@ -93,15 +93,40 @@ __device__ __forceinline__ void philox4x32_10(uint32_t c[4], uint32_t k0, uint32
 #ifndef QMCCPW_SMEM_TABLES
 #define QMCCPW_SMEM_TABLES 0
 #endif
+// QMCCPW_EXP256 (W1 units, with the shared tables): exp from a 256-entry 2^(j/256) table and a
+// degree-4 polynomial on |r| <= ln2/512 -- the same 2.4e-18 fit error as the 64-entry table's
+// degree 5, one DFMA fewer per exponential; 2 KB of shared memory instead of 0.5 KB
+#ifndef QMCCPW_EXP256
+#define QMCCPW_EXP256 0
+#endif
+#define QMCCPW_EXP256_ON (QMCCPW_EXP256 && QMCCPW_SMEM_TABLES)
 #if QMCCPW_SMEM_TABLES
 __shared__ double2 s_log_tab[64];
+#if QMCCPW_EXP256_ON
+__shared__ double s_exp_tab[256];
+#else
 __shared__ double s_exp_tab[64];
+#endif
 #define QMCCPW_LOG_TAB(i) s_log_tab[i]
 #define QMCCPW_EXP_TAB(i) s_exp_tab[i]
 #else
 #define QMCCPW_LOG_TAB(i) __ldg(reinterpret_cast<const double2*>(LOG_TAB) + (i))
 #define QMCCPW_EXP_TAB(i) __ldg(EXP_TAB + (i))
 #endif
+#if QMCCPW_EXP256_ON
+constexpr int kExpBits = 8, kExpDegK = 4;
+#define EXP_PK EXP256_POLY_D4
+#define EXP_INV_LN2K (4.0 * EXP64_INV_LN2)   // 256/ln2 (exact power-of-two scalings of the
+#define EXP_LN2_HIK (0.25 * EXP64_LN2_HI)    // 64-entry table's constants)
+#define EXP_LN2_LOK (0.25 * EXP64_LN2_LO)
+#else
+constexpr int kExpBits = 6, kExpDegK = kExpDeg;
+#define EXP_PK EXP_P
+#define EXP_INV_LN2K MC.e64_inv_ln2
+#define EXP_LN2_HIK MC.e64_ln2_hi
+#define EXP_LN2_LOK MC.e64_ln2_lo
+#endif
+constexpr int kExpMask = (1 << kExpBits) - 1;
 // QMCCPW_ICDF_SHIFTED_LOG (W1 units, with the shared tables): the normals' logarithm returns
 // ln t + 3.125 directly -- a second table (1/c_i, ln c_i + 3.125) -- so the central polynomial's
 // variable v = -ln t - 3.125 is its negation (free in the DFMA) and the tail test w >= 6.25 is the
@@ -114,9 +139,14 @@ __shared__ double2 s_log_tab_c[64];
 #endif
 __device__ __forceinline__ void math_tables_load(int tid, int nthreads) {
 #if QMCCPW_SMEM_TABLES
+#if QMCCPW_EXP256_ON
+    for (int i = tid; i < 256; i += nthreads) s_exp_tab[i] = __ldg(EXP_TAB256 + i);
+#endif
     for (int i = tid; i < 64; i += nthreads) {
         s_log_tab[i] = __ldg(reinterpret_cast<const double2*>(LOG_TAB) + i);
+#if !QMCCPW_EXP256_ON
         s_exp_tab[i] = __ldg(EXP_TAB + i);
+#endif
 #if QMCCPW_ICDF_SHIFTED_LOG
         const double2 c = __ldg(reinterpret_cast<const double2*>(LOG_TAB) + i);
         s_log_tab_c[i] = make_double2(c.x, c.y + 3.125);
@@ -134,17 +164,17 @@ __device__ __forceinline__ void math_tables_load(int tid, int nthreads) {
 // polynomial (rel. error 3.4e-21 before rounding); 2^k added to the exponent field.
 // 7 coefficients instead of 13: ~40 % fewer FP64 operations than a |r| <= ln2/2 form.
 __device__ __forceinline__ double fast_exp(double x) {
-    const double t = fma(x, MC.e64_inv_ln2, MC.shift);
+    const double t = fma(x, EXP_INV_LN2K, MC.shift);
     const int ni = __double2loint(t);
     const double n = t - MC.shift;
-    double r = fma(n, -MC.e64_ln2_hi, x);
-    r = fma(n, -MC.e64_ln2_lo, r);
-    const double T = QMCCPW_EXP_TAB(ni & 63);
-    double p = EXP_P[kExpDeg];
+    double r = fma(n, -EXP_LN2_HIK, x);
+    r = fma(n, -EXP_LN2_LOK, r);
+    const double T = QMCCPW_EXP_TAB(ni & kExpMask);
+    double p = EXP_PK[kExpDegK];
 #pragma unroll
-    for (int j = kExpDeg - 1; j >= 0; --j) p = fma(p, r, EXP_P[j]);
+    for (int j = kExpDegK - 1; j >= 0; --j) p = fma(p, r, EXP_PK[j]);
     p *= T;
-    return __hiloint2double(__double2hiint(p) + ((ni >> 6) << 20), __double2loint(p));
+    return __hiloint2double(__double2hiint(p) + ((ni >> kExpBits) << 20), __double2loint(p));
 }
 
 // 1/y for y in [1, 4): FP64 MUFU seed + two Newton steps
@@ -264,23 +294,23 @@ __device__ __forceinline__ double normal_from_u32(uint32_t y) {
 // coefficient loaded into a uniform register feeds two DFMAs and the two Horner
 // chains hide each other's latency ------------------------------------------
 __device__ __forceinline__ void fast_exp_x2(double xa, double xb, double& ra, double& rb) {
-    const double ta = fma(xa, MC.e64_inv_ln2, MC.shift), tb = fma(xb, MC.e64_inv_ln2, MC.shift);
+    const double ta = fma(xa, EXP_INV_LN2K, MC.shift), tb = fma(xb, EXP_INV_LN2K, MC.shift);
     const int na = __double2loint(ta), nb = __double2loint(tb);
-    const double Ta = QMCCPW_EXP_TAB(na & 63), Tb = QMCCPW_EXP_TAB(nb & 63);
+    const double Ta = QMCCPW_EXP_TAB(na & kExpMask), Tb = QMCCPW_EXP_TAB(nb & kExpMask);
     const double fa = ta - MC.shift, fb = tb - MC.shift;
-    double qa = fma(fa, -MC.e64_ln2_hi, xa), qb = fma(fb, -MC.e64_ln2_hi, xb);
-    qa = fma(fa, -MC.e64_ln2_lo, qa);
-    qb = fma(fb, -MC.e64_ln2_lo, qb);
-    double pa = EXP_P[kExpDeg], pb = EXP_P[kExpDeg];
+    double qa = fma(fa, -EXP_LN2_HIK, xa), qb = fma(fb, -EXP_LN2_HIK, xb);
+    qa = fma(fa, -EXP_LN2_LOK, qa);
+    qb = fma(fb, -EXP_LN2_LOK, qb);
+    double pa = EXP_PK[kExpDegK], pb = EXP_PK[kExpDegK];
 #pragma unroll
-    for (int j = kExpDeg - 1; j >= 0; --j) {
-        pa = fma(pa, qa, EXP_P[j]);
-        pb = fma(pb, qb, EXP_P[j]);
+    for (int j = kExpDegK - 1; j >= 0; --j) {
+        pa = fma(pa, qa, EXP_PK[j]);
+        pb = fma(pb, qb, EXP_PK[j]);
     }
     pa *= Ta;
     pb *= Tb;
-    ra = __hiloint2double(__double2hiint(pa) + ((na >> 6) << 20), __double2loint(pa));
-    rb = __hiloint2double(__double2hiint(pb) + ((nb >> 6) << 20), __double2loint(pb));
+    ra = __hiloint2double(__double2hiint(pa) + ((na >> kExpBits) << 20), __double2loint(pa));
+    rb = __hiloint2double(__double2hiint(pb) + ((nb >> kExpBits) << 20), __double2loint(pb));
 }
 
 // four exponentials with interleaved Horner chains (one coefficient load per four DFMAs)
@@ -289,25 +319,25 @@ __device__ __forceinline__ void fast_exp_x4(const double (&x)[4], double (&r)[4]
     int n[4];
 #pragma unroll
     for (int i = 0; i < 4; ++i) {
-        t[i] = fma(x[i], MC.e64_inv_ln2, MC.shift);
+        t[i] = fma(x[i], EXP_INV_LN2K, MC.shift);
         n[i] = __double2loint(t[i]);
-        T[i] = QMCCPW_EXP_TAB(n[i] & 63);
+        T[i] = QMCCPW_EXP_TAB(n[i] & kExpMask);
         f[i] = t[i] - MC.shift;
-        q[i] = fma(f[i], -MC.e64_ln2_hi, x[i]);
+        q[i] = fma(f[i], -EXP_LN2_HIK, x[i]);
     }
 #pragma unroll
     for (int i = 0; i < 4; ++i) {
-        q[i] = fma(f[i], -MC.e64_ln2_lo, q[i]);
-        p[i] = EXP_P[kExpDeg];
+        q[i] = fma(f[i], -EXP_LN2_LOK, q[i]);
+        p[i] = EXP_PK[kExpDegK];
     }
 #pragma unroll
-    for (int j = kExpDeg - 1; j >= 0; --j)
+    for (int j = kExpDegK - 1; j >= 0; --j)
 #pragma unroll
-        for (int i = 0; i < 4; ++i) p[i] = fma(p[i], q[i], EXP_P[j]);
+        for (int i = 0; i < 4; ++i) p[i] = fma(p[i], q[i], EXP_PK[j]);
 #pragma unroll
     for (int i = 0; i < 4; ++i) {
         p[i] *= T[i];
-        r[i] = __hiloint2double(__double2hiint(p[i]) + ((n[i] >> 6) << 20), __double2loint(p[i]));
+        r[i] = __hiloint2double(__double2hiint(p[i]) + ((n[i] >> kExpBits) << 20), __double2loint(p[i]));
     }
 }
 

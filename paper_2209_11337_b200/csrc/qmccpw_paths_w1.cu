@@ -2,6 +2,9 @@
 // launch_paths dispatcher (X1 kernels: qmccpw_paths_x1.cu; PCA on DMMA: qmccpw_pca_*.cu).
 #define QMCCPW_SMEM_TABLES 1  // exp / log tables in shared memory (see qmccpw_math.cuh)
 #define QMCCPW_LOG1P_FACTORED 1  // (qmccpw_math.cuh fast_log)
+#ifndef QMCCPW_EXP256
+#define QMCCPW_EXP256 1  // (qmccpw_math.cuh fast_exp: 256-entry table, degree 4)
+#endif
 #ifndef QMCCPW_ICDF_SHIFTED_LOG
 #define QMCCPW_ICDF_SHIFTED_LOG 1  // (qmccpw_math.cuh normal_from_u32_xn)
 #endif

@@ -5,6 +5,9 @@
 #endif
 #define QMCCPW_SMEM_TABLES QMCCPW_PCA_W1_SMEM_TABLES
 #define QMCCPW_LOG1P_FACTORED 1  // (qmccpw_math.cuh fast_log)
+#ifndef QMCCPW_EXP256
+#define QMCCPW_EXP256 1  // (qmccpw_math.cuh fast_exp: 256-entry table, degree 4)
+#endif
 #ifndef QMCCPW_ICDF_SHIFTED_LOG
 #define QMCCPW_ICDF_SHIFTED_LOG 1  // (qmccpw_math.cuh normal_from_u32_xn)
 #endif
