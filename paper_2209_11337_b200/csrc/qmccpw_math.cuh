@@ -100,6 +100,8 @@ __device__ __forceinline__ void philox4x32_10(uint32_t c[4], uint32_t k0, uint32
 #define QMCCPW_EXP256 0
 #endif
 #define QMCCPW_EXP256_ON (QMCCPW_EXP256 && QMCCPW_SMEM_TABLES)
+// (units without the shared tables read the 256-entry table through L1: QMCCPW_EXP256_L1)
+#define QMCCPW_EXP256_L1 (QMCCPW_EXP256 && !QMCCPW_SMEM_TABLES)
 #if QMCCPW_SMEM_TABLES
 __shared__ double2 s_log_tab[64];
 #if QMCCPW_EXP256_ON
@@ -111,9 +113,13 @@ __shared__ double s_exp_tab[64];
 #define QMCCPW_EXP_TAB(i) s_exp_tab[i]
 #else
 #define QMCCPW_LOG_TAB(i) __ldg(reinterpret_cast<const double2*>(LOG_TAB) + (i))
+#if QMCCPW_EXP256_L1
+#define QMCCPW_EXP_TAB(i) __ldg(EXP_TAB256 + (i))
+#else
 #define QMCCPW_EXP_TAB(i) __ldg(EXP_TAB + (i))
 #endif
-#if QMCCPW_EXP256_ON
+#endif
+#if QMCCPW_EXP256_ON || QMCCPW_EXP256_L1
 constexpr int kExpBits = 8, kExpDegK = 4;
 #define EXP_PK EXP256_POLY_D4
 #define EXP_INV_LN2K (4.0 * EXP64_INV_LN2)   // 256/ln2 (exact power-of-two scalings of the
